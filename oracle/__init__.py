@@ -1,0 +1,454 @@
+"""CPU oracle for the meshfree ALE BGK step (arXiv 2408.02350) -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2408_02350_b200``) never imports it and shares no code with it; the
+only shared module is ``bgk_inputs`` (seeded input generators, no method
+arithmetic).
+
+The arithmetic lives in ``bgk_oracle.c`` (plain fp64 loops, -O2
+-ffp-contract=off, each function citing PAPER.md).  This file is ctypes
+marshalling plus two drivers built only from the C primitives:
+``run_steps`` (whole cloud) and ``sampled_first_step`` (one step at a handful of
+particles of a cloud too large to materialise, used for full-size sampled
+parity and for the bounded CPU baseline).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "bgk_oracle.c")
+_LIB = os.path.join(_HERE, "libbgk_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OR_OK, OR_E_INVALID, OR_E_CAPACITY, OR_E_DEFICIENT, OR_E_DEGENERATE, OR_E_WALL = range(6)
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle shared library (gcc, -O2 -ffp-contract=off, OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+               "-shared", "-o", _LIB, _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+class OrCfg(C.Structure):
+    _fields_ = [("dims", C.c_int32), ("Nv", C.c_int32), ("vmax", C.c_double), ("L", C.c_double),
+                ("h", C.c_double), ("h2", C.c_double), ("alpha_w", C.c_double), ("dt", C.c_double),
+                ("R", C.c_double), ("kb", C.c_double), ("dmol", C.c_double), ("Twall", C.c_double),
+                ("Ulid", C.c_double * 3), ("dx", C.c_double), ("ale", C.c_int32), ("pad", C.c_int32)]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_D = C.c_double
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = C.CDLL(_LIB)
+            sig = {
+                "or_dv": (_D, [_P]),
+                "or_axis_node": (_D, [_P, C.c_int]),
+                "or_num_nodes": (_I64, [_P]),
+                "or_node_velocity": (None, [_P, _I64, _P]),
+                "or_neighbors_of": (_I64, [C.c_int, _P, _I64, _D, _I64, _P, _I64]),
+                "or_neighbors": (C.c_int, [C.c_int, _P, _I64, _D, _P, _P, _I64, _P]),
+                "or_sym_eigenvalues": (None, [C.c_int, _P, _P]),
+                "or_weight": (_D, [_D, _D, _D]),
+                "or_wls_one": (C.c_int, [C.c_int, _P, _I64, C.c_int, _P, _D, _D, _P, _P]),
+                "or_frame": (None, [C.c_int, _P, _P]),
+                "or_rotate": (None, [C.c_int, _P, _P, _P]),
+                "or_wls_all": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P]),
+                "or_transport_one": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _I64, _I64]),
+                "or_coef_absmax_one": (_D, [_P, _P, C.c_int, _P, _P]),
+                "or_moments_row": (C.c_int, [_P, _P, _P]),
+                "or_tau": (_D, [_P, _D, _D, _P]),
+                "or_maxwellian_row": (None, [_P, _D, _P, _D, _P]),
+                "or_relax_row": (None, [_I64, _D, _D, _P, _P, _P]),
+                "or_wall_normal": (None, [C.c_int, C.c_int, _P]),
+                "or_wall_velocity": (None, [_P, C.c_int, _P]),
+                "or_boundary_weights_one": (C.c_int, [C.c_int, _P, _P, _I64, C.c_int, _P, _D, _D, _P]),
+                "or_diffuse_one": (C.c_int, [_P, C.c_int, C.c_int, _P, _P, _P, _P]),
+                "or_init_f": (None, [_P, _I64, _P, _P, _P, _P]),
+                "or_step": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+                "or_moments_all": (C.c_int, [_P, _I64, _P, _P, _P]),
+                "or_omp_threads": (C.c_int, []),
+                "or_set_threads": (None, [C.c_int]),
+            }
+            for name, (res, args) in sig.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, bad=-1):
+        super().__init__(f"oracle error {code} at particle {bad}")
+        self.code, self.bad = code, bad
+
+
+def make_cfg(cfg, dt=None) -> OrCfg:
+    """or_cfg from a bgk_inputs.CavityConfig."""
+    from bgk_inputs import ALPHA_W, D_MOL, K_B, R_GAS, T0
+    c = OrCfg()
+    c.dims, c.Nv, c.vmax, c.L = cfg.dims, cfg.Nv, cfg.vmax, cfg.L
+    c.h, c.h2, c.alpha_w = cfg.h, cfg.h2, ALPHA_W
+    c.dt = cfg.dt if dt is None else dt
+    c.R, c.kb, c.dmol, c.Twall = R_GAS, K_B, D_MOL, T0
+    for a in range(3):
+        c.Ulid[a] = cfg.U_lid[a]
+    c.dx, c.ale = cfg.dx, cfg.ale
+    return c
+
+
+def nval(c: OrCfg) -> int:
+    return 2 if c.dims == 2 else 1
+
+
+def num_nodes(c: OrCfg) -> int:
+    return int(lib().or_num_nodes(C.byref(c)))
+
+
+def node_velocities(c: OrCfg) -> np.ndarray:
+    K = num_nodes(c)
+    out = np.zeros((K, c.dims))
+    v = np.zeros(3)
+    for k in range(K):
+        lib().or_node_velocity(C.byref(c), k, _p(v))
+        out[k] = v[: c.dims]
+    return out
+
+
+def axis_nodes(c: OrCfg) -> np.ndarray:
+    return np.array([lib().or_axis_node(C.byref(c), j) for j in range(c.Nv + 1)])
+
+
+def dv(c: OrCfg) -> float:
+    return float(lib().or_dv(C.byref(c)))
+
+
+# ---------------------------------------------------------------- geometry
+def neighbors(x: np.ndarray, h2: float):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    N, d = x.shape
+    off = np.zeros(N + 1, dtype=np.int64)
+    need = C.c_int64(0)
+    lib().or_neighbors(d, _p(x), N, h2, _p(off), None, 0, C.byref(need))
+    idx = np.zeros(max(need.value, 1), dtype=np.int32)
+    st = lib().or_neighbors(d, _p(x), N, h2, _p(off), _p(idx), need.value, C.byref(need))
+    assert st == OR_OK
+    return off, idx[: need.value]
+
+
+def neighbors_of(x: np.ndarray, h2: float, i: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    N, d = x.shape
+    m = lib().or_neighbors_of(d, _p(x), N, h2, i, None, 0)
+    out = np.zeros(max(m, 1), dtype=np.int32)
+    lib().or_neighbors_of(d, _p(x), N, h2, i, _p(out), m)
+    return out[:m]
+
+
+def weight(r2: float, h2: float, alpha: float = 6.0) -> float:
+    return float(lib().or_weight(r2, h2, alpha))
+
+
+def sym_eigenvalues(A: np.ndarray) -> np.ndarray:
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    lam = np.zeros(A.shape[0])
+    lib().or_sym_eigenvalues(A.shape[0], _p(A), _p(lam))
+    return lam
+
+
+def wls_one(x, i, nb, h2, alpha=6.0):
+    """(S[d,d], a[m,d]) for particle i, or raises OracleError(OR_E_DEFICIENT)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = x.shape[1]
+    nb = np.ascontiguousarray(nb, dtype=np.int32)
+    S = np.zeros((d, d))
+    a = np.zeros((max(len(nb), 1), d))
+    st = lib().or_wls_one(d, _p(x), i, len(nb), _p(nb), h2, alpha, _p(S), _p(a))
+    if st != OR_OK:
+        raise OracleError(st, i)
+    return S, a[: len(nb)]
+
+
+def frame(dj) -> np.ndarray:
+    dj = np.ascontiguousarray(dj, dtype=np.float64)
+    d = len(dj)
+    fr = np.zeros(d * d)
+    lib().or_frame(d, _p(dj), _p(fr))
+    return fr.reshape(d, d)
+
+
+def rotate(a, fr) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    fr = np.ascontiguousarray(fr, dtype=np.float64)
+    d = len(a)
+    out = np.zeros(d)
+    lib().or_rotate(d, _p(a), _p(fr), _p(out))
+    return out
+
+
+def wls_all(x, kind, off, idx, h2, alpha=6.0):
+    """S[N,d,d], a[nnz,d], frames[nnz,d,d], rot[nnz,d] for interior particles."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    kind = np.ascontiguousarray(kind, dtype=np.int8)
+    N, d = x.shape
+    nnz = len(idx)
+    S = np.zeros((N, d, d))
+    a = np.zeros((max(nnz, 1), d))
+    fr = np.zeros((max(nnz, 1), d, d))
+    rot = np.zeros((max(nnz, 1), d))
+    bad = C.c_int64(-1)
+    st = lib().or_wls_all(d, _p(x), N, _p(kind), _p(off), _p(np.ascontiguousarray(idx)), h2, alpha,
+                          _p(S), _p(a), _p(fr), _p(rot), C.byref(bad))
+    if st != OR_OK:
+        raise OracleError(st, bad.value)
+    return S, a[:nnz], fr[:nnz], rot[:nnz]
+
+
+def boundary_weights_one(x, kind, b, nb, h2, alpha=6.0) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    kind = np.ascontiguousarray(kind, dtype=np.int8)
+    nb = np.ascontiguousarray(nb, dtype=np.int32)
+    cw = np.zeros(max(len(nb), 1))
+    st = lib().or_boundary_weights_one(x.shape[1], _p(x), _p(kind), b, len(nb), _p(nb), h2, alpha, _p(cw))
+    if st != OR_OK:
+        raise OracleError(st, b)
+    return cw[: len(nb)]
+
+
+def boundary_weights(x, kind, off, idx, h2, alpha=6.0) -> np.ndarray:
+    cw = np.zeros(len(idx))
+    for b in np.nonzero(kind != 0)[0]:
+        s, e = off[b], off[b + 1]
+        cw[s:e] = boundary_weights_one(x, kind, int(b), idx[s:e], h2, alpha)
+    return cw
+
+
+# ---------------------------------------------------------------- kinetics
+def tau(c: OrCfg, rho: float, T: float):
+    lam = C.c_double(0.0)
+    t = lib().or_tau(C.byref(c), rho, T, C.byref(lam))
+    return float(t), float(lam.value)
+
+
+def maxwellian_row(c: OrCfg, rho, U, T) -> np.ndarray:
+    K = num_nodes(c)
+    M = np.zeros(nval(c) * K)
+    U3 = np.zeros(3)
+    U3[: c.dims] = U
+    lib().or_maxwellian_row(C.byref(c), rho, _p(U3), T, _p(M))
+    return M
+
+
+def moments_row(c: OrCfg, f: np.ndarray, check: bool = True):
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    out = np.zeros(c.dims + 2)
+    st = lib().or_moments_row(C.byref(c), _p(f), _p(out))
+    if check and st != OR_OK:
+        raise OracleError(st)
+    return out[0], out[1:1 + c.dims].copy(), out[1 + c.dims]
+
+
+def relax_row(tau_, dt, ft, M) -> np.ndarray:
+    ft = np.ascontiguousarray(ft, dtype=np.float64)
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    out = np.zeros_like(ft)
+    lib().or_relax_row(len(ft), tau_, dt, _p(ft), _p(M), _p(out))
+    return out
+
+
+def wall_normal(d, wid) -> np.ndarray:
+    n = np.zeros(3)
+    lib().or_wall_normal(d, wid, _p(n))
+    return n[:d]
+
+
+def _ptr_array(rows):
+    arr = (C.c_void_p * max(len(rows), 1))()
+    for i, r in enumerate(rows):
+        arr[i] = None if r is None else r.ctypes.data
+    return arr
+
+
+def transport_one(c: OrCfg, W, rot, frames, fnb_rows, fi, k_begin=0, k_end=None) -> np.ndarray:
+    K = num_nodes(c)
+    k_end = K if k_end is None else k_end
+    W3 = np.zeros(3)
+    W3[: c.dims] = W
+    rot = np.ascontiguousarray(rot, dtype=np.float64)
+    frames = np.ascontiguousarray(frames, dtype=np.float64)
+    fi = np.ascontiguousarray(fi, dtype=np.float64)
+    rows = [np.ascontiguousarray(r, dtype=np.float64) for r in fnb_rows]
+    out = fi.copy()
+    lib().or_transport_one(C.byref(c), _p(W3), len(rows), _p(rot), _p(frames), _ptr_array(rows),
+                           _p(fi), _p(out), k_begin, k_end)
+    return out
+
+
+def coef_absmax_one(c: OrCfg, W, rot, frames) -> float:
+    W3 = np.zeros(3)
+    W3[: c.dims] = W
+    rot = np.ascontiguousarray(rot, dtype=np.float64)
+    frames = np.ascontiguousarray(frames, dtype=np.float64)
+    return float(lib().or_coef_absmax_one(C.byref(c), _p(W3), len(rot), _p(rot), _p(frames)))
+
+
+def diffuse_one(c: OrCfg, wid, cw, fnb_rows):
+    K = num_nodes(c)
+    cw = np.ascontiguousarray(cw, dtype=np.float64)
+    rows = [None if r is None else np.ascontiguousarray(r, dtype=np.float64) for r in fnb_rows]
+    fb = np.zeros(nval(c) * K)
+    rw = C.c_double(0.0)
+    st = lib().or_diffuse_one(C.byref(c), wid, len(rows), _p(cw), _ptr_array(rows), _p(fb), C.byref(rw))
+    if st != OR_OK:
+        raise OracleError(st)
+    return fb, float(rw.value)
+
+
+# ---------------------------------------------------------------- drivers
+def init_f(c: OrCfg, rho, U, T) -> np.ndarray:
+    N = len(rho)
+    f = np.zeros((N, nval(c) * num_nodes(c)))
+    U3 = np.ascontiguousarray(U, dtype=np.float64)
+    lib().or_init_f(C.byref(c), N, _p(np.ascontiguousarray(rho, dtype=np.float64)), _p(U3),
+                    _p(np.ascontiguousarray(T, dtype=np.float64)), _p(f))
+    return f
+
+
+class State:
+    """Whole-cloud oracle state (x, kind, f, W, macro)."""
+
+    def __init__(self, c: OrCfg, cloud):
+        self.c = c
+        self.x = np.ascontiguousarray(cloud["x"], dtype=np.float64).copy()
+        self.kind = np.ascontiguousarray(cloud["kind"], dtype=np.int8)
+        self.f = init_f(c, cloud["rho"], cloud["U"], cloud["T"])
+        self.W = np.ascontiguousarray(cloud["U"], dtype=np.float64).copy()
+        if not c.ale:
+            self.W[:] = 0.0
+        N, d = self.x.shape
+        self.macro = np.zeros((N, d + 2))
+        self.rho_w = np.zeros(N)
+
+    def step(self, n: int = 1):
+        bad = C.c_int64(-1)
+        N = self.x.shape[0]
+        for _ in range(n):
+            st = lib().or_step(C.byref(self.c), N, _p(self.x), _p(self.kind), _p(self.f), _p(self.W),
+                               _p(self.macro), _p(self.rho_w), C.byref(bad))
+            if st != OR_OK:
+                raise OracleError(st, bad.value)
+        return self
+
+    def moments(self):
+        N, d = self.x.shape
+        out = np.zeros((N, d + 2))
+        bad = C.c_int64(-1)
+        st = lib().or_moments_all(C.byref(self.c), N, _p(self.f), _p(out), C.byref(bad))
+        if st != OR_OK:
+            raise OracleError(st, bad.value)
+        return out[:, 0], out[:, 1:1 + d], out[:, 1 + d]
+
+
+def run_steps(cfg, n_steps: int, cloud=None, dt=None) -> State:
+    from bgk_inputs import make_cloud
+    c = make_cfg(cfg, dt)
+    s = State(c, cloud if cloud is not None else make_cloud(cfg))
+    s.step(n_steps)
+    return s
+
+
+def omp_threads() -> int:
+    return int(lib().or_omp_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().or_set_threads(int(n))
+
+
+def sampled_first_step(cfg, cloud, sample, k_range=None):
+    """First step n=0 -> 1 at the sampled particles of a full-size cloud.
+
+    Builds only what the sample needs, from the oracle's own primitives: f^0
+    rows (Maxwellian of the seeded initial fields) of the sample and of its
+    neighbours (and, for boundary particles, of its interior neighbours'
+    neighbours), brute-force neighbour lists, WLS, transport, moments,
+    relaxation and diffuse reflection.  Returns {i: dict(f=row, rho, U, T, x)}
+    with f the full row of f^1 and (rho, U, T) the recovered state for
+    interior particles.  ``k_range`` limits transport to a node range (rows are
+    then only valid there; relaxation needs all nodes, so it is skipped).
+    """
+    c = make_cfg(cfg)
+    x, kind = cloud["x"], cloud["kind"]
+    d = c.dims
+    K = num_nodes(c)
+    f0 = {}
+
+    def row0(j):
+        if j not in f0:
+            f0[j] = maxwellian_row(c, cloud["rho"][j], cloud["U"][j], cloud["T"][j])
+        return f0[j]
+
+    def interior_f1(i):
+        nb = neighbors_of(x, c.h2, i)
+        S, a = wls_one(x, i, nb, c.h2, c.alpha_w)
+        frs = np.stack([frame(x[j] - x[i]) for j in nb])
+        rot = np.stack([rotate(a[q], frs[q]) for q in range(len(nb))])
+        W = cloud["U"][i] if c.ale else np.zeros(d)
+        kb, ke = (0, K) if k_range is None else k_range
+        ft = transport_one(c, W, rot, frs, [row0(int(j)) for j in nb], row0(i), kb, ke)
+        if k_range is not None:
+            return {"ft": ft}
+        rho, U, T = moments_row(c, ft)
+        t, _ = tau(c, rho, T)
+        M = maxwellian_row(c, rho, U, T)
+        f1 = relax_row(t, c.dt, ft, M)
+        xn = x[i].copy()
+        if c.ale:
+            eps = 1e-3 * c.dx
+            xn = np.clip(x[i] + c.dt * U, eps, c.L - eps)
+        return {"f": f1, "ft": ft, "rho": rho, "U": U, "T": T, "x": xn, "S": S, "rot": rot, "nb": nb}
+
+    out = {}
+    cache = {}
+    for i in sample:
+        i = int(i)
+        if kind[i] == 0:
+            out[i] = cache.setdefault(i, interior_f1(i))
+        else:
+            nb = neighbors_of(x, c.h2, i)
+            cw = boundary_weights_one(x, kind, i, nb, c.h2, c.alpha_w)
+            rows = []
+            for q, j in enumerate(nb):
+                j = int(j)
+                if kind[j] == 0:
+                    if j not in cache:
+                        cache[j] = interior_f1(j)
+                    rows.append(cache[j]["f"])
+                else:
+                    rows.append(None)
+            fb, rw = diffuse_one(c, int(kind[i]), cw, rows)
+            out[i] = {"f": fb, "rho_w": rw, "x": x[i].copy(), "nb": nb, "cw": cw}
+    return out
