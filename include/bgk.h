@@ -1,0 +1,204 @@
+/*
+ * bgk.h -- C ABI of the B200-native time step of the meshfree ALE scheme for
+ * the BGK equation (arXiv 2408.02350, "PAPER.md" below; line numbers P:n).
+ *
+ * One step covers, for every particle and every discrete velocity
+ * (P:163-199 full model, P:202-262 Chu-reduced 2D model):
+ *   neighbour search, weighted-least-squares stencil coefficients
+ *   (P:290-365), positive upwind transport, moments (P:185-193,
+ *   P:226-255), local Maxwellian, implicit relaxation
+ *   (P:196-199), ALE motion and diffuse-reflection walls
+ *   (construction in DESIGN.md reading Z17).
+ *
+ * Conventions
+ *  - All floating point is IEEE fp64.  Particles are indexed 0..N-1 in the
+ *    order the caller passes them.  kind[i] = 0 for interior particles and
+ *    1..2*dims for boundary particles on wall id kind[i]
+ *    (1: x=0, 2: x=L, 3: y=0, 4: y=L, 5: z=0, 6: z=L; the lid is wall 2*dims).
+ *  - Velocity grid: per axis v_j = -vmax + j*dv, j = 0..Nv,
+ *    dv = 2 vmax / Nv; node k = ((j1*(Nv+1)) + j2)*(Nv+1) + j3 (last axis
+ *    fastest).  A "column" is the set of nodes sharing (j2[, j3]); there are
+ *    (Nv+1)^(dims-1) columns, each holding Nv+1 nodes along v_1.  A rank owns
+ *    the columns [col_begin, col_end) of the grid (velocity sharding across
+ *    GPUs, one process per GPU).
+ *  - Canonical distribution layout at the ABI (bgk_get_f / bgk_set_f):
+ *    f[N][nval][Nv+1][ncol_local] row-major, nval = 2 (g1, g2) in 2D
+ *    and 1 (f) in 3D.  With one rank and all columns this is f[N][nval][K].
+ *  - Device memory is owned by the caller (PyTorch allocates it): the library
+ *    carves its buffers out of one caller-provided device workspace and never
+ *    allocates device memory itself.  The context object is a small host
+ *    struct owned by the library (bgk_destroy frees it).
+ *  - Pointers documented "host or device" may be either (unified addressing);
+ *    the call copies with cudaMemcpyAsync(cudaMemcpyDefault) on the given
+ *    stream and synchronises that stream before returning.
+ *  - Every call returns a bgk_status and never throws.  Kernel-side failures
+ *    (deficient stencil, degenerate state, capacity, out-of-domain) are
+ *    latched in a device error word and reported by the next synchronising
+ *    call (bgk_sync, bgk_wls_coeffs, bgk_build_neighbors, bgk_moments,
+ *    bgk_get_f).  bgk_last_error gives the message and the particle index.
+ *  - All work is enqueued on the caller's stream; bgk_step enqueues no host
+ *    synchronisation and is CUDA-graph capturable.
+ */
+#ifndef BGK_B200_H
+#define BGK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bgk_ctx bgk_ctx;
+typedef void* bgk_stream; /* a cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = legacy default stream */
+
+typedef enum {
+    BGK_OK = 0,
+    BGK_E_INVALID_ARG = 1,      /* bad configuration or argument */
+    BGK_E_CAPACITY = 2,         /* neighbour storage too small (needed count reported) */
+    BGK_E_DEFICIENT_STENCIL = 3,/* < dims+2 neighbours or lambda_min < 1e-12 lambda_max */
+    BGK_E_DEGENERATE_STATE = 4, /* rho <= 0 or T <= 1e-12 K after moment recovery */
+    BGK_E_OUT_OF_DOMAIN = 5,    /* a particle outside [0, L]^dims */
+    BGK_E_CUDA = 6,             /* a CUDA runtime error (message in bgk_last_error) */
+    BGK_E_WALL = 7              /* diffuse-reflection denominator <= 0 */
+} bgk_status;
+
+typedef struct bgk_config {
+    int32_t dims;        /* 2 = Chu-reduced 2D model (values g1, g2), 3 = full 3D model */
+    int32_t Nv;          /* velocity cells per axis, even, >= 2: Nv+1 nodes per axis */
+    double vmax;         /* velocity bound; > 0 */
+    double L;            /* cavity edge [m] */
+    double h;            /* neighbour radius [m], h = 3.1 dx */
+    double h2;           /* h*h exactly as the caller computed it; neighbour test d2 <= h2 */
+    double alpha_w;      /* Gaussian weight exponent, 6 */
+    double dt;           /* time step [s] */
+    double R;            /* specific gas constant */
+    double kb;           /* Boltzmann constant */
+    double dmol;         /* molecular diameter [m] */
+    double T_wall;       /* wall temperature [K] */
+    double U_lid[3];     /* lid velocity [m/s]; other walls at rest */
+    double dx;           /* nominal particle spacing [m]; ALE clamp margin = 1e-3 dx */
+    int32_t ale;         /* 1: ALE, W = U^n, particles move, geometry rebuilt every step;
+                            0: fixed cloud, W = 0, geometry built once and cached */
+    int32_t col_begin;   /* first velocity column owned by this rank */
+    int32_t col_end;     /* one past the last owned column; col_begin = col_end = 0 means all */
+    int32_t max_neighbors; /* per-particle neighbour capacity (0: 96 in 2D, 256 in 3D) */
+} bgk_config;
+
+/* Bytes of device workspace bgk_init_cloud needs for N particles. */
+bgk_status bgk_workspace_size(const bgk_config* cfg, int64_t N, size_t* bytes);
+
+/* Create a context and fill the initial state.
+ *   x      : host or device, N*dims fp64 positions (row-major [N][dims]), inside [0, L]^dims.
+ *   kind   : host or device, N int8 (0 interior, 1..2*dims wall id).
+ *   macro0 : host or device, N*(dims+2) fp64 initial (rho, U[dims], T) per particle, or NULL for
+ *            the uniform state (rho, U, T) = (1, 0, T_wall).  f^0 = M(rho^0, U^0, T^0) at every
+ *            particle; the transport velocity W^0 = U^0 (ALE) or 0 (fixed cloud).
+ *   workspace, ws_bytes : caller-owned device memory of at least bgk_workspace_size bytes,
+ *            16-byte aligned; it must outlive the context.
+ * Errors: BGK_E_INVALID_ARG (dims not 2/3, odd or < 2 Nv, vmax <= 0, N < 1, bad column
+ * range, workspace too small), BGK_E_OUT_OF_DOMAIN.  Synchronises the stream. */
+bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* kind,
+                          const double* macro0, int64_t N, void* workspace, size_t ws_bytes,
+                          bgk_stream stream, bgk_ctx** out);
+
+/* Cell-linked-list neighbour search on the current positions:
+ * N(i) = { j != i : ((x_j-x_i)^2 + (y_j-y_i)^2) + (z_j-z_i)^2 <= h2 }, each operation rounded
+ * (no FMA), ascending j.  Also refreshes the context's internal lists.
+ * If offsets/idx are non-NULL (device), writes the CSR copy there: offsets[N+1] int64,
+ * idx[offsets[N]] int32; cap = capacity of idx.  *needed (host, may be NULL) receives offsets[N].
+ * Errors: BGK_E_CAPACITY if offsets[N] > cap or any particle exceeds max_neighbors.
+ * Synchronises the stream. */
+bgk_status bgk_build_neighbors(bgk_ctx* ctx, int64_t* offsets, int32_t* idx, int64_t cap,
+                               int64_t* needed, bgk_stream stream);
+
+/* Batched WLS stencil coefficients on the current neighbour lists:
+ * interior particles: S = (M^T W M)^{-1}, a_j = w_j S d_j, frame (n, t[, b]) of each pair,
+ * rotated coefficients (abar, bbar[, gbar]) = (a.n, a.t[, a.b]); boundary particles: linear
+ * WLS interpolation weights c_bj over interior neighbours (Z19).
+ * Errors: BGK_E_DEFICIENT_STENCIL with the first offending particle.  Synchronises. */
+bgk_status bgk_wls_coeffs(bgk_ctx* ctx, bgk_stream stream);
+
+/* Copy WLS results out (device or host pointers, NULL to skip):
+ *   S[N][dims][dims] (interior rows), rot[nnz][dims] = (abar, bbar[, gbar]),
+ *   frames[nnz][dims][dims] = rows n, t[, b], cw[nnz] = boundary weights (0 elsewhere).
+ * nnz = offsets[N] of the last neighbour build.  Synchronises. */
+bgk_status bgk_get_wls(bgk_ctx* ctx, double* S, double* rot, double* frames, double* cw,
+                       bgk_stream stream);
+
+/* n_steps time steps n -> n+1 (S:414 order): [ALE: neighbours + WLS on x^n],
+ * transport, moment recovery, relaxation, [ALE: move], diffuse reflection.  Single rank
+ * only (col range = all columns); multi-rank runs use the split-phase calls below.
+ * Asynchronous; errors are latched (see conventions). */
+bgk_status bgk_step(bgk_ctx* ctx, int n_steps, bgk_stream stream);
+
+/* Split phases of one step, for velocity-sharded runs (one rank per GPU):
+ *   bgk_step_transport: [ALE: neighbours + WLS], transport of the local columns, and the
+ *        rank-local moment sums written to bgk_buffer(BGK_BUF_MOMENT_SUMS) ([N][5] fp64);
+ *   -- caller: all_reduce(SUM) of that buffer across ranks --
+ *   bgk_step_relax: moments -> (rho, U, T, tau), relaxation of the local columns, ALE move,
+ *        boundary interpolation of the local columns and the rank-local incoming wall flux in
+ *        bgk_buffer(BGK_BUF_WALL_FLUX) ([N] fp64);
+ *   -- caller: all_reduce(SUM) of that buffer --
+ *   bgk_step_boundary: rho_w and the outgoing half of every boundary row.
+ * Asynchronous. */
+bgk_status bgk_step_transport(bgk_ctx* ctx, bgk_stream stream);
+bgk_status bgk_step_relax(bgk_ctx* ctx, bgk_stream stream);
+bgk_status bgk_step_boundary(bgk_ctx* ctx, bgk_stream stream);
+
+typedef enum {
+    BGK_BUF_MOMENT_SUMS = 0, /* [N][5] fp64 rank-local sums (sum f, sum v f, sum |v|^2 f (+g2)) */
+    BGK_BUF_WALL_FLUX = 1,   /* [N] fp64 rank-local sum_{v.n<0} (v.n) f_b (boundary rows) */
+    BGK_BUF_F = 2            /* the current distribution buffer (internal layout) */
+} bgk_buffer_id;
+
+/* Device pointer and byte size of an internal buffer (inside the caller's workspace). */
+bgk_status bgk_buffer(bgk_ctx* ctx, bgk_buffer_id id, void** ptr, size_t* bytes);
+
+/* Moments of the current distribution at every particle:
+ * rho = dv^d sum f, U = dv^d sum v f / rho, 3 rho R T = dv^d sum |v-U|^2 f (+ dv^2 sum g2 in 2D).
+ * rho[N], U[N][dims], T[N]: host or device, any may be NULL.  Single rank; for sharded runs use
+ * bgk_moments_partial + all_reduce + bgk_moments_finalize.  Synchronises. */
+bgk_status bgk_moments(bgk_ctx* ctx, double* rho, double* U, double* T, bgk_stream stream);
+bgk_status bgk_moments_partial(bgk_ctx* ctx, bgk_stream stream); /* into BGK_BUF_MOMENT_SUMS */
+bgk_status bgk_moments_finalize(bgk_ctx* ctx, double* rho, double* U, double* T, bgk_stream stream);
+
+/* Recovered state (rho, U, T) of the last step at interior particles: macro[N][dims+2].
+ * Host or device.  Synchronises. */
+bgk_status bgk_get_macro(bgk_ctx* ctx, double* macro, bgk_stream stream);
+
+/* Distribution in the canonical layout (see conventions), host or device.  Synchronises. */
+bgk_status bgk_get_f(bgk_ctx* ctx, double* f, bgk_stream stream);
+bgk_status bgk_set_f(bgk_ctx* ctx, const double* f, bgk_stream stream);
+
+/* Positions x[N][dims] (host or device).  Synchronises. */
+bgk_status bgk_get_positions(bgk_ctx* ctx, double* x, bgk_stream stream);
+
+/* Neighbour lists of the last build: offsets[N+1], idx[nnz] (host or device; NULL idx to read
+ * the count only via *nnz).  Synchronises. */
+bgk_status bgk_get_neighbors(bgk_ctx* ctx, int64_t* offsets, int32_t* idx, int64_t* nnz,
+                             bgk_stream stream);
+
+/* Largest explicit-stable dt on the current geometry and W:
+ * 1 / max_{i,k} sum_j |C_ijk| over local columns.  Synchronises. */
+bgk_status bgk_stable_dt(bgk_ctx* ctx, double* dt_out, bgk_stream stream);
+
+/* Number of CUDA kernels one bgk_step(ctx, 1) launches (for launch accounting). */
+bgk_status bgk_launches_per_step(bgk_ctx* ctx, int64_t* n);
+
+/* Wait for the stream and report any latched device error. */
+bgk_status bgk_sync(bgk_ctx* ctx, bgk_stream stream);
+
+/* Message of the last error and the offending particle index (-1 if none). */
+const char* bgk_last_error(bgk_ctx* ctx, int64_t* particle);
+
+/* Free the host context (the workspace stays owned by the caller). */
+bgk_status bgk_destroy(bgk_ctx* ctx);
+
+/* Library version string. */
+const char* bgk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BGK_B200_H */

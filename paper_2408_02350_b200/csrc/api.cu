@@ -1,0 +1,478 @@
+// api.cu -- the C ABI of include/bgk.h: context, workspace carving, launch
+// sequence of one step (split into the three phases a velocity-sharded run
+// interleaves with its two all-reduces), copies and error reporting.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "bgk_internal.cuh"
+
+using namespace bgk;
+
+namespace {
+
+constexpr const char* kVersion = "bgk_b200 0.1.0 (sm_100a, fp64)";
+
+struct Carver {
+    char* base;
+    size_t off = 0;
+    bool dry;
+    template <typename T>
+    T* take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T* p = dry ? nullptr : reinterpret_cast<T*>(base + off);
+        off += sizeof(T) * std::max<size_t>(count, 1);
+        return p;
+    }
+};
+
+bool valid_cfg(const bgk_config* c, int64_t N) {
+    if (!c || N < 1) return false;
+    if (c->dims != 2 && c->dims != 3) return false;
+    if (c->Nv < 2 || (c->Nv & 1) || c->Nv + 1 > 64) return false;
+    if (!(c->vmax > 0.0) || !(c->L > 0.0) || !(c->h > 0.0) || !(c->h2 > 0.0) || !(c->dt >= 0.0)) return false;
+    if (!(c->R > 0.0) || !(c->kb > 0.0) || !(c->dmol > 0.0) || !(c->T_wall > 0.0) || !(c->alpha_w > 0.0)) return false;
+    if (N > (int64_t)INT32_MAX) return false;
+    return true;
+}
+
+// geometry + mapping that only depends on the configuration and N
+void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
+    c->cfg = *cfg;
+    c->d = cfg->dims;
+    c->nv = c->d == 2 ? 2 : 1;
+    c->n1 = cfg->Nv + 1;
+    c->ncol_g = c->d == 2 ? c->n1 : c->n1 * c->n1;
+    if (cfg->col_begin == 0 && cfg->col_end == 0) {
+        c->c0 = 0;
+        c->c1 = c->ncol_g;
+    } else {
+        c->c0 = cfg->col_begin;
+        c->c1 = cfg->col_end;
+    }
+    c->ncol = c->c1 - c->c0;
+    c->N = N;
+    c->Kloc = (int64_t)c->n1 * c->ncol;
+    c->RS = c->Kloc * c->nv;
+    c->max_nb = cfg->max_neighbors > 0 ? cfg->max_neighbors : (c->d == 2 ? 96 : 256);
+    c->cap = N * (int64_t)c->max_nb;
+    int nc = (int)std::floor(cfg->L / cfg->h);
+    nc = std::max(1, std::min(nc, kMaxCellsPerAxis));
+    while (nc > 1 && cfg->L / nc < cfg->h * (1.0 + 1e-12)) --nc;   // cell edge strictly >= h
+    c->ncell = 1;
+    for (int a = 0; a < 3; ++a) {
+        c->nc[a] = a < c->d ? nc : 1;
+        c->edge[a] = cfg->L / nc;
+        c->ncell *= c->nc[a];
+    }
+    c->dv = 2.0 * cfg->vmax / cfg->Nv;
+    c->vmin = -cfg->vmax;
+    c->PD = c->d == 2 ? 4 : 10;
+    c->R = transport_rows_per_thread(c->d, c->n1);
+    c->nchunk = c->n1 / c->R;
+    c->nslots = c->ncol * c->nchunk;
+    c->nwpp = (c->nslots + 31) / 32;
+    c->bnd_chunk = 256;
+    c->bnd_nch = (int)((c->Kloc + 255) / 256);
+}
+
+size_t carve(bgk_ctx* c, char* base, bool dry) {
+    Carver k{base, 0, dry};
+    const int64_t N = c->N;
+    const int d = c->d;
+    c->x = k.take<double>(N * d);
+    c->kind = k.take<int8_t>(N);
+    c->interior = k.take<int32_t>(N);
+    c->boundary = k.take<int32_t>(N);
+    c->W = k.take<double>(N * d);
+    c->macro = k.take<double>(N * (d + 2));
+    c->f[0] = k.take<double>((size_t)N * c->RS);
+    c->f[1] = k.take<double>((size_t)N * c->RS);
+    c->partials = k.take<double>((size_t)N * c->nwpp * kPM);
+    c->sums = k.take<double>((size_t)N * kPM);
+    c->wallpart = k.take<double>((size_t)N * c->bnd_nch);
+    c->wallnum = k.take<double>(N);
+    c->Mw = k.take<double>((size_t)2 * d * c->RS);
+    c->wall_den = k.take<double>(2 * d);
+    c->outbuf = k.take<double>(N * (d + 2));
+    c->err = k.take<int64_t>(4);
+    c->stab = k.take<unsigned long long>(1);
+    c->scan_tmp = k.take<int64_t>(1024);
+    c->g.cell_of = k.take<int32_t>(N);
+    c->g.cell_cnt = k.take<int32_t>(c->ncell);
+    c->g.cell_start = k.take<int32_t>(c->ncell + 1);
+    c->g.cell_fill = k.take<int32_t>(c->ncell);
+    c->g.cell_pts = k.take<int32_t>(N);
+    c->g.nb_cnt = k.take<int32_t>(N);
+    c->g.nb_off = k.take<int64_t>(N + 1);
+    c->g.nb_idx = k.take<int32_t>(c->cap);
+    c->g.S = k.take<double>(N * d * d);
+    c->g.P = k.take<double>((size_t)c->cap * c->PD);
+    c->g.cw = k.take<double>(c->cap);
+    c->g.order = k.take<int32_t>(N);
+    return k.off + 256;
+}
+
+bgk_status cuda_fail(bgk_ctx* c, cudaError_t e) {
+    if (c) {
+        std::snprintf(c->msg, sizeof(c->msg), "CUDA error: %s", cudaGetErrorString(e));
+        c->bad = -1;
+    }
+    return BGK_E_CUDA;
+}
+
+bgk_status check_launch(bgk_ctx* c) {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BGK_OK : cuda_fail(c, e);
+}
+
+const char* code_msg(int code) {
+    switch (code) {
+        case BGK_E_CAPACITY: return "neighbour capacity exceeded (max_neighbors)";
+        case BGK_E_DEFICIENT_STENCIL: return "deficient WLS stencil (< dims+2 neighbours or ill-conditioned)";
+        case BGK_E_DEGENERATE_STATE: return "degenerate state (rho <= 0 or T <= 1e-12)";
+        case BGK_E_OUT_OF_DOMAIN: return "particle outside [0, L]^dims";
+        case BGK_E_WALL: return "diffuse-reflection denominator <= 0";
+        default: return "error";
+    }
+}
+
+// synchronise the stream and surface (then clear) a latched device error
+bgk_status sync_check(bgk_ctx* c, cudaStream_t s) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(c, e);
+    int64_t h[2];
+    e = cudaMemcpy(h, c->err, sizeof(h), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e);
+    if (h[0] != 0) {
+        std::snprintf(c->msg, sizeof(c->msg), "%s", code_msg((int)h[0]));
+        c->bad = h[1] == INT64_MAX ? -1 : h[1];
+        const int64_t reset[2] = {0, INT64_MAX};
+        cudaMemcpy(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice);
+        return (bgk_status)h[0];
+    }
+    return BGK_OK;
+}
+
+cudaStream_t S(bgk_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void ensure_geometry(bgk_ctx* c, cudaStream_t s) {
+    if (c->cfg.ale || !c->geometry_valid) {
+        launch_build_neighbors(c, s);
+        launch_wls(c, s);
+        c->geometry_valid = true;
+    }
+}
+
+bgk_status copy_out(bgk_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
+    if (e != cudaSuccess) return cuda_fail(c, e);
+    return BGK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bgk_version(void) { return kVersion; }
+
+bgk_status bgk_workspace_size(const bgk_config* cfg, int64_t N, size_t* bytes) {
+    if (!valid_cfg(cfg, N) || !bytes) return BGK_E_INVALID_ARG;
+    bgk_ctx tmp{};
+    derive(&tmp, cfg, N);
+    if (tmp.c0 < 0 || tmp.c1 > tmp.ncol_g || tmp.c0 >= tmp.c1) return BGK_E_INVALID_ARG;
+    *bytes = carve(&tmp, nullptr, true);
+    return BGK_OK;
+}
+
+bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* kind, const double* macro0,
+                          int64_t N, void* workspace, size_t ws_bytes, bgk_stream stream, bgk_ctx** out) {
+    if (!out || !x || !kind || !workspace) return BGK_E_INVALID_ARG;
+    *out = nullptr;
+    size_t need = 0;
+    if (bgk_workspace_size(cfg, N, &need) != BGK_OK || ws_bytes < need) return BGK_E_INVALID_ARG;
+    if (reinterpret_cast<uintptr_t>(workspace) % 16) return BGK_E_INVALID_ARG;
+    bgk_ctx* c = new (std::nothrow) bgk_ctx{};
+    if (!c) return BGK_E_INVALID_ARG;
+    derive(c, cfg, N);
+    carve(c, reinterpret_cast<char*>(workspace), false);
+    c->bad = -1;
+    c->fcur = 0;
+    c->geometry_valid = false;
+    cudaStream_t s = S(stream);
+    // kinds on the host to build the static interior / boundary lists
+    std::vector<int8_t> hk(N);
+    cudaError_t e = cudaMemcpy(hk.data(), kind, N, cudaMemcpyDefault);
+    if (e != cudaSuccess) { bgk_status st = cuda_fail(c, e); delete c; return st; }
+    std::vector<int32_t> in, bd;
+    for (int64_t i = 0; i < N; ++i) {
+        if (hk[i] < 0 || hk[i] > 2 * c->d) { delete c; return BGK_E_INVALID_ARG; }
+        (hk[i] == 0 ? in : bd).push_back((int32_t)i);
+    }
+    c->N_int = (int64_t)in.size();
+    c->N_b = (int64_t)bd.size();
+    const int64_t reset[4] = {0, INT64_MAX, 0, 0};
+    cudaMemcpyAsync(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(c->stab, 0, sizeof(unsigned long long), s);
+    cudaMemcpyAsync(c->x, x, sizeof(double) * N * c->d, cudaMemcpyDefault, s);
+    cudaMemcpyAsync(c->kind, hk.data(), N, cudaMemcpyHostToDevice, s);
+    if (!in.empty()) cudaMemcpyAsync(c->interior, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
+    if (!bd.empty()) cudaMemcpyAsync(c->boundary, bd.data(), sizeof(int32_t) * bd.size(), cudaMemcpyHostToDevice, s);
+    // interior ids also serve as the initial processing order
+    if (!in.empty()) cudaMemcpyAsync(c->g.order, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
+    const double* m0 = nullptr;
+    if (macro0) {
+        cudaMemcpyAsync(c->outbuf, macro0, sizeof(double) * N * (c->d + 2), cudaMemcpyDefault, s);
+        m0 = c->outbuf;
+    }
+    launch_check_domain(c, s);
+    launch_wall_tables(c, s);
+    launch_init_f(c, m0, s);
+    bgk_status st = check_launch(c);
+    if (st == BGK_OK) st = sync_check(c, s);
+    if (st != BGK_OK && st != BGK_E_OUT_OF_DOMAIN && st != BGK_E_WALL) { delete c; return st; }
+    if (st != BGK_OK) { delete c; return st; }
+    *out = c;
+    return BGK_OK;
+}
+
+bgk_status bgk_build_neighbors(bgk_ctx* c, int64_t* offsets, int32_t* idx, int64_t cap, int64_t* needed,
+                               bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    launch_build_neighbors(c, s);
+    c->geometry_valid = false;
+    bgk_status st = check_launch(c);
+    if (st == BGK_OK) st = sync_check(c, s);
+    int64_t nnz = 0;
+    cudaMemcpy(&nnz, c->g.nb_off + c->N, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    c->nnz_last = nnz;
+    if (needed) *needed = nnz;
+    if (st != BGK_OK) return st;
+    if (offsets) {
+        if (idx && nnz > cap) {
+            std::snprintf(c->msg, sizeof(c->msg), "idx capacity %lld < needed %lld", (long long)cap, (long long)nnz);
+            return BGK_E_CAPACITY;
+        }
+        if ((st = copy_out(c, offsets, c->g.nb_off, sizeof(int64_t) * (c->N + 1), s)) != BGK_OK) return st;
+        if (idx && nnz && (st = copy_out(c, idx, c->g.nb_idx, sizeof(int32_t) * nnz, s)) != BGK_OK) return st;
+        return sync_check(c, s);
+    }
+    return BGK_OK;
+}
+
+bgk_status bgk_wls_coeffs(bgk_ctx* c, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    launch_wls(c, s);
+    bgk_status st = check_launch(c);
+    if (st == BGK_OK) st = sync_check(c, s);
+    c->geometry_valid = (st == BGK_OK);
+    return st;
+}
+
+bgk_status bgk_get_wls(bgk_ctx* c, double* Sout, double* rot, double* frames, double* cw, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    const int d = c->d;
+    int64_t nnz = 0;
+    cudaMemcpy(&nnz, c->g.nb_off + c->N, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    bgk_status st;
+    if (Sout && (st = copy_out(c, Sout, c->g.S, sizeof(double) * c->N * d * d, s)) != BGK_OK) return st;
+    if (cw && nnz && (st = copy_out(c, cw, c->g.cw, sizeof(double) * nnz, s)) != BGK_OK) return st;
+    if (rot || frames) {
+        double* scratch = c->f[1 - c->fcur];
+        if ((size_t)nnz * (d + d * d) > (size_t)c->N * c->RS) return BGK_E_CAPACITY;
+        double* r = scratch;
+        double* fr = scratch + (size_t)nnz * d;
+        cudaMemsetAsync(scratch, 0, sizeof(double) * nnz * (d + d * d), s);
+        launch_wls_export(c, r, fr, s);
+        if ((st = check_launch(c)) != BGK_OK) return st;
+        if (rot && nnz && (st = copy_out(c, rot, r, sizeof(double) * nnz * d, s)) != BGK_OK) return st;
+        if (frames && nnz && (st = copy_out(c, frames, fr, sizeof(double) * nnz * d * d, s)) != BGK_OK) return st;
+    }
+    return sync_check(c, s);
+}
+
+bgk_status bgk_step_transport(bgk_ctx* c, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    ensure_geometry(c, s);
+    launch_transport(c, c->f[c->fcur], c->f[1 - c->fcur], s);
+    launch_moment_reduce(c, s);
+    return check_launch(c);
+}
+
+bgk_status bgk_step_relax(bgk_ctx* c, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    double* fn = c->f[1 - c->fcur];
+    launch_relax(c, fn, s);
+    launch_boundary_interp(c, fn, s);
+    return check_launch(c);
+}
+
+bgk_status bgk_step_boundary(bgk_ctx* c, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    launch_boundary_fill(c, c->f[1 - c->fcur], s);
+    c->fcur = 1 - c->fcur;
+    return check_launch(c);
+}
+
+bgk_status bgk_step(bgk_ctx* c, int n_steps, bgk_stream stream) {
+    if (!c || n_steps < 0) return BGK_E_INVALID_ARG;
+    if (c->ncol != c->ncol_g) return BGK_E_INVALID_ARG;   // sharded runs use the split phases
+    for (int n = 0; n < n_steps; ++n) {
+        bgk_status st;
+        if ((st = bgk_step_transport(c, stream)) != BGK_OK) return st;
+        if ((st = bgk_step_relax(c, stream)) != BGK_OK) return st;
+        if ((st = bgk_step_boundary(c, stream)) != BGK_OK) return st;
+    }
+    return BGK_OK;
+}
+
+bgk_status bgk_buffer(bgk_ctx* c, bgk_buffer_id id, void** ptr, size_t* bytes) {
+    if (!c || !ptr || !bytes) return BGK_E_INVALID_ARG;
+    switch (id) {
+        case BGK_BUF_MOMENT_SUMS: *ptr = c->sums; *bytes = sizeof(double) * c->N * kPM; return BGK_OK;
+        case BGK_BUF_WALL_FLUX: *ptr = c->wallnum; *bytes = sizeof(double) * c->N; return BGK_OK;
+        case BGK_BUF_F: *ptr = c->f[c->fcur]; *bytes = sizeof(double) * c->N * c->RS; return BGK_OK;
+    }
+    return BGK_E_INVALID_ARG;
+}
+
+bgk_status bgk_moments_partial(bgk_ctx* c, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    launch_row_moments(c, c->f[c->fcur], S(stream));
+    return check_launch(c);
+}
+
+bgk_status bgk_moments_finalize(bgk_ctx* c, double* rho, double* U, double* T, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    launch_moments_finalize(c, c->outbuf, s);
+    bgk_status st = check_launch(c);
+    if (st == BGK_OK) st = sync_check(c, s);
+    const int d = c->d;
+    std::vector<double> h(c->N * (d + 2));
+    cudaError_t e = cudaMemcpy(h.data(), c->outbuf, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e);
+    std::vector<double> r(c->N), u(c->N * d), t(c->N);
+    for (int64_t i = 0; i < c->N; ++i) {
+        r[i] = h[i * (d + 2)];
+        for (int a = 0; a < d; ++a) u[i * d + a] = h[i * (d + 2) + 1 + a];
+        t[i] = h[i * (d + 2) + 1 + d];
+    }
+    if (rho) cudaMemcpy(rho, r.data(), sizeof(double) * c->N, cudaMemcpyDefault);
+    if (U) cudaMemcpy(U, u.data(), sizeof(double) * c->N * d, cudaMemcpyDefault);
+    if (T) cudaMemcpy(T, t.data(), sizeof(double) * c->N, cudaMemcpyDefault);
+    return st;
+}
+
+bgk_status bgk_moments(bgk_ctx* c, double* rho, double* U, double* T, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    if (c->ncol != c->ncol_g) return BGK_E_INVALID_ARG;
+    bgk_status st = bgk_moments_partial(c, stream);
+    if (st != BGK_OK) return st;
+    return bgk_moments_finalize(c, rho, U, T, stream);
+}
+
+bgk_status bgk_get_macro(bgk_ctx* c, double* macro, bgk_stream stream) {
+    if (!c || !macro) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    bgk_status st = copy_out(c, macro, c->macro, sizeof(double) * c->N * (c->d + 2), s);
+    if (st != BGK_OK) return st;
+    return sync_check(c, s);
+}
+
+bgk_status bgk_get_f(bgk_ctx* c, double* f, bgk_stream stream) {
+    if (!c || !f) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    double* scratch = c->f[1 - c->fcur];
+    launch_to_canonical(c, c->f[c->fcur], scratch, s);
+    bgk_status st = check_launch(c);
+    if (st != BGK_OK) return st;
+    if ((st = copy_out(c, f, scratch, sizeof(double) * c->N * c->RS, s)) != BGK_OK) return st;
+    return sync_check(c, s);
+}
+
+bgk_status bgk_set_f(bgk_ctx* c, const double* f, bgk_stream stream) {
+    if (!c || !f) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    double* scratch = c->f[1 - c->fcur];
+    bgk_status st = copy_out(c, scratch, f, sizeof(double) * c->N * c->RS, s);
+    if (st != BGK_OK) return st;
+    launch_from_canonical(c, scratch, c->f[c->fcur], s);
+    if ((st = check_launch(c)) != BGK_OK) return st;
+    return sync_check(c, s);
+}
+
+bgk_status bgk_get_positions(bgk_ctx* c, double* x, bgk_stream stream) {
+    if (!c || !x) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    bgk_status st = copy_out(c, x, c->x, sizeof(double) * c->N * c->d, s);
+    if (st != BGK_OK) return st;
+    return sync_check(c, s);
+}
+
+bgk_status bgk_get_neighbors(bgk_ctx* c, int64_t* offsets, int32_t* idx, int64_t* nnz, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    bgk_status st = sync_check(c, s);
+    if (st != BGK_OK) return st;
+    int64_t n = 0;
+    cudaMemcpy(&n, c->g.nb_off + c->N, sizeof(int64_t), cudaMemcpyDeviceToHost);
+    if (nnz) *nnz = n;
+    if (offsets && (st = copy_out(c, offsets, c->g.nb_off, sizeof(int64_t) * (c->N + 1), s)) != BGK_OK) return st;
+    if (idx && n && (st = copy_out(c, idx, c->g.nb_idx, sizeof(int32_t) * n, s)) != BGK_OK) return st;
+    return sync_check(c, s);
+}
+
+bgk_status bgk_stable_dt(bgk_ctx* c, double* dt_out, bgk_stream stream) {
+    if (!c || !dt_out) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    ensure_geometry(c, s);
+    cudaMemsetAsync(c->stab, 0, sizeof(unsigned long long), s);
+    launch_transport(c, c->f[c->fcur], c->f[1 - c->fcur], s);
+    bgk_status st = check_launch(c);
+    if (st == BGK_OK) st = sync_check(c, s);
+    if (st != BGK_OK) return st;
+    unsigned long long bits = 0;
+    cudaMemcpy(&bits, c->stab, sizeof(bits), cudaMemcpyDeviceToHost);
+    double m;
+    std::memcpy(&m, &bits, sizeof(m));
+    *dt_out = m > 0.0 ? 1.0 / m : INFINITY;
+    return BGK_OK;
+}
+
+bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
+    if (!c || !n) return BGK_E_INVALID_ARG;
+    int64_t k = 0;
+    if (c->cfg.ale) k += launches_neighbors() + launches_wls() - (c->N_b ? 0 : 1) - (c->N_int ? 0 : 1);
+    if (c->N_int) k += 3;        // transport, moment reduce, relax
+    if (c->N_b) k += 3;          // boundary interp, wall reduce, fill
+    *n = k;
+    return BGK_OK;
+}
+
+bgk_status bgk_sync(bgk_ctx* c, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    return sync_check(c, S(stream));
+}
+
+const char* bgk_last_error(bgk_ctx* c, int64_t* particle) {
+    if (!c) return "null context";
+    if (particle) *particle = c->bad;
+    return c->msg;
+}
+
+bgk_status bgk_destroy(bgk_ctx* c) {
+    delete c;
+    return BGK_OK;
+}
+
+}  // extern "C"

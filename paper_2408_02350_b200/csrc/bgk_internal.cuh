@@ -1,0 +1,135 @@
+// bgk_internal.cuh -- internal state and device helpers of the B200 BGK step.
+//
+// Internal distribution layout:
+//   f[p][k1][col][q], p = particle, k1 = 0..n1-1 index along v_1 (n1 = Nv+1),
+//   col = local velocity column (nodes sharing (j2[, j3])), q = value (g1, g2 in
+//   2D; f in 3D).  A warp's 32 lanes own 32 consecutive (chunk, column) slots
+//   of one particle and walk k1 sequentially, so every load of a neighbour row
+//   at fixed k1 is one coalesced 256-B (3D) / 512-B (2D) transaction.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/bgk.h"
+
+namespace bgk {
+
+constexpr int kPM = 5;          // moment partials per particle: s0, s_v (d), s_E  (2D: s0, s1, s2, sE, 0)
+constexpr int kMaxCellsPerAxis = 4096;
+
+struct Geo {                    // per-step geometry arrays (device)
+    int32_t* cell_of;           // [N]
+    int32_t* cell_cnt;          // [ncell]
+    int32_t* cell_start;        // [ncell+1]
+    int32_t* cell_fill;         // [ncell]
+    int32_t* cell_pts;          // [N] particles grouped by cell, ascending inside a cell
+    int32_t* nb_cnt;            // [N]
+    int64_t* nb_off;            // [N+1]
+    int32_t* nb_idx;            // [cap]
+    double* S;                  // [N][d*d]
+    double* P;                  // [cap][PD] pair data p_n, p_t[, p_b] = abar n, bbar t[, gbar b]
+    double* cw;                 // [cap] boundary interpolation weights
+    int32_t* order;             // [N_int] interior particles in cell order (transport processing order)
+};
+
+}  // namespace bgk
+
+struct bgk_ctx {
+    bgk_config cfg;
+    int d, nv, n1, ncol_g, c0, c1, ncol;
+    int64_t N, N_int, N_b, Kloc, RS;   // RS = doubles per particle row = Kloc*nv
+    int max_nb;
+    int64_t cap;
+    int nc[3];
+    int ncell;
+    double edge[3];
+    double dv, vmin;
+    int PD;                     // doubles of pair data per CSR entry
+    int R, nchunk, nslots, nwpp; // transport mapping
+    int bnd_chunk, bnd_nch;     // boundary node chunking
+    bool geometry_valid;
+    int fcur;
+    // device buffers (carved from the caller's workspace)
+    double* x;          // [N][d]
+    int8_t* kind;       // [N]
+    int32_t* interior;  // [N_int] static list of interior particles
+    int32_t* boundary;  // [N_b] static list of boundary particles
+    double* W;          // [N][d] transport velocity of the next step
+    double* macro;      // [N][d+2] recovered (rho, U, T)
+    double* f[2];       // [N][RS] double buffer
+    double* partials;   // [N][nwpp][kPM]
+    double* sums;       // [N][kPM] rank-local (then all-reduced) moment sums
+    double* wallpart;   // [N_b][bnd_nch]
+    double* wallnum;    // [N] rank-local (then all-reduced) incoming wall flux
+    double* Mw;         // [2d][RS] wall Maxwellians M(1, U_w, T_w) on the local columns
+    double* wall_den;   // [2d] sum_{v.n>0} (v.n) M_w over the GLOBAL grid
+    double* outbuf;     // [N][d+2] scratch for moments / copies
+    int64_t* err;       // [4] code, particle, needed, spare
+    unsigned long long* stab;  // [1] max_{i,k} sum_j |C_ijk| as ordered bits
+    int64_t* scan_tmp;  // [1024]
+    bgk::Geo g;
+    // host-side error state
+    char msg[256];
+    int64_t bad;
+    int64_t nnz_last;
+};
+
+namespace bgk {
+
+// ------------------------------------------------------------ device helpers
+__device__ __forceinline__ double axis_node(double vmax, double dv, int j) {
+    return -vmax + (double)j * dv;
+}
+
+// squared distance with every operation rounded, no contraction (Z22)
+template <int D>
+__device__ __forceinline__ double dist2_rn(const double* xi, const double* xj) {
+    double s = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        double t = __dsub_rn(xj[a], xi[a]);
+        s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    return s;
+}
+
+__device__ __forceinline__ void latch_error(int64_t* err, int code, int64_t particle) {
+    unsigned long long* e = reinterpret_cast<unsigned long long*>(err);
+    atomicCAS(e, 0ull, (unsigned long long)code);
+    atomicMin(reinterpret_cast<long long*>(err + 1), (long long)particle);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ---------------------------------------------------------------- launchers
+void launch_build_neighbors(bgk_ctx* c, cudaStream_t s);
+void launch_wls(bgk_ctx* c, cudaStream_t s);
+void launch_wls_export(bgk_ctx* c, double* rot, double* frames, cudaStream_t s);
+void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
+void launch_moment_reduce(bgk_ctx* c, cudaStream_t s);
+void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s);
+void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s);
+void launch_boundary_fill(bgk_ctx* c, double* fnew, cudaStream_t s);
+void launch_wall_tables(bgk_ctx* c, cudaStream_t s);
+void launch_init_f(bgk_ctx* c, const double* macro0, cudaStream_t s);
+void launch_row_moments(bgk_ctx* c, const double* f, cudaStream_t s);
+void launch_moments_finalize(bgk_ctx* c, double* out, cudaStream_t s);
+void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
+void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
+void launch_check_domain(bgk_ctx* c, cudaStream_t s);
+int transport_rows_per_thread(int d, int n1);
+int launches_neighbors();
+int launches_wls();
+
+}  // namespace bgk

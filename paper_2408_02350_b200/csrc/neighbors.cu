@@ -1,0 +1,255 @@
+// neighbors.cu -- cell-linked-list neighbour search.
+//
+// N(i) = { j != i : ((x_j-x_i)^2 + (y_j-y_i)^2) + (z_j-z_i)^2 <= h2 } with every
+// operation rounded (__dsub_rn/__dmul_rn/__dadd_rn, no FMA), ascending j, so the
+// lists are bit-identical to a brute-force O(N^2) scan with the same arithmetic.
+//
+// Pipeline (all on the caller's stream, no host sync):
+//   k_cell_assign  particle -> cell (edge >= h, 3^d sweep suffices), counts
+//   k_scan         exclusive scan of cell counts (single block)
+//   k_cell_fill    scatter particle ids into cells, k_cell_sort: ascending per cell
+//   k_compact      interior particles in cell order -> transport processing order
+//   k_nb_count     warp per particle: lanes test the 3^d cells' candidates, ballot+popc
+//   k_scan         exclusive scan of counts -> CSR offsets (int64)
+//   k_nb_fill      warp per particle: ballot compaction into shared memory, rank sort, store
+#include "bgk_internal.cuh"
+
+namespace bgk {
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+
+// exclusive scan of n int32 counts into out[0..n] (out[n] = total); one block of 1024.
+template <typename Tout>
+__global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __restrict__ in, Tout* __restrict__ out,
+                                                        int64_t n) {
+    __shared__ int64_t wsum[32];
+    const int t = threadIdx.x;
+    const int64_t chunk = (n + kScanThreads - 1) / kScanThreads;
+    const int64_t b = t * chunk, e = min(n, b + chunk);
+    int64_t local = 0;
+    for (int64_t i = b; i < e; ++i) local += in[i];
+    // block exclusive scan of `local`
+    const int lane = t & 31, wid = t >> 5;
+    int64_t v = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    if (lane == 31) wsum[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t w = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t u = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += u;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    int64_t run = v - local + (wid > 0 ? wsum[wid - 1] : 0);
+    for (int64_t i = b; i < e; ++i) {
+        out[i] = (Tout)run;
+        run += in[i];
+    }
+    if (t == kScanThreads - 1) out[n] = (Tout)(run);
+    if (n == 0 && t == 0) out[0] = 0;
+}
+
+template <int D>
+__global__ void k_cell_assign(const double* __restrict__ x, int64_t N, double L, double inv_e0, double inv_e1,
+                              double inv_e2, int nc0, int nc1, int nc2, int32_t* __restrict__ cell_of,
+                              int32_t* __restrict__ cell_cnt, int64_t* err) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double inv[3] = {inv_e0, inv_e1, inv_e2};
+    const int nc[3] = {nc0, nc1, nc2};
+    int cidx[3] = {0, 0, 0};
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        double v = x[i * D + a];
+        if (!(v >= 0.0 && v <= L)) ok = false;
+        int c = (int)floor(v * inv[a]);
+        cidx[a] = min(max(c, 0), nc[a] - 1);
+    }
+    if (!ok) latch_error(err, BGK_E_OUT_OF_DOMAIN, i);
+    int cell = (D == 3) ? (cidx[2] * nc1 + cidx[1]) * nc0 + cidx[0] : cidx[1] * nc0 + cidx[0];
+    cell_of[i] = cell;
+    atomicAdd(cell_cnt + cell, 1);
+}
+
+__global__ void k_cell_fill(int64_t N, const int32_t* __restrict__ cell_of, const int32_t* __restrict__ cell_start,
+                            int32_t* __restrict__ cell_fill, int32_t* __restrict__ cell_pts) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int c = cell_of[i];
+    int pos = cell_start[c] + atomicAdd(cell_fill + c, 1);
+    cell_pts[pos] = (int32_t)i;
+}
+
+__global__ void k_cell_sort(int ncell, const int32_t* __restrict__ cell_start, int32_t* __restrict__ cell_pts) {
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncell) return;
+    int b = cell_start[c], e = cell_start[c + 1];
+    for (int q = b + 1; q < e; ++q) {  // insertion sort, cells hold a few dozen points
+        int v = cell_pts[q], r = q - 1;
+        while (r >= b && cell_pts[r] > v) {
+            cell_pts[r + 1] = cell_pts[r];
+            --r;
+        }
+        cell_pts[r + 1] = v;
+    }
+}
+
+// order = interior particles in cell order (stable compaction, one block)
+__global__ void __launch_bounds__(kScanThreads) k_compact(const int32_t* __restrict__ cell_pts,
+                                                           const int8_t* __restrict__ kind, int64_t n,
+                                                           int32_t* __restrict__ order) {
+    __shared__ int64_t wsum[32];
+    const int t = threadIdx.x;
+    const int64_t chunk = (n + kScanThreads - 1) / kScanThreads;
+    const int64_t b = t * chunk, e = min(n, b + chunk);
+    int64_t local = 0;
+    for (int64_t i = b; i < e; ++i) local += (kind[cell_pts[i]] == 0);
+    const int lane = t & 31, wid = t >> 5;
+    int64_t v = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    if (lane == 31) wsum[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        int64_t w = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t u = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += u;
+        }
+        wsum[lane] = w;
+    }
+    __syncthreads();
+    int64_t run = v - local + (wid > 0 ? wsum[wid - 1] : 0);
+    for (int64_t i = b; i < e; ++i) {
+        int p = cell_pts[i];
+        if (kind[p] == 0) order[run++] = p;
+    }
+}
+
+template <int D, bool FILL>
+__global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, const int32_t* __restrict__ cell_of,
+                            const int32_t* __restrict__ cell_start, const int32_t* __restrict__ cell_pts, int nc0,
+                            int nc1, int nc2, int max_nb, int32_t* __restrict__ nb_cnt,
+                            const int64_t* __restrict__ nb_off, int32_t* __restrict__ nb_idx, int64_t cap,
+                            int64_t* err) {
+    extern __shared__ int32_t sbuf[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + wib;
+    if (i >= N) return;
+    int32_t* buf = sbuf + wib * max_nb;
+    double xi[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xi[a] = x[i * D + a];
+    const int cell = cell_of[i];
+    const int cx = cell % nc0, cy = (cell / nc0) % nc1, cz = (D == 3) ? cell / (nc0 * nc1) : 0;
+    int m = 0;
+    for (int dz = (D == 3 ? -1 : 0); dz <= (D == 3 ? 1 : 0); ++dz) {
+        const int z = cz + dz;
+        if (z < 0 || z >= nc2) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+            const int y = cy + dy;
+            if (y < 0 || y >= nc1) continue;
+            for (int dx = -1; dx <= 1; ++dx) {
+                const int xx = cx + dx;
+                if (xx < 0 || xx >= nc0) continue;
+                const int c = (z * nc1 + y) * nc0 + xx;
+                const int cb = cell_start[c], ce = cell_start[c + 1];
+                for (int base = cb; base < ce; base += 32) {
+                    const int t = base + lane;
+                    int j = -1;
+                    bool hit = false;
+                    if (t < ce) {
+                        j = cell_pts[t];
+                        if (j != (int)i) {
+                            double xj[3];
+#pragma unroll
+                            for (int a = 0; a < D; ++a) xj[a] = x[(int64_t)j * D + a];
+                            hit = dist2_rn<D>(xi, xj) <= h2;
+                        }
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                    if (FILL && hit) {
+                        const int slot = m + __popc(bal & ((1u << lane) - 1u));
+                        if (slot < max_nb) buf[slot] = j;
+                    }
+                    m += __popc(bal);
+                }
+            }
+        }
+    }
+    if (!FILL) {
+        if (lane == 0) {
+            nb_cnt[i] = m;
+            if (m > max_nb) latch_error(err, BGK_E_CAPACITY, i);
+        }
+        return;
+    }
+    __syncwarp();
+    const int64_t off = nb_off[i];
+    if (m > max_nb || off + m > cap) return;  // capacity error already latched / reported by host
+    for (int q = lane; q < m; q += 32) {      // rank sort: lists are short (< max_nb)
+        const int v = buf[q];
+        int rank = 0;
+        for (int r = 0; r < m; ++r) rank += (buf[r] < v);
+        nb_idx[off + rank] = v;
+    }
+}
+
+}  // namespace
+
+int launches_neighbors() { return 8; }
+
+void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
+    const int64_t N = c->N;
+    const int tpb = 256;
+    const unsigned nb = (unsigned)((N + tpb - 1) / tpb);
+    cudaMemsetAsync(c->g.cell_cnt, 0, sizeof(int32_t) * c->ncell, s);
+    cudaMemsetAsync(c->g.cell_fill, 0, sizeof(int32_t) * c->ncell, s);
+    if (c->d == 3)
+        k_cell_assign<3><<<nb, tpb, 0, s>>>(c->x, N, c->cfg.L, 1.0 / c->edge[0], 1.0 / c->edge[1], 1.0 / c->edge[2],
+                                           c->nc[0], c->nc[1], c->nc[2], c->g.cell_of, c->g.cell_cnt, c->err);
+    else
+        k_cell_assign<2><<<nb, tpb, 0, s>>>(c->x, N, c->cfg.L, 1.0 / c->edge[0], 1.0 / c->edge[1], 1.0,
+                                           c->nc[0], c->nc[1], 1, c->g.cell_of, c->g.cell_cnt, c->err);
+    k_scan<int32_t><<<1, kScanThreads, 0, s>>>(c->g.cell_cnt, c->g.cell_start, c->ncell);
+    k_cell_fill<<<nb, tpb, 0, s>>>(N, c->g.cell_of, c->g.cell_start, c->g.cell_fill, c->g.cell_pts);
+    k_cell_sort<<<(c->ncell + 127) / 128, 128, 0, s>>>(c->ncell, c->g.cell_start, c->g.cell_pts);
+    k_compact<<<1, kScanThreads, 0, s>>>(c->g.cell_pts, c->kind, N, c->g.order);
+    const int wpb = 8;
+    const unsigned nbw = (unsigned)((N + wpb - 1) / wpb);
+    const size_t smem = sizeof(int32_t) * wpb * c->max_nb;
+    if (c->d == 3) {
+        k_neighbors<3, false><<<nbw, wpb * 32, 0, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
+                                                      c->g.cell_pts, c->nc[0], c->nc[1], c->nc[2], c->max_nb,
+                                                      c->g.nb_cnt, nullptr, nullptr, c->cap, c->err);
+        k_scan<int64_t><<<1, kScanThreads, 0, s>>>(c->g.nb_cnt, c->g.nb_off, N);
+        k_neighbors<3, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
+                                                        c->g.cell_pts, c->nc[0], c->nc[1], c->nc[2], c->max_nb,
+                                                        c->g.nb_cnt, c->g.nb_off, c->g.nb_idx, c->cap, c->err);
+    } else {
+        k_neighbors<2, false><<<nbw, wpb * 32, 0, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
+                                                      c->g.cell_pts, c->nc[0], c->nc[1], 1, c->max_nb,
+                                                      c->g.nb_cnt, nullptr, nullptr, c->cap, c->err);
+        k_scan<int64_t><<<1, kScanThreads, 0, s>>>(c->g.nb_cnt, c->g.nb_off, N);
+        k_neighbors<2, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
+                                                        c->g.cell_pts, c->nc[0], c->nc[1], 1, c->max_nb,
+                                                        c->g.nb_cnt, c->g.nb_off, c->g.nb_idx, c->cap, c->err);
+    }
+}
+
+}  // namespace bgk

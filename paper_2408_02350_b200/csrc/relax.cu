@@ -1,0 +1,542 @@
+// relax.cu -- moment recovery, local Maxwellian, implicit BGK relaxation, ALE
+// motion, diffuse-reflection walls, initial state and diagnostics moments.
+//
+//  k_moment_reduce : per-particle sum of the transport warps' partials (fixed order)
+//  k_relax         : rho, U, T from the (all-reduced) sums,
+//                    tau, M^{n+1} inline as a product of three 1D Gaussian
+//                    factors (P:46-49 / P:98-105 with Z1, Z2),
+//                    f^{n+1} = (tau ftilde + dt M)/(tau + dt),
+//                    W <- U^{n+1}, x += dt U^{n+1} clamped
+//  k_bnd_interp    : incoming half of each boundary row by WLS interpolation of the
+//                    interior f^{n+1} (Z17, Z19) + rank-local incoming wall flux partials
+//  k_wall_reduce   : per boundary particle, fixed-order sum of the flux partials
+//  k_bnd_fill      : rho_w = -flux_in / sum_{v.n>0}(v.n) M_w ; outgoing half = rho_w M_w
+#include "bgk_internal.cuh"
+
+namespace bgk {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int q = 0; q < NT / 32; ++q) t += sh[q];   // fixed order
+    return t;                                            // valid in thread 0
+}
+
+// node velocity components of local node t = k1 * ncol + col
+template <int D>
+__device__ __forceinline__ void node_vel(int t, int ncol, int c0, int n1, double vmax, double dv, double (&v)[3],
+                                         int (&kk)[3]) {
+    const int k1 = t / ncol, col = t - k1 * ncol, gc = c0 + col;
+    kk[0] = k1;
+    if constexpr (D == 3) {
+        kk[1] = gc / n1;
+        kk[2] = gc - kk[1] * n1;
+    } else {
+        kk[1] = gc;
+        kk[2] = 0;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) v[a] = (a < D) ? axis_node(vmax, dv, kk[a]) : 0.0;
+}
+
+__global__ void k_moment_reduce(const int32_t* __restrict__ ids, int64_t n, const double* __restrict__ partials,
+                                int nwpp, double* __restrict__ sums) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int p = ids[t];
+    double acc[kPM] = {0, 0, 0, 0, 0};
+    for (int w = 0; w < nwpp; ++w)
+#pragma unroll
+        for (int q = 0; q < kPM; ++q) acc[q] += partials[((int64_t)p * nwpp + w) * kPM + q];
+#pragma unroll
+    for (int q = 0; q < kPM; ++q) sums[(int64_t)p * kPM + q] = acc[q];
+}
+
+struct RelaxArgs {
+    const int32_t* ids;
+    const double* sums;
+    double* f;       // ftilde in, f^{n+1} out (in place)
+    double* macro;
+    double* W;
+    double* x;
+    int64_t* err;
+    int64_t n;
+    int n1, ncol, c0, Kloc, ale;
+    double vmax, dv, dt, R, kb, dmol, L, clamp_eps;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    __shared__ double e[D][64];
+    __shared__ double par[8];
+    const int64_t bi = blockIdx.x;
+    if (bi >= A.n) return;
+    const int p = A.ids[bi];
+    if (threadIdx.x == 0) {
+        const double* s = A.sums + (int64_t)p * kPM;
+        double dvd = A.dv * A.dv;
+        if (D == 3) dvd *= A.dv;
+        const double rho = s[0] * dvd;
+        double U[D], uu = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { U[a] = s[1 + a] / s[0]; uu += U[a] * U[a]; }
+        const double e3 = s[1 + D] * dvd - rho * uu;          // 3 rho R T
+        const double T = e3 / (3.0 * rho * A.R);
+        bool bad = !(rho > 0.0) || !(T > 1e-12);
+        if (bad) latch_error(A.err, BGK_E_DEGENERATE_STATE, p);
+        const double RT = A.R * T;
+        const double lambda = A.kb / (sqrt(2.0) * kPi * rho * A.R * A.dmol * A.dmol);
+        const double Cbar = sqrt(8.0 * RT / kPi);
+        const double tau = 4.0 * lambda / (kPi * Cbar);
+        const double inv = 1.0 / (tau + A.dt);
+        const double twoPiRT = 2.0 * kPi * RT;
+        const double pref = (D == 3) ? rho / (twoPiRT * sqrt(twoPiRT)) : rho / twoPiRT;
+        par[0] = bad ? 1.0 : tau * inv;   // a1: degenerate rows are left as ftilde
+        par[1] = bad ? 0.0 : A.dt * inv;  // a2
+        par[2] = pref;
+        par[3] = RT;
+        par[4] = 1.0 / (2.0 * RT);
+#pragma unroll
+        for (int a = 0; a < D; ++a) par[5 + a] = U[a];
+        double* mo = A.macro + (int64_t)p * (D + 2);
+        mo[0] = rho;
+#pragma unroll
+        for (int a = 0; a < D; ++a) mo[1 + a] = U[a];
+        mo[1 + D] = T;
+        if (A.ale && !bad) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                A.W[(int64_t)p * D + a] = U[a];
+                double xn = A.x[(int64_t)p * D + a] + A.dt * U[a];
+                xn = fmin(fmax(xn, A.clamp_eps), A.L - A.clamp_eps);
+                A.x[(int64_t)p * D + a] = xn;
+            }
+        }
+    }
+    __syncthreads();
+    const double inv2RT = par[4];
+    for (int t = threadIdx.x; t < D * A.n1; t += blockDim.x) {
+        const int a = t / A.n1, j = t - a * A.n1;
+        const double dvel = axis_node(A.vmax, A.dv, j) - par[5 + a];
+        e[a][j] = exp(-dvel * dvel * inv2RT);
+    }
+    __syncthreads();
+    const double a1 = par[0], a2 = par[1], pref = par[2], RT = par[3];
+    double* fp = A.f + (int64_t)p * A.Kloc * NV;
+    for (int t = threadIdx.x; t < A.Kloc; t += blockDim.x) {
+        const int k1 = t / A.ncol, col = t - k1 * A.ncol, gc = A.c0 + col;
+        double M;
+        if constexpr (D == 3) {
+            const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+            M = pref * e[0][k1] * e[1][k2] * e[2][k3];
+            fp[t] = a1 * fp[t] + a2 * M;
+        } else {
+            M = pref * e[0][k1] * e[1][gc];
+            double2 g = reinterpret_cast<double2*>(fp)[t];
+            g.x = a1 * g.x + a2 * M;
+            g.y = a1 * g.y + a2 * (RT * M);
+            reinterpret_cast<double2*>(fp)[t] = g;
+        }
+    }
+}
+
+// Maxwellian M(rho, U, T) (2D: (G1, G2)) at node velocity v
+template <int D>
+__device__ __forceinline__ void maxwellian_at(double rho, const double* U, double T, double R, const double (&v)[3],
+                                              double (&out)[2]) {
+    const double RT = R * T;
+    double q = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) q += (v[a] - U[a]) * (v[a] - U[a]);
+    const double twoPiRT = 2.0 * kPi * RT;
+    const double pref = (D == 3) ? rho / (twoPiRT * sqrt(twoPiRT)) : rho / twoPiRT;
+    out[0] = pref * exp(-q / (2.0 * RT));
+    out[1] = RT * out[0];
+}
+
+template <int D>
+__global__ void k_init_f(const double* __restrict__ macro0, int64_t N, double* __restrict__ f,
+                         double* __restrict__ macro, double* __restrict__ W, int ale, int n1, int ncol, int c0,
+                         int64_t Kloc, double vmax, double dv, double R, double Twall) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    const int64_t p = blockIdx.x;
+    if (p >= N) return;
+    double rho = 1.0, U[3] = {0, 0, 0}, T = Twall;
+    if (macro0) {
+        rho = macro0[p * (D + 2)];
+#pragma unroll
+        for (int a = 0; a < D; ++a) U[a] = macro0[p * (D + 2) + 1 + a];
+        T = macro0[p * (D + 2) + 1 + D];
+    }
+    if (threadIdx.x == 0) {
+        macro[p * (D + 2)] = rho;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            macro[p * (D + 2) + 1 + a] = U[a];
+            W[p * D + a] = ale ? U[a] : 0.0;
+        }
+        macro[p * (D + 2) + 1 + D] = T;
+    }
+    for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
+        double v[3];
+        int kk[3];
+        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+        double M[2];
+        maxwellian_at<D>(rho, U, T, R, v, M);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) f[(p * Kloc + t) * NV + q] = M[q];
+    }
+}
+
+// wall tables: Mw[w][local node] = M(1, U_w, T_w); den[w] = sum over the GLOBAL grid of
+// (v.n)^+ M_w (2D: G1), identical on every rank.
+template <int D>
+__global__ void k_wall_M(double* __restrict__ Mw, int n1, int ncol, int c0, int64_t Kloc, double vmax, double dv,
+                         double R, double Twall, double lid0, double lid1, double lid2) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    const int wid = blockIdx.y + 1;
+    const double U[3] = {wid == 2 * D ? lid0 : 0.0, wid == 2 * D ? lid1 : 0.0, wid == 2 * D ? lid2 : 0.0};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Kloc; t += (int64_t)gridDim.x * blockDim.x) {
+        double v[3];
+        int kk[3];
+        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+        double M[2];
+        maxwellian_at<D>(1.0, U, Twall, R, v, M);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) Mw[((int64_t)blockIdx.y * Kloc + t) * NV + q] = M[q];
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_wall_den(double* __restrict__ den, int n1, int ncol_g, double vmax,
+                                                  double dv, double R, double Twall, double lid0, double lid1,
+                                                  double lid2, int64_t* err) {
+    __shared__ double sh[32];
+    const int wid = blockIdx.x + 1;
+    const int axis = (wid - 1) / 2;
+    const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
+    const double U[3] = {wid == 2 * D ? lid0 : 0.0, wid == 2 * D ? lid1 : 0.0, wid == 2 * D ? lid2 : 0.0};
+    const int64_t K = (int64_t)n1 * ncol_g;
+    double acc = 0.0;
+    for (int64_t t = threadIdx.x; t < K; t += blockDim.x) {
+        double v[3];
+        int kk[3];
+        node_vel<D>((int)t, ncol_g, 0, n1, vmax, dv, v, kk);
+        const double vn = sgn * v[axis];
+        if (vn > 0.0) {
+            double M[2];
+            maxwellian_at<D>(1.0, U, Twall, R, v, M);
+            acc += vn * M[0];
+        }
+    }
+    const double tot = block_sum<256>(acc, sh);
+    if (threadIdx.x == 0) {
+        den[blockIdx.x] = tot;
+        if (!(tot > 0.0)) latch_error(err, BGK_E_WALL, -1);
+    }
+}
+
+constexpr int kBndChunk = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restrict__ bids, const int8_t* __restrict__ kind,
+                                                          const int64_t* __restrict__ nb_off,
+                                                          const int32_t* __restrict__ nb_idx,
+                                                          const double* __restrict__ cw, double* __restrict__ f,
+                                                          double* __restrict__ wallpart, int nch, int n1, int ncol,
+                                                          int c0, int64_t Kloc, double vmax, double dv) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    __shared__ double sh[32];
+    const int bi = blockIdx.x;
+    const int b = bids[bi];
+    const int wid = kind[b];
+    const int axis = (wid - 1) / 2;
+    const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
+    const int64_t t = (int64_t)blockIdx.y * kBndChunk + threadIdx.x;
+    const bool in_range = t < Kloc;
+    double vn = 1.0;
+    if (in_range) {
+        double v[3];
+        int kk[3];
+        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+        vn = sgn * v[axis];
+    }
+    const bool incoming = in_range && vn <= 0.0;
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+    const int64_t off = nb_off[b], end = nb_off[b + 1];
+    for (int64_t e = off; e < end; ++e) {
+        const double c = __ldg(cw + e);
+        if (c == 0.0) continue;                     // boundary neighbours carry zero weight (uniform)
+        const int64_t j = __ldg(nb_idx + e);
+        if (incoming) {
+            if constexpr (NV == 1) {
+                acc[0] = fma(c, __ldg(f + j * Kloc + t), acc[0]);
+            } else {
+                const double2 g = __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t);
+                acc[0] = fma(c, g.x, acc[0]);
+                acc[1] = fma(c, g.y, acc[1]);
+            }
+        }
+    }
+    double flux = 0.0;
+    if (incoming) {
+        if constexpr (NV == 1) f[(int64_t)b * Kloc + t] = acc[0];
+        else reinterpret_cast<double2*>(f)[(int64_t)b * Kloc + t] = make_double2(acc[0], acc[1]);
+        if (vn < 0.0) flux = vn * acc[0];
+    }
+    const double tot = block_sum<kBndChunk>(flux, sh);
+    if (threadIdx.x == 0) wallpart[(int64_t)bi * nch + blockIdx.y] = tot;
+}
+
+__global__ void k_wall_reduce(const int32_t* __restrict__ bids, int64_t nb, const double* __restrict__ wallpart,
+                              int nch, double* __restrict__ wallnum) {
+    const int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (bi >= nb) return;
+    double s = 0.0;
+    for (int q = 0; q < nch; ++q) s += wallpart[bi * nch + q];
+    wallnum[bids[bi]] = s;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kBndChunk) k_bnd_fill(const int32_t* __restrict__ bids, const int8_t* __restrict__ kind,
+                                                        const double* __restrict__ wallnum,
+                                                        const double* __restrict__ den, const double* __restrict__ Mw,
+                                                        double* __restrict__ f, int n1, int ncol, int c0, int64_t Kloc,
+                                                        double vmax, double dv) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    const int b = bids[blockIdx.x];
+    const int wid = kind[b];
+    const int axis = (wid - 1) / 2;
+    const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
+    const int64_t t = (int64_t)blockIdx.y * kBndChunk + threadIdx.x;
+    if (t >= Kloc) return;
+    double v[3];
+    int kk[3];
+    node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+    if (!(sgn * v[axis] > 0.0)) return;
+    const double rho_w = -wallnum[b] / den[wid - 1];
+    const double* M = Mw + ((int64_t)(wid - 1) * Kloc + t) * NV;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) f[((int64_t)b * Kloc + t) * NV + q] = rho_w * M[q];
+}
+
+// moments of every row (diagnostics, bgk_moments): sums[p] = (s0, s_v, s_E[+g2])
+template <int D>
+__global__ void __launch_bounds__(256) k_row_moments(const double* __restrict__ f, int64_t N, double* __restrict__ sums,
+                                                     int n1, int ncol, int c0, int64_t Kloc, double vmax, double dv) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    __shared__ double sh[32];
+    const int64_t p = blockIdx.x;
+    if (p >= N) return;
+    double s[kPM] = {0, 0, 0, 0, 0};
+    for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
+        double v[3];
+        int kk[3];
+        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+        const double g = f[(p * Kloc + t) * NV];
+        s[0] += g;
+#pragma unroll
+        for (int a = 0; a < D; ++a) s[1 + a] += v[a] * g;
+        double vv = 0.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) vv += v[a] * v[a];
+        s[1 + D] += vv * g;
+        if constexpr (NV == 2) s[1 + D] += f[(p * Kloc + t) * NV + 1];
+    }
+#pragma unroll
+    for (int q = 0; q < kPM; ++q) {
+        const double tot = block_sum<256>(s[q], sh);
+        if (threadIdx.x == 0) sums[p * kPM + q] = tot;
+    }
+}
+
+template <int D>
+__global__ void k_moments_finalize(const double* __restrict__ sums, int64_t N, double dv, double R,
+                                   double* __restrict__ out, int64_t* err) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= N) return;
+    const double* s = sums + p * kPM;
+    double dvd = dv * dv;
+    if (D == 3) dvd *= dv;
+    const double rho = s[0] * dvd;
+    double uu = 0.0;
+    double* o = out + p * (D + 2);
+    o[0] = rho;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const double u = s[1 + a] / s[0];
+        o[1 + a] = u;
+        uu += u * u;
+    }
+    const double T = (s[1 + D] * dvd - rho * uu) / (3.0 * rho * R);
+    o[1 + D] = T;
+    if (!(rho > 0.0) || !(T > 1e-12)) latch_error(err, BGK_E_DEGENERATE_STATE, p);
+}
+
+// internal [p][k1][col][q]  <->  canonical [p][q][k1][col]
+template <bool TO_CANON>
+__global__ void k_transpose2(const double* __restrict__ in, double* __restrict__ out, int64_t N, int64_t Kloc) {
+    const int64_t total = N * Kloc;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = t / Kloc, k = t - p * Kloc;
+        if (TO_CANON) {
+            out[(p * 2 + 0) * Kloc + k] = in[t * 2 + 0];
+            out[(p * 2 + 1) * Kloc + k] = in[t * 2 + 1];
+        } else {
+            out[t * 2 + 0] = in[(p * 2 + 0) * Kloc + k];
+            out[t * 2 + 1] = in[(p * 2 + 1) * Kloc + k];
+        }
+    }
+}
+
+template <int D>
+__global__ void k_check_domain(const double* __restrict__ x, int64_t N, double L, int64_t* err) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        const double v = x[i * D + a];
+        if (!(v >= 0.0 && v <= L)) latch_error(err, BGK_E_OUT_OF_DOMAIN, i);
+    }
+}
+
+}  // namespace
+
+void launch_moment_reduce(bgk_ctx* c, cudaStream_t s) {
+    if (!c->N_int) return;
+    k_moment_reduce<<<(unsigned)((c->N_int + 255) / 256), 256, 0, s>>>(c->interior, c->N_int, c->partials, c->nwpp,
+                                                                        c->sums);
+}
+
+void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
+    if (!c->N_int) return;
+    RelaxArgs a;
+    a.ids = c->interior;
+    a.sums = c->sums;
+    a.f = fnew;
+    a.macro = c->macro;
+    a.W = c->W;
+    a.x = c->x;
+    a.err = c->err;
+    a.n = c->N_int;
+    a.n1 = c->n1;
+    a.ncol = c->ncol;
+    a.c0 = c->c0;
+    a.Kloc = (int)c->Kloc;
+    a.ale = c->cfg.ale;
+    a.vmax = c->cfg.vmax;
+    a.dv = c->dv;
+    a.dt = c->cfg.dt;
+    a.R = c->cfg.R;
+    a.kb = c->cfg.kb;
+    a.dmol = c->cfg.dmol;
+    a.L = c->cfg.L;
+    a.clamp_eps = 1e-3 * c->cfg.dx;
+    if (c->d == 3) k_relax<3><<<(unsigned)c->N_int, 256, 0, s>>>(a);
+    else k_relax<2><<<(unsigned)c->N_int, 256, 0, s>>>(a);
+}
+
+void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
+    if (!c->N_b) return;
+    dim3 g((unsigned)c->N_b, (unsigned)c->bnd_nch);
+    if (c->d == 3)
+        k_bnd_interp<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw, fnew,
+                                                c->wallpart, c->bnd_nch, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
+                                                c->dv);
+    else
+        k_bnd_interp<2><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw, fnew,
+                                                c->wallpart, c->bnd_nch, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
+                                                c->dv);
+    k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart, c->bnd_nch,
+                                                                    c->wallnum);
+}
+
+void launch_boundary_fill(bgk_ctx* c, double* fnew, cudaStream_t s) {
+    if (!c->N_b) return;
+    dim3 g((unsigned)c->N_b, (unsigned)c->bnd_nch);
+    if (c->d == 3)
+        k_bnd_fill<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->wallnum, c->wall_den, c->Mw, fnew, c->n1,
+                                              c->ncol, c->c0, c->Kloc, c->cfg.vmax, c->dv);
+    else
+        k_bnd_fill<2><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->wallnum, c->wall_den, c->Mw, fnew, c->n1,
+                                              c->ncol, c->c0, c->Kloc, c->cfg.vmax, c->dv);
+}
+
+void launch_wall_tables(bgk_ctx* c, cudaStream_t s) {
+    const bgk_config& k = c->cfg;
+    const int nw = 2 * c->d;
+    dim3 g((unsigned)std::min<int64_t>((c->Kloc + 255) / 256, 4096), (unsigned)nw);
+    if (c->d == 3) {
+        k_wall_M<3><<<g, 256, 0, s>>>(c->Mw, c->n1, c->ncol, c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall,
+                                      k.U_lid[0], k.U_lid[1], k.U_lid[2]);
+        k_wall_den<3><<<nw, 256, 0, s>>>(c->wall_den, c->n1, c->ncol_g, k.vmax, c->dv, k.R, k.T_wall, k.U_lid[0],
+                                         k.U_lid[1], k.U_lid[2], c->err);
+    } else {
+        k_wall_M<2><<<g, 256, 0, s>>>(c->Mw, c->n1, c->ncol, c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall,
+                                      k.U_lid[0], k.U_lid[1], k.U_lid[2]);
+        k_wall_den<2><<<nw, 256, 0, s>>>(c->wall_den, c->n1, c->ncol_g, k.vmax, c->dv, k.R, k.T_wall, k.U_lid[0],
+                                         k.U_lid[1], k.U_lid[2], c->err);
+    }
+}
+
+void launch_init_f(bgk_ctx* c, const double* macro0, cudaStream_t s) {
+    const bgk_config& k = c->cfg;
+    if (c->d == 3)
+        k_init_f<3><<<(unsigned)c->N, 256, 0, s>>>(macro0, c->N, c->f[c->fcur], c->macro, c->W, k.ale, c->n1, c->ncol,
+                                                   c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall);
+    else
+        k_init_f<2><<<(unsigned)c->N, 256, 0, s>>>(macro0, c->N, c->f[c->fcur], c->macro, c->W, k.ale, c->n1, c->ncol,
+                                                   c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall);
+}
+
+void launch_row_moments(bgk_ctx* c, const double* f, cudaStream_t s) {
+    if (c->d == 3)
+        k_row_moments<3><<<(unsigned)c->N, 256, 0, s>>>(f, c->N, c->sums, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
+                                                        c->dv);
+    else
+        k_row_moments<2><<<(unsigned)c->N, 256, 0, s>>>(f, c->N, c->sums, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
+                                                        c->dv);
+}
+
+void launch_moments_finalize(bgk_ctx* c, double* out, cudaStream_t s) {
+    const unsigned g = (unsigned)((c->N + 255) / 256);
+    if (c->d == 3) k_moments_finalize<3><<<g, 256, 0, s>>>(c->sums, c->N, c->dv, c->cfg.R, out, c->err);
+    else k_moments_finalize<2><<<g, 256, 0, s>>>(c->sums, c->N, c->dv, c->cfg.R, out, c->err);
+}
+
+void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
+    if (c->nv == 1) {
+        cudaMemcpyAsync(fout, fin, sizeof(double) * c->N * c->RS, cudaMemcpyDeviceToDevice, s);
+        return;
+    }
+    k_transpose2<true><<<4096, 256, 0, s>>>(fin, fout, c->N, c->Kloc);
+}
+
+void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
+    if (c->nv == 1) {
+        cudaMemcpyAsync(fout, fin, sizeof(double) * c->N * c->RS, cudaMemcpyDeviceToDevice, s);
+        return;
+    }
+    k_transpose2<false><<<4096, 256, 0, s>>>(fin, fout, c->N, c->Kloc);
+}
+
+void launch_check_domain(bgk_ctx* c, cudaStream_t s) {
+    const unsigned g = (unsigned)((c->N + 255) / 256);
+    if (c->d == 3) k_check_domain<3><<<g, 256, 0, s>>>(c->x, c->N, c->cfg.L, c->err);
+    else k_check_domain<2><<<g, 256, 0, s>>>(c->x, c->N, c->cfg.L, c->err);
+}
+
+}  // namespace bgk

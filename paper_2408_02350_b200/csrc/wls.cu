@@ -1,0 +1,311 @@
+// wls.cu -- batched weighted-least-squares stencil coefficients
+// and the rotated upwind coefficients of the positive scheme.
+//
+// One warp per particle.  Lanes stride over the particle's neighbours to build
+// the small normal matrix A = sum_j w_j d_j d_j^T (2x2 / 3x3), a butterfly
+// reduction gives every lane the same A, every lane inverts it (Gauss-Jordan,
+// partial pivoting) and tests it (Jacobi eigenvalues, lambda_min < 1e-12
+// lambda_max -> deficient), then lanes stride over the pairs again
+// and write the pair data the transport kernel consumes:
+//     a_j = w_j S d_j,  frame (n, t[, b]) of d_j (trig-free form of P:400 / P:420-431,
+//     with (cos phi, sin phi) = (1, 0) when dx = dy = 0, Z10),
+//     rot = (a.n, a.t[, a.b])  (Z8),
+//     P[e] = (abar n, bbar t[, gbar b])   -- so the flux coefficient is
+//     C = sum_e (P_e.c - |P_e.c|)  (abar > 0; P:408-410, P:476-480 with Z5-Z7).
+// Offsets are scaled by 1/h inside the solve so the matrices are O(1).
+// Boundary particles get linear-WLS interpolation weights over their interior
+// neighbours (Z19): c_bj = w_j e0^T B^{-1} (1, d_j/h), B = sum w (1, d/h)(1, d/h)^T.
+#include "bgk_internal.cuh"
+
+namespace bgk {
+
+namespace {
+
+template <int n>
+__device__ bool small_inverse(const double (&A)[n][n], double (&Ai)[n][n]) {
+    double M[n][2 * n];
+#pragma unroll
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int q = 0; q < 2 * n; ++q) M[r][q] = q < n ? A[r][q] : (q - n == r ? 1.0 : 0.0);
+#pragma unroll
+    for (int col = 0; col < n; ++col) {
+        int piv = col;
+        double best = fabs(M[col][col]);
+#pragma unroll
+        for (int r = col + 1; r < n; ++r)
+            if (fabs(M[r][col]) > best) { best = fabs(M[r][col]); piv = r; }
+        if (best == 0.0) return false;
+        if (piv != col) {
+#pragma unroll
+            for (int r = col + 1; r < n; ++r)
+                if (r == piv)
+#pragma unroll
+                    for (int q = 0; q < 2 * n; ++q) { double t = M[col][q]; M[col][q] = M[r][q]; M[r][q] = t; }
+        }
+        const double ip = 1.0 / M[col][col];
+#pragma unroll
+        for (int q = 0; q < 2 * n; ++q) M[col][q] *= ip;
+#pragma unroll
+        for (int r = 0; r < n; ++r) {
+            if (r == col) continue;
+            const double fct = M[r][col];
+#pragma unroll
+            for (int q = 0; q < 2 * n; ++q) M[r][q] -= fct * M[col][q];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int q = 0; q < n; ++q) Ai[r][q] = M[r][n + q];
+    return true;
+}
+
+// lambda_min / lambda_max of a symmetric n x n matrix by cyclic Jacobi sweeps
+template <int n>
+__device__ bool well_conditioned(const double (&A)[n][n]) {
+    double a[n][n];
+#pragma unroll
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int q = 0; q < n; ++q) a[r][q] = A[r][q];
+    for (int sweep = 0; sweep < 12; ++sweep) {
+        double off = 0.0, dia = 0.0;
+#pragma unroll
+        for (int r = 0; r < n; ++r)
+#pragma unroll
+            for (int q = 0; q < n; ++q) (r == q ? dia : off) += a[r][q] * a[r][q];
+        if (off <= 1e-40 * dia) break;
+#pragma unroll
+        for (int p = 0; p < n; ++p)
+#pragma unroll
+            for (int q = p + 1; q < n; ++q) {
+                if (a[p][q] == 0.0) continue;
+                const double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+                const double t = copysign(1.0, th) / (fabs(th) + sqrt(th * th + 1.0));
+                const double cs = rsqrt(t * t + 1.0), sn = t * cs;
+#pragma unroll
+                for (int k = 0; k < n; ++k) {
+                    const double akp = a[k][p], akq = a[k][q];
+                    a[k][p] = cs * akp - sn * akq;
+                    a[k][q] = sn * akp + cs * akq;
+                }
+#pragma unroll
+                for (int k = 0; k < n; ++k) {
+                    const double apk = a[p][k], aqk = a[q][k];
+                    a[p][k] = cs * apk - sn * aqk;
+                    a[q][k] = sn * apk + cs * aqk;
+                }
+            }
+    }
+    double lo = a[0][0], hi = a[0][0];
+#pragma unroll
+    for (int r = 1; r < n; ++r) { lo = fmin(lo, a[r][r]); hi = fmax(hi, a[r][r]); }
+    return hi > 0.0 && lo >= 1e-12 * hi;
+}
+
+// frame rows of direction d (any scale): F[0] = n, F[1] = t, F[2] = b
+template <int D>
+__device__ __forceinline__ void frame_of(const double (&d)[D], double (&F)[D][D]) {
+    if constexpr (D == 2) {
+        const double r = sqrt(d[0] * d[0] + d[1] * d[1]);
+        const double cp = d[0] / r, sp = d[1] / r;
+        F[0][0] = cp;  F[0][1] = sp;
+        F[1][0] = -sp; F[1][1] = cp;
+    } else {
+        const double rxy2 = d[0] * d[0] + d[1] * d[1];
+        const double rxy = sqrt(rxy2);
+        const double r = sqrt(rxy2 + d[D - 1] * d[D - 1]);
+        double cp = 1.0, sp = 0.0;                  // Z10: phi = atan2(+0,+0) = 0
+        if (rxy > 0.0) { cp = d[0] / rxy; sp = d[1] / rxy; }
+        const double ct = d[D - 1] / r, st = rxy / r;
+        double* f = &F[0][0];
+        f[0] = st * cp; f[1] = st * sp; f[2] = ct;       // n
+        f[3] = ct * cp; f[4] = ct * sp; f[5] = -st;      // t
+        f[6] = -sp;     f[7] = cp;      f[8] = 0.0;      // b
+    }
+}
+
+template <int D>
+__global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __restrict__ ids, int64_t n_ids,
+                               const int64_t* __restrict__ nb_off, const int32_t* __restrict__ nb_idx, double h,
+                               double h2, double alpha, double* __restrict__ S_out, double* __restrict__ P,
+                               double* __restrict__ rot_out, double* __restrict__ frame_out, int64_t* err) {
+    constexpr int PD = (D == 2) ? 4 : 10;
+    const int lane = threadIdx.x & 31;
+    const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= n_ids) return;
+    const int p = ids[w];
+    const int64_t off = nb_off[p];
+    const int m = (int)(nb_off[p + 1] - off);
+    const double inv_h = 1.0 / h;
+    double xi[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xi[a] = x[(int64_t)p * D + a];
+    double A[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int q = 0; q < D; ++q) A[r][q] = 0.0;
+    for (int e = lane; e < m; e += 32) {
+        const int j = nb_idx[off + e];
+        double xj[D], dd[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; dd[a] = (xj[a] - xi[a]) * inv_h; }
+        const double wgt = exp(-alpha * dist2_rn<D>(xi, xj) / h2);
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int q = 0; q < D; ++q) A[r][q] += wgt * dd[r] * dd[q];
+    }
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int q = 0; q < D; ++q) A[r][q] = warp_sum(A[r][q]);
+    double Si[D][D];
+    bool ok = (m >= D + 2) && well_conditioned<D>(A) && small_inverse<D>(A, Si);
+    if (!ok) {
+        if (lane == 0) latch_error(err, BGK_E_DEFICIENT_STENCIL, p);
+        return;
+    }
+    if (lane == 0 && S_out) {
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int q = 0; q < D; ++q) S_out[(int64_t)p * D * D + r * D + q] = Si[r][q] * inv_h * inv_h;
+    }
+    for (int e = lane; e < m; e += 32) {
+        const int j = nb_idx[off + e];
+        double xj[D], dd[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; dd[a] = (xj[a] - xi[a]) * inv_h; }
+        const double wgt = exp(-alpha * dist2_rn<D>(xi, xj) / h2);
+        double av[D];   // a_j = w_j S d_j, physical units 1/m
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) s += Si[r][q] * dd[q];
+            av[r] = wgt * s * inv_h;
+        }
+        double F[D][D];
+        frame_of<D>(dd, F);
+        double rot[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) s += av[a] * F[k][a];
+            rot[k] = s;
+        }
+        double* pe = P + (off + e) * PD;
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+#pragma unroll
+            for (int a = 0; a < D; ++a) pe[k * D + a] = rot[k] * F[k][a];
+        if (PD > D * D) pe[PD - 1] = 0.0;
+        if (rot_out) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) rot_out[(off + e) * D + k] = rot[k];
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+#pragma unroll
+                for (int a = 0; a < D; ++a) frame_out[(off + e) * D * D + k * D + a] = F[k][a];
+        }
+    }
+}
+
+template <int D>
+__global__ void k_wls_boundary(const double* __restrict__ x, const int8_t* __restrict__ kind,
+                               const int32_t* __restrict__ ids, int64_t n_ids, const int64_t* __restrict__ nb_off,
+                               const int32_t* __restrict__ nb_idx, double h, double h2, double alpha,
+                               double* __restrict__ cw, int64_t* err) {
+    constexpr int n = D + 1;
+    const int lane = threadIdx.x & 31;
+    const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= n_ids) return;
+    const int b = ids[w];
+    const int64_t off = nb_off[b];
+    const int m = (int)(nb_off[b + 1] - off);
+    const double inv_h = 1.0 / h;
+    double xb[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) xb[a] = x[(int64_t)b * D + a];
+    double B[n][n];
+#pragma unroll
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int q = 0; q < n; ++q) B[r][q] = 0.0;
+    int mi = 0;
+    for (int e = lane; e < m; e += 32) {
+        const int j = nb_idx[off + e];
+        if (kind[j] != 0) continue;
+        ++mi;
+        double xj[D], Pv[n];
+        Pv[0] = 1.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; Pv[1 + a] = (xj[a] - xb[a]) * inv_h; }
+        const double wgt = exp(-alpha * dist2_rn<D>(xb, xj) / h2);
+#pragma unroll
+        for (int r = 0; r < n; ++r)
+#pragma unroll
+            for (int q = 0; q < n; ++q) B[r][q] += wgt * Pv[r] * Pv[q];
+    }
+    mi = warp_sum(mi);
+#pragma unroll
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int q = 0; q < n; ++q) B[r][q] = warp_sum(B[r][q]);
+    double Bi[n][n];
+    const bool ok = (mi >= D + 2) && well_conditioned<n>(B) && small_inverse<n>(B, Bi);
+    if (!ok) {
+        if (lane == 0) latch_error(err, BGK_E_DEFICIENT_STENCIL, b);
+        return;
+    }
+    for (int e = lane; e < m; e += 32) {
+        const int j = nb_idx[off + e];
+        double c = 0.0;
+        if (kind[j] == 0) {
+            double xj[D], Pv[n];
+            Pv[0] = 1.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; Pv[1 + a] = (xj[a] - xb[a]) * inv_h; }
+            const double wgt = exp(-alpha * dist2_rn<D>(xb, xj) / h2);
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < n; ++q) s += Bi[0][q] * Pv[q];
+            c = wgt * s;
+        }
+        cw[off + e] = c;
+    }
+}
+
+}  // namespace
+
+int launches_wls() { return 2; }
+
+static void run_wls(bgk_ctx* c, double* rot, double* frames, cudaStream_t s) {
+    const int wpb = 4;
+    const unsigned gi = (unsigned)((c->N_int + wpb - 1) / wpb);
+    const unsigned gb = (unsigned)((c->N_b + wpb - 1) / wpb);
+    const double h = c->cfg.h, h2 = c->cfg.h2, al = c->cfg.alpha_w;
+    if (c->d == 3) {
+        if (gi) k_wls_interior<3><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2,
+                                                         al, c->g.S, c->g.P, rot, frames, c->err);
+        if (gb && !rot)
+            k_wls_boundary<3><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
+                                                     h2, al, c->g.cw, c->err);
+    } else {
+        if (gi) k_wls_interior<2><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2,
+                                                         al, c->g.S, c->g.P, rot, frames, c->err);
+        if (gb && !rot)
+            k_wls_boundary<2><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
+                                                     h2, al, c->g.cw, c->err);
+    }
+}
+
+void launch_wls(bgk_ctx* c, cudaStream_t s) { run_wls(c, nullptr, nullptr, s); }
+
+void launch_wls_export(bgk_ctx* c, double* rot, double* frames, cudaStream_t s) { run_wls(c, rot, frames, s); }
+
+}  // namespace bgk
