@@ -1,0 +1,363 @@
+"""Benchmark: particle x velocity updates/s of the fp64 BGK step (and achieved HBM GB/s).
+
+Workload (BASELINE.json north_star target): 3D driven cavity C5, 40^3 particles x 25^3
+velocity nodes (Nv = 24), Kn = 1, dt = 1e-11, ALE mode (neighbours + WLS rebuilt every
+step), synthetic seeded "stress" initial state (bgk_inputs).  One "step" is the whole hot
+path: neighbour search, WLS, transport, moments, Maxwellian + relaxation, ALE move,
+diffuse-reflection walls.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+N > 1 is launched with torch.distributed.run (one rank per GPU); the velocity grid is
+sharded by columns and the only data exchange is two NCCL all-reduces per step (moment
+sums [N,5] and wall flux [N]).  --impl reference times the CPU oracle (the paper-defined
+reference of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bgk_inputs as bi  # noqa: E402
+
+METRIC = "particle x velocity updates/s per BGK step (fp64) and achieved HBM GB/s"
+UNIT = "updates/s"
+FP64_LANES_PER_SM = 64           # B200: 64 FP64 FMA lanes per SM (B200_PROFILING / datasheet 37 TF)
+N_SM = 148
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+def oracle_sample_rate(cfg, cloud, seconds: float = 15.0, threads: int = 0, max_particles: int = 4096):
+    """Time the oracle (as it stands) on interior particles of the workload: each task is the
+    oracle's whole first step at one particle (neighbours, WLS, transport over all K nodes,
+    moments, Maxwellian, relaxation).  Returns (updates/s, cores, sample description)."""
+    import concurrent.futures as cf
+
+    import oracle
+    oracle.build()
+    kind = cloud["kind"]
+    inter = np.nonzero(kind == 0)[0]
+    rng = np.random.default_rng(2408)
+    order = rng.permutation(inter)[:max_particles]
+    threads = threads or min(os.cpu_count() or 1, 32)
+    K = cfg.n_nodes
+    done = 0
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(threads) as ex:   # ctypes releases the GIL inside the C oracle
+        it = iter(order)
+        futs = set()
+        while True:
+            while len(futs) < 2 * threads:
+                try:
+                    i = int(next(it))
+                except StopIteration:
+                    break
+                futs.add(ex.submit(oracle.sampled_first_step, cfg, cloud, [i]))
+            if not futs:
+                break
+            fin, futs = cf.wait(futs, return_when=cf.FIRST_COMPLETED)
+            done += len(fin)
+            if time.perf_counter() - t0 > seconds:
+                for f in futs:
+                    f.cancel()
+                cf.wait(futs)
+                done += sum(1 for f in futs if f.done() and not f.cancelled())
+                break
+    dt = time.perf_counter() - t0
+    rate = done * K / dt
+    desc = (f"oracle full first step at {done} random interior particles of {cfg.name} "
+            f"(all {K} nodes each), {threads} threads, {dt:.1f} s")
+    return rate, threads, desc
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_02350_b200 import Bgk
+    from paper_2408_02350_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = bi.CONFIGS[args.config] if args.config in bi.CONFIGS else getattr(bi, args.config)
+    cloud = bi.make_cloud(cfg)
+    ncol = (cfg.Nv + 1) ** (cfg.dims - 1)
+    shard = bi.column_shards(ncol, world)[rank]
+    g = Bgk(cfg, cloud, col_range=shard if world > 1 else None, device=dev)
+    N, K = g.N, cfg.n_nodes
+    n_int = int((cloud["kind"] == 0).sum())
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if world > 1:
+            g.step_sharded()
+        else:
+            g.step(1)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    g.sync()
+    barrier()
+    # ---- timed region: K whole steps (inputs are HBM-resident; f = N*K*8 B >> L2)
+    peaks, peak_src = load_peaks()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    g.sync()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ms_step = ms / args.steps
+    updates = N * K * args.steps
+    value = updates / (ms / 1e3)
+
+    # ---- per-phase breakdown (paper Table 3), CUDA events on the launching stream
+    phases = _lib.PHASES
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)]
+    acc = np.zeros(len(phases))
+    nph = max(2, min(args.steps, 5))
+    barrier()
+    for _ in range(nph):
+        ev[0].record(stream)
+        for q in range(len(phases)):
+            g.run_phase(q)
+            if world > 1 and q == 2:
+                dist.all_reduce(g.buffer(_lib.BUF_MOMENT_SUMS))
+            if world > 1 and q == 4:
+                dist.all_reduce(g.buffer(_lib.BUF_WALL_FLUX))
+            ev[q + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        acc += [ev[q].elapsed_time(ev[q + 1]) for q in range(len(phases))]
+    phase_ms = {p: float(v / nph) for p, v in zip(phases, acc)}
+    g.sync()
+
+    # ---- roofline of the dominant kernel (transport): fp64-issue bound
+    off, idx = g.neighbors()
+    inter = cloud["kind"] == 0
+    sum_m = int(np.diff(off)[inter].sum())
+    k_loc = g.Kloc
+    t_tr = phase_ms["transport"] / 1e3
+    instr_per_triple = 10.0          # SURVEY.md §8(d) lean count: 3 projections + 5 add/abs + 2 accumulates
+    algo_instr = instr_per_triple * sum_m * k_loc
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_instr = N_SM * FP64_LANES_PER_SM * sm_max * 1e6
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "transport_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(cfg.name)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "k_transport (fp64 pipe)",
+                "achieved": algo_instr / t_tr / 1e12, "peak": peak_instr / 1e12,
+                "unit": "T fp64-instr/s", "frac": algo_instr / t_tr / peak_instr, "traffic": traffic,
+                "per_unit": f"{instr_per_triple:g} fp64 instr per (particle, neighbour, node) triple; "
+                            f"{sum_m} interior pairs x {k_loc} local nodes",
+                "peak_src": f"{N_SM} SM x {FP64_LANES_PER_SM} FP64 lanes x {sm_max:.0f} MHz (sm_max of "
+                            f"{peak_src} peaks)"}
+    # achieved HBM (algorithmic): 32 B per particle-velocity value per step
+    # (read f^n, write ftilde, read ftilde, write f^{n+1})
+    nval = 2 if cfg.dims == 2 else 1
+    bytes_step = 32.0 * N * K * nval
+    hbm_gbs = bytes_step / (ms_step / 1e3) / 1e9
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Kl = g.Kloc
+        host_f = torch.empty((N, nval, Kl), dtype=torch.float64, pin_memory=True)
+        g.get_f(host_f)
+        rho = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        U = torch.empty((N, cfg.dims), dtype=torch.float64, pin_memory=True)
+        T = torch.empty(N, dtype=torch.float64, pin_memory=True)
+        n_e2e = max(1, min(args.steps, args.e2e_steps))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            g.set_f(host_f)                      # H2D of the step's input state
+            if world > 1:
+                g.step_sharded()
+                rr, uu, tt = g.moments_sharded()
+            else:
+                g.step(1)
+                rr, uu, tt = g.moments()         # D2H of the step's result (rho, U, T)
+        barrier()
+        dt_e2e = time.perf_counter() - t0
+        tt_ = torch.tensor([dt_e2e], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+        dt_e2e = float(tt_.item())
+        e2e = {"value": N * K * n_e2e / dt_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(host_f.numel() * 8 * world),
+               "d2h_bytes_per_step": int(N * (cfg.dims + 2) * 8),
+               "steps": n_e2e, "path": "bgk_set_f(pinned host) + bgk_step + bgk_moments(host)"}
+
+    launches = g.launches_per_step() * args.steps
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "particles": N, "interior": n_int, "velocity_nodes": K,
+                   "interior_pairs": sum_m, "ale": bool(cfg.ale), "init": cfg.init, "dt": cfg.dt,
+                   "parallelism": f"velocity-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2 (f = {N * K * nval * 8 / 1e9:.1f} GB per buffer)"},
+        "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / float(peaks.get("hbm_gbs", 6650.0)),
+        "phases_ms": phase_ms,
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, desc = oracle_sample_rate(cfg, cloud, seconds=args.cpu_seconds)
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- reference arm (oracle)
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = bi.CONFIGS[args.config] if args.config in bi.CONFIGS else getattr(bi, args.config)
+    cloud = bi.make_cloud(cfg)
+    per = max(5.0, min(30.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample_rate(cfg, cloud, seconds=per / 3)
+    rates, cores, desc = [], 1, ""
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, cores, desc = oracle_sample_rate(cfg, cloud, seconds=per)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    value = float(np.mean(rates))
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": cfg.name, "particles": cfg.n_particles, "velocity_nodes": cfg.n_nodes},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C5_3d_40cube_Nv24")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

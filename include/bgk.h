@@ -146,6 +146,22 @@ bgk_status bgk_step_transport(bgk_ctx* ctx, bgk_stream stream);
 bgk_status bgk_step_relax(bgk_ctx* ctx, bgk_stream stream);
 bgk_status bgk_step_boundary(bgk_ctx* ctx, bgk_stream stream);
 
+/* Finer phases of one step, in order, for per-phase timing (the paper's Table 3 breakdown):
+ * bgk_step_transport = GEOMETRY + TRANSPORT + MOMENT_SUMS, bgk_step_relax = RELAX +
+ * BOUNDARY_INTERP, bgk_step_boundary = BOUNDARY_FILL (which also makes f^{n+1} current).
+ * GEOMETRY rebuilds neighbours + WLS only in ALE mode or when the cached geometry is stale.
+ * Asynchronous. */
+typedef enum {
+    BGK_PHASE_GEOMETRY = 0,        /* cell-list neighbour search + WLS coefficients */
+    BGK_PHASE_TRANSPORT = 1,       /* positive upwind transport + moment partials */
+    BGK_PHASE_MOMENT_SUMS = 2,     /* per-particle reduction of the partials */
+    BGK_PHASE_RELAX = 3,           /* moments -> tau -> Maxwellian -> relaxation, ALE move */
+    BGK_PHASE_BOUNDARY_INTERP = 4, /* incoming half of boundary rows + wall flux (Z17, Z19) */
+    BGK_PHASE_BOUNDARY_FILL = 5    /* outgoing half = rho_w M_w; swap buffers */
+} bgk_phase;
+
+bgk_status bgk_run_phase(bgk_ctx* ctx, bgk_phase phase, bgk_stream stream);
+
 typedef enum {
     BGK_BUF_MOMENT_SUMS = 0, /* [N][5] fp64 rank-local sums (sum f, sum v f, sum |v|^2 f (+g2)) */
     BGK_BUF_WALL_FLUX = 1,   /* [N] fp64 rank-local sum_{v.n<0} (v.n) f_b (boundary rows) */

@@ -17,6 +17,7 @@ BGK_OK = 0
 STATUS = {0: "BGK_OK", 1: "BGK_E_INVALID_ARG", 2: "BGK_E_CAPACITY", 3: "BGK_E_DEFICIENT_STENCIL",
           4: "BGK_E_DEGENERATE_STATE", 5: "BGK_E_OUT_OF_DOMAIN", 6: "BGK_E_CUDA", 7: "BGK_E_WALL"}
 BUF_MOMENT_SUMS, BUF_WALL_FLUX, BUF_F = 0, 1, 2
+PHASES = ("geometry", "transport", "moment_sums", "relax", "boundary_interp", "boundary_fill")
 
 
 class BgkConfig(C.Structure):
@@ -42,6 +43,7 @@ SIGNATURES = {
     "bgk_step_transport": [_P, _P],
     "bgk_step_relax": [_P, _P],
     "bgk_step_boundary": [_P, _P],
+    "bgk_run_phase": [_P, _I, _P],
     "bgk_buffer": [_P, _I, _P, _P],
     "bgk_moments": [_P, _P, _P, _P, _P],
     "bgk_moments_partial": [_P, _P],

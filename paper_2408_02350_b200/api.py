@@ -121,6 +121,9 @@ class Bgk:
     def step_boundary(self):
         self._check(self.L.bgk_step_boundary(self.ctx, self.stream))
 
+    def run_phase(self, phase: int):
+        self._check(self.L.bgk_run_phase(self.ctx, int(phase), self.stream))
+
     def step_sharded(self, group=None):
         """One step of a velocity-sharded run: the only data exchange is two
         all-reduces (moment sums [N,5], wall flux [N]) over the process group."""

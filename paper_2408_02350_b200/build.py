@@ -13,7 +13,7 @@ SOURCES = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 HEADERS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(REPO, "include", "bgk.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--use_fast_math=false"]
+              "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
 
 
 def _nvcc():

@@ -297,30 +297,40 @@ bgk_status bgk_get_wls(bgk_ctx* c, double* Sout, double* rot, double* frames, do
     return sync_check(c, s);
 }
 
-bgk_status bgk_step_transport(bgk_ctx* c, bgk_stream stream) {
-    if (!c) return BGK_E_INVALID_ARG;
-    cudaStream_t s = S(stream);
-    ensure_geometry(c, s);
-    launch_transport(c, c->f[c->fcur], c->f[1 - c->fcur], s);
-    launch_moment_reduce(c, s);
-    return check_launch(c);
-}
-
-bgk_status bgk_step_relax(bgk_ctx* c, bgk_stream stream) {
+bgk_status bgk_run_phase(bgk_ctx* c, bgk_phase phase, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
     cudaStream_t s = S(stream);
     double* fn = c->f[1 - c->fcur];
-    launch_relax(c, fn, s);
-    launch_boundary_interp(c, fn, s);
+    switch (phase) {
+        case BGK_PHASE_GEOMETRY: ensure_geometry(c, s); break;
+        case BGK_PHASE_TRANSPORT: launch_transport(c, c->f[c->fcur], fn, s); break;
+        case BGK_PHASE_MOMENT_SUMS: launch_moment_reduce(c, s); break;
+        case BGK_PHASE_RELAX: launch_relax(c, fn, s); break;
+        case BGK_PHASE_BOUNDARY_INTERP: launch_boundary_interp(c, fn, s); break;
+        case BGK_PHASE_BOUNDARY_FILL:
+            launch_boundary_fill(c, fn, s);
+            c->fcur = 1 - c->fcur;
+            break;
+        default: return BGK_E_INVALID_ARG;
+    }
     return check_launch(c);
 }
 
+bgk_status bgk_step_transport(bgk_ctx* c, bgk_stream stream) {
+    bgk_status st;
+    if ((st = bgk_run_phase(c, BGK_PHASE_GEOMETRY, stream)) != BGK_OK) return st;
+    if ((st = bgk_run_phase(c, BGK_PHASE_TRANSPORT, stream)) != BGK_OK) return st;
+    return bgk_run_phase(c, BGK_PHASE_MOMENT_SUMS, stream);
+}
+
+bgk_status bgk_step_relax(bgk_ctx* c, bgk_stream stream) {
+    bgk_status st;
+    if ((st = bgk_run_phase(c, BGK_PHASE_RELAX, stream)) != BGK_OK) return st;
+    return bgk_run_phase(c, BGK_PHASE_BOUNDARY_INTERP, stream);
+}
+
 bgk_status bgk_step_boundary(bgk_ctx* c, bgk_stream stream) {
-    if (!c) return BGK_E_INVALID_ARG;
-    cudaStream_t s = S(stream);
-    launch_boundary_fill(c, c->f[1 - c->fcur], s);
-    c->fcur = 1 - c->fcur;
-    return check_launch(c);
+    return bgk_run_phase(c, BGK_PHASE_BOUNDARY_FILL, stream);
 }
 
 bgk_status bgk_step(bgk_ctx* c, int n_steps, bgk_stream stream) {
