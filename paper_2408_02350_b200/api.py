@@ -141,6 +141,17 @@ class Bgk:
         off = ptr.value - self.ws.data_ptr()
         return self.ws[off:off + nb.value].view(torch.float64)
 
+    @property
+    def ncs(self) -> int:
+        """Stored column stride of the internal layout f[N][n1][ncs][nval] (include/bgk.h BGK_BUF_F):
+        the local column count rounded up to even in 3D (16-byte TMA row strides)."""
+        return self.ncol + (self.ncol & 1) if self.dims == 3 else self.ncol
+
+    def f_internal(self) -> torch.Tensor:
+        """The current distribution buffer as a [N, n1, ncol, nval] view (padding stripped)."""
+        f = self.buffer(_lib.BUF_F).view(self.N, self.n1, self.ncs, self.nval)
+        return f[:, :, : self.ncol, :]
+
     def sync(self):
         self._check(self.L.bgk_sync(self.ctx, self.stream))
 

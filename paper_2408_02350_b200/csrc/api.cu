@@ -56,7 +56,9 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->ncol = c->c1 - c->c0;
     c->N = N;
     c->Kloc = (int64_t)c->n1 * c->ncol;
-    c->RS = c->Kloc * c->nv;
+    c->ncs = c->d == 3 ? c->ncol + (c->ncol & 1) : c->ncol;
+    c->Ks = (int64_t)c->n1 * c->ncs;
+    c->RS = c->Ks * c->nv;
     c->max_nb = cfg->max_neighbors > 0 ? cfg->max_neighbors : (c->d == 2 ? 96 : 256);
     c->cap = N * (int64_t)c->max_nb;
     int nc = (int)std::floor(cfg->L / cfg->h);
@@ -73,10 +75,11 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->PD = c->d == 2 ? 4 : 10;
     c->R = transport_rows_per_thread(c->d, c->n1);
     c->nchunk = c->n1 / c->R;
-    c->nslots = c->ncol * c->nchunk;
-    c->nwpp = (c->nslots + 31) / 32;
+    c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
+    c->nwpp = c->nchunk * c->ncg;
+    c->nslots = c->nwpp * 32;
     c->bnd_chunk = 256;
-    c->bnd_nch = (int)((c->Kloc + 255) / 256);
+    c->bnd_nch = (int)((c->Ks + 255) / 256);
 }
 
 size_t carve(bgk_ctx* c, char* base, bool dry) {
@@ -212,10 +215,29 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
         if (hk[i] < 0 || hk[i] > 2 * c->d) { delete c; return BGK_E_INVALID_ARG; }
         (hk[i] == 0 ? in : bd).push_back((int32_t)i);
     }
+    {   // boundary particles sorted by (wall, z, y, x): neighbours on a face are adjacent in the list
+        std::vector<double> hx(N * c->d);
+        e = cudaMemcpy(hx.data(), x, sizeof(double) * N * c->d, cudaMemcpyDefault);
+        if (e != cudaSuccess) { bgk_status st = cuda_fail(c, e); delete c; return st; }
+        const int d = c->d;
+        std::stable_sort(bd.begin(), bd.end(), [&](int32_t a, int32_t b) {
+            if (hk[a] != hk[b]) return hk[a] < hk[b];
+            for (int q = d - 1; q >= 0; --q)
+                if (hx[(int64_t)a * d + q] != hx[(int64_t)b * d + q]) return hx[(int64_t)a * d + q] < hx[(int64_t)b * d + q];
+            return a < b;
+        });
+    }
     c->N_int = (int64_t)in.size();
     c->N_b = (int64_t)bd.size();
+    if (!make_tensor_maps(c)) {
+        delete c;
+        return BGK_E_CUDA;
+    }
     const int64_t reset[4] = {0, INT64_MAX, 0, 0};
     cudaMemcpyAsync(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice, s);
+    // padding columns stay zero forever (TMA boxes of the last column group read them)
+    cudaMemsetAsync(c->f[0], 0, sizeof(double) * N * c->RS, s);
+    cudaMemsetAsync(c->f[1], 0, sizeof(double) * N * c->RS, s);
     cudaMemsetAsync(c->stab, 0, sizeof(unsigned long long), s);
     cudaMemcpyAsync(c->x, x, sizeof(double) * N * c->d, cudaMemcpyDefault, s);
     cudaMemcpyAsync(c->kind, hk.data(), N, cudaMemcpyHostToDevice, s);
@@ -406,7 +428,7 @@ bgk_status bgk_get_f(bgk_ctx* c, double* f, bgk_stream stream) {
     launch_to_canonical(c, c->f[c->fcur], scratch, s);
     bgk_status st = check_launch(c);
     if (st != BGK_OK) return st;
-    if ((st = copy_out(c, f, scratch, sizeof(double) * c->N * c->RS, s)) != BGK_OK) return st;
+    if ((st = copy_out(c, f, scratch, sizeof(double) * c->N * c->nv * c->Kloc, s)) != BGK_OK) return st;
     return sync_check(c, s);
 }
 
@@ -414,7 +436,7 @@ bgk_status bgk_set_f(bgk_ctx* c, const double* f, bgk_stream stream) {
     if (!c || !f) return BGK_E_INVALID_ARG;
     cudaStream_t s = S(stream);
     double* scratch = c->f[1 - c->fcur];
-    bgk_status st = copy_out(c, scratch, f, sizeof(double) * c->N * c->RS, s);
+    bgk_status st = copy_out(c, scratch, f, sizeof(double) * c->N * c->nv * c->Kloc, s);
     if (st != BGK_OK) return st;
     launch_from_canonical(c, scratch, c->f[c->fcur], s);
     if ((st = check_launch(c)) != BGK_OK) return st;

@@ -7,6 +7,7 @@
 //   of one particle and walk k1 sequentially, so every load of a neighbour row
 //   at fixed k1 is one coalesced 256-B (3D) / 512-B (2D) transaction.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -37,7 +38,10 @@ struct Geo {                    // per-step geometry arrays (device)
 struct bgk_ctx {
     bgk_config cfg;
     int d, nv, n1, ncol_g, c0, c1, ncol;
-    int64_t N, N_int, N_b, Kloc, RS;   // RS = doubles per particle row = Kloc*nv
+    int ncs;                           // stored column stride: ncol rounded up to even in 3D (16-B TMA strides)
+    int64_t N, N_int, N_b, Kloc, Ks, RS;   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
+    int ncg;                           // 32-column groups per chunk (transport)
+    CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
     int max_nb;
     int64_t cap;
     int nc[3];
@@ -129,6 +133,12 @@ void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream
 void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_check_domain(bgk_ctx* c, cudaStream_t s);
 int transport_rows_per_thread(int d, int n1);
+bool make_tensor_maps(bgk_ctx* c);
+// storage index of local node t = k1*ncol + col  ->  k1*ncs + col
+__host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int ncs) {
+    const int64_t k1 = t / ncol;
+    return k1 * ncs + (t - k1 * ncol);
+}
 int launches_neighbors();
 int launches_wls();
 

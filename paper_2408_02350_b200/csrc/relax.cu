@@ -49,6 +49,17 @@ __device__ __forceinline__ void node_vel(int t, int ncol, int c0, int n1, double
     for (int a = 0; a < 3; ++a) v[a] = (a < D) ? axis_node(vmax, dv, kk[a]) : 0.0;
 }
 
+// velocity of STORED node ts = k1 * ncs + col; false for the padding column (col >= ncol)
+template <int D>
+__device__ __forceinline__ bool node_vel_s(int64_t ts, int ncs, int ncol, int c0, int n1, double vmax, double dv,
+                                           double (&v)[3]) {
+    const int k1 = (int)(ts / ncs), col = (int)(ts - (int64_t)k1 * ncs);
+    if (col >= ncol) return false;
+    int kk[3];
+    node_vel<D>(k1 * ncol + col, ncol, c0, n1, vmax, dv, v, kk);
+    return true;
+}
+
 __global__ void k_moment_reduce(const int32_t* __restrict__ ids, int64_t n, const double* __restrict__ partials,
                                 int nwpp, double* __restrict__ sums) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -71,7 +82,7 @@ struct RelaxArgs {
     double* x;
     int64_t* err;
     int64_t n;
-    int n1, ncol, c0, Kloc, ale;
+    int n1, ncol, ncs, c0, Ks, ale;
     double vmax, dv, dt, R, kb, dmol, L, clamp_eps;
 };
 
@@ -133,20 +144,43 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
     }
     __syncthreads();
     const double a1 = par[0], a2 = par[1], pref = par[2], RT = par[3];
-    double* fp = A.f + (int64_t)p * A.Kloc * NV;
-    for (int t = threadIdx.x; t < A.Kloc; t += blockDim.x) {
-        const int k1 = t / A.ncol, col = t - k1 * A.ncol, gc = A.c0 + col;
-        double M;
-        if constexpr (D == 3) {
-            const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-            M = pref * e[0][k1] * e[1][k2] * e[2][k3];
-            fp[t] = a1 * fp[t] + a2 * M;
-        } else {
-            M = pref * e[0][k1] * e[1][gc];
-            double2 g = reinterpret_cast<double2*>(fp)[t];
-            g.x = a1 * g.x + a2 * M;
-            g.y = a1 * g.y + a2 * (RT * M);
-            reinterpret_cast<double2*>(fp)[t] = g;
+    double2* fp2 = reinterpret_cast<double2*>(A.f + (int64_t)p * A.Ks * NV);
+    // 16-byte accesses: in 3D two adjacent columns (ncs is even), in 2D the (g1, g2) pair of a node.
+    // Four independent loads in flight per thread keep enough bytes moving to stream at HBM rate.
+    const int n2 = (D == 3) ? A.Ks / 2 : A.Ks;
+    constexpr int U = 4;
+    for (int u0 = threadIdx.x; u0 < n2; u0 += U * blockDim.x) {
+        double2 g[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int u = u0 + q * blockDim.x;
+            if (u < n2) g[q] = fp2[u];
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int u = u0 + q * blockDim.x;
+            if (u >= n2) break;
+            if constexpr (D == 3) {
+                const int t = 2 * u;
+                const int k1 = t / A.ncs, col = t - k1 * A.ncs, gc = A.c0 + col;
+                const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+                const double base = pref * e[0][k1] * e[1][k2];
+                const double M0 = base * e[2][k3];
+                // the second column may be the next v_2 line (k3 = n1-1 -> 0) or the padding column
+                double M1 = 0.0;
+                if (col + 1 < A.ncol) {
+                    const int gc1 = gc + 1, k21 = gc1 / A.n1, k31 = gc1 - k21 * A.n1;
+                    M1 = pref * e[0][k1] * e[1][k21] * e[2][k31];
+                }
+                g[q].x = a1 * g[q].x + a2 * M0;
+                g[q].y = (col + 1 < A.ncol) ? a1 * g[q].y + a2 * M1 : 0.0;
+            } else {
+                const int k1 = u / A.ncs, col = u - k1 * A.ncs;
+                const double M = pref * e[0][k1] * e[1][A.c0 + col];
+                g[q].x = a1 * g[q].x + a2 * M;
+                g[q].y = a1 * g[q].y + a2 * (RT * M);
+            }
+            fp2[u] = g[q];
         }
     }
 }
@@ -167,8 +201,8 @@ __device__ __forceinline__ void maxwellian_at(double rho, const double* U, doubl
 
 template <int D>
 __global__ void k_init_f(const double* __restrict__ macro0, int64_t N, double* __restrict__ f,
-                         double* __restrict__ macro, double* __restrict__ W, int ale, int n1, int ncol, int c0,
-                         int64_t Kloc, double vmax, double dv, double R, double Twall) {
+                         double* __restrict__ macro, double* __restrict__ W, int ale, int n1, int ncol, int ncs,
+                         int c0, int64_t Ks, double vmax, double dv, double R, double Twall) {
     constexpr int NV = (D == 2) ? 2 : 1;
     const int64_t p = blockIdx.x;
     if (p >= N) return;
@@ -188,33 +222,30 @@ __global__ void k_init_f(const double* __restrict__ macro0, int64_t N, double* _
         }
         macro[p * (D + 2) + 1 + D] = T;
     }
-    for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
+    for (int64_t t = threadIdx.x; t < Ks; t += blockDim.x) {
         double v[3];
-        int kk[3];
-        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+        if (!node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) continue;
         double M[2];
         maxwellian_at<D>(rho, U, T, R, v, M);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) f[(p * Kloc + t) * NV + q] = M[q];
+        for (int q = 0; q < NV; ++q) f[(p * Ks + t) * NV + q] = M[q];
     }
 }
 
 // wall tables: Mw[w][local node] = M(1, U_w, T_w); den[w] = sum over the GLOBAL grid of
 // (v.n)^+ M_w (2D: G1), identical on every rank.
 template <int D>
-__global__ void k_wall_M(double* __restrict__ Mw, int n1, int ncol, int c0, int64_t Kloc, double vmax, double dv,
-                         double R, double Twall, double lid0, double lid1, double lid2) {
+__global__ void k_wall_M(double* __restrict__ Mw, int n1, int ncol, int ncs, int c0, int64_t Ks, double vmax,
+                         double dv, double R, double Twall, double lid0, double lid1, double lid2) {
     constexpr int NV = (D == 2) ? 2 : 1;
     const int wid = blockIdx.y + 1;
     const double U[3] = {wid == 2 * D ? lid0 : 0.0, wid == 2 * D ? lid1 : 0.0, wid == 2 * D ? lid2 : 0.0};
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Kloc; t += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Ks; t += (int64_t)gridDim.x * blockDim.x) {
         double v[3];
-        int kk[3];
-        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
-        double M[2];
-        maxwellian_at<D>(1.0, U, Twall, R, v, M);
+        double M[2] = {0.0, 0.0};
+        if (node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) maxwellian_at<D>(1.0, U, Twall, R, v, M);
 #pragma unroll
-        for (int q = 0; q < NV; ++q) Mw[((int64_t)blockIdx.y * Kloc + t) * NV + q] = M[q];
+        for (int q = 0; q < NV; ++q) Mw[((int64_t)blockIdx.y * Ks + t) * NV + q] = M[q];
     }
 }
 
@@ -249,56 +280,87 @@ __global__ void __launch_bounds__(256) k_wall_den(double* __restrict__ den, int 
 
 constexpr int kBndChunk = 256;
 
+// Block = (group of kBndGroup consecutive boundary particles of the face-sorted list, chunk of
+// 256 stored nodes).  Neighbouring boundary particles share most interior neighbours, so the
+// rows loaded for one particle of the group are L1 hits for the next.
+constexpr int kBndGroup = 8;
+
 template <int D>
-__global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restrict__ bids, const int8_t* __restrict__ kind,
+__global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restrict__ bids, int64_t nb,
+                                                          const int8_t* __restrict__ kind,
                                                           const int64_t* __restrict__ nb_off,
                                                           const int32_t* __restrict__ nb_idx,
                                                           const double* __restrict__ cw, double* __restrict__ f,
                                                           double* __restrict__ wallpart, int nch, int n1, int ncol,
-                                                          int c0, int64_t Kloc, double vmax, double dv) {
+                                                          int ncs, int c0, int64_t Kloc, int max_nb, double vmax,
+                                                          double dv) {
+    // Kloc here is the STORED node count per row (n1 * ncs)
     constexpr int NV = (D == 2) ? 2 : 1;
     __shared__ double sh[32];
-    const int bi = blockIdx.x;
-    const int b = bids[bi];
-    const int wid = kind[b];
-    const int axis = (wid - 1) / 2;
-    const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
+    __shared__ int s_cnt;
+    extern __shared__ unsigned char bsm[];
+    int32_t* sj = reinterpret_cast<int32_t*>(bsm);                 // interior neighbours of b (compacted)
+    double* sc = reinterpret_cast<double*>(bsm + ((max_nb * 4 + 15) / 16) * 16);
     const int64_t t = (int64_t)blockIdx.y * kBndChunk + threadIdx.x;
-    const bool in_range = t < Kloc;
-    double vn = 1.0;
-    if (in_range) {
-        double v[3];
-        int kk[3];
-        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
-        vn = sgn * v[axis];
-    }
-    const bool incoming = in_range && vn <= 0.0;
-    double acc[NV];
+    double v[3] = {0.0, 0.0, 0.0};
+    const bool in_range = t < Kloc && node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v);
+    const int lane = threadIdx.x & 31;
+    for (int g = 0; g < kBndGroup; ++g) {
+        const int64_t bi = (int64_t)blockIdx.x * kBndGroup + g;
+        if (bi >= nb) break;                                // block-uniform
+        const int b = bids[bi];
+        const int64_t off = nb_off[b];
+        const int m = (int)(nb_off[b + 1] - off);
+        __syncthreads();                                    // previous particle's list fully consumed
+        if (threadIdx.x < 32) {                             // warp 0 compacts the nonzero weights, in order
+            int base = 0;
+            for (int e0 = 0; e0 < m; e0 += 32) {
+                const int e = e0 + lane;
+                const double c = e < m ? cw[off + e] : 0.0;
+                const bool keep = c != 0.0;
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int slot = base + __popc(bal & ((1u << lane) - 1u));
+                    sj[slot] = nb_idx[off + e];
+                    sc[slot] = c;
+                }
+                base += __popc(bal);
+            }
+            if (lane == 0) s_cnt = base;
+        }
+        __syncthreads();
+        const int mi = s_cnt;
+        const int wid = kind[b];
+        const int axis = (wid - 1) / 2;
+        const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
+        const double vn = sgn * v[axis];
+        const bool incoming = in_range && vn <= 0.0;
+        double acc[NV];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-    const int64_t off = nb_off[b], end = nb_off[b + 1];
-    for (int64_t e = off; e < end; ++e) {
-        const double c = __ldg(cw + e);
-        if (c == 0.0) continue;                     // boundary neighbours carry zero weight (uniform)
-        const int64_t j = __ldg(nb_idx + e);
+        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
         if (incoming) {
-            if constexpr (NV == 1) {
-                acc[0] = fma(c, __ldg(f + j * Kloc + t), acc[0]);
-            } else {
-                const double2 g = __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t);
-                acc[0] = fma(c, g.x, acc[0]);
-                acc[1] = fma(c, g.y, acc[1]);
+#pragma unroll 8
+            for (int e = 0; e < mi; ++e) {
+                const int64_t j = sj[e];
+                const double c = sc[e];
+                if constexpr (NV == 1) {
+                    acc[0] = fma(c, __ldg(f + j * Kloc + t), acc[0]);
+                } else {
+                    const double2 gv = __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t);
+                    acc[0] = fma(c, gv.x, acc[0]);
+                    acc[1] = fma(c, gv.y, acc[1]);
+                }
             }
         }
+        double flux = 0.0;
+        if (incoming) {
+            if constexpr (NV == 1) f[(int64_t)b * Kloc + t] = acc[0];
+            else reinterpret_cast<double2*>(f)[(int64_t)b * Kloc + t] = make_double2(acc[0], acc[1]);
+            if (vn < 0.0) flux = vn * acc[0];
+        }
+        const double tot = block_sum<kBndChunk>(flux, sh);
+        if (threadIdx.x == 0) wallpart[bi * nch + blockIdx.y] = tot;
     }
-    double flux = 0.0;
-    if (incoming) {
-        if constexpr (NV == 1) f[(int64_t)b * Kloc + t] = acc[0];
-        else reinterpret_cast<double2*>(f)[(int64_t)b * Kloc + t] = make_double2(acc[0], acc[1]);
-        if (vn < 0.0) flux = vn * acc[0];
-    }
-    const double tot = block_sum<kBndChunk>(flux, sh);
-    if (threadIdx.x == 0) wallpart[(int64_t)bi * nch + blockIdx.y] = tot;
 }
 
 __global__ void k_wall_reduce(const int32_t* __restrict__ bids, int64_t nb, const double* __restrict__ wallpart,
@@ -314,8 +376,8 @@ template <int D>
 __global__ void __launch_bounds__(kBndChunk) k_bnd_fill(const int32_t* __restrict__ bids, const int8_t* __restrict__ kind,
                                                         const double* __restrict__ wallnum,
                                                         const double* __restrict__ den, const double* __restrict__ Mw,
-                                                        double* __restrict__ f, int n1, int ncol, int c0, int64_t Kloc,
-                                                        double vmax, double dv) {
+                                                        double* __restrict__ f, int n1, int ncol, int ncs, int c0,
+                                                        int64_t Kloc, double vmax, double dv) {
     constexpr int NV = (D == 2) ? 2 : 1;
     const int b = bids[blockIdx.x];
     const int wid = kind[b];
@@ -324,8 +386,7 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_fill(const int32_t* __restric
     const int64_t t = (int64_t)blockIdx.y * kBndChunk + threadIdx.x;
     if (t >= Kloc) return;
     double v[3];
-    int kk[3];
-    node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+    if (!node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) return;
     if (!(sgn * v[axis] > 0.0)) return;
     const double rho_w = -wallnum[b] / den[wid - 1];
     const double* M = Mw + ((int64_t)(wid - 1) * Kloc + t) * NV;
@@ -336,7 +397,9 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_fill(const int32_t* __restric
 // moments of every row (diagnostics, bgk_moments): sums[p] = (s0, s_v, s_E[+g2])
 template <int D>
 __global__ void __launch_bounds__(256) k_row_moments(const double* __restrict__ f, int64_t N, double* __restrict__ sums,
-                                                     int n1, int ncol, int c0, int64_t Kloc, double vmax, double dv) {
+                                                     int n1, int ncol, int ncs, int c0, int64_t Kloc, double vmax,
+                                                     double dv) {
+    // Kloc = STORED nodes per row (n1 * ncs)
     constexpr int NV = (D == 2) ? 2 : 1;
     __shared__ double sh[32];
     const int64_t p = blockIdx.x;
@@ -344,8 +407,7 @@ __global__ void __launch_bounds__(256) k_row_moments(const double* __restrict__ 
     double s[kPM] = {0, 0, 0, 0, 0};
     for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
         double v[3];
-        int kk[3];
-        node_vel<D>((int)t, ncol, c0, n1, vmax, dv, v, kk);
+        if (!node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) continue;
         const double g = f[(p * Kloc + t) * NV];
         s[0] += g;
 #pragma unroll
@@ -386,19 +448,20 @@ __global__ void k_moments_finalize(const double* __restrict__ sums, int64_t N, d
     if (!(rho > 0.0) || !(T > 1e-12)) latch_error(err, BGK_E_DEGENERATE_STATE, p);
 }
 
-// internal [p][k1][col][q]  <->  canonical [p][q][k1][col]
+// internal [p][k1][col (stride ncs)][q]  <->  canonical [p][q][k1][col (ncol)]
 template <bool TO_CANON>
-__global__ void k_transpose2(const double* __restrict__ in, double* __restrict__ out, int64_t N, int64_t Kloc) {
-    const int64_t total = N * Kloc;
+__global__ void k_transpose(const double* __restrict__ in, double* __restrict__ out, int64_t N, int nv, int n1,
+                            int ncol, int ncs) {
+    const int64_t Kc = (int64_t)n1 * ncol, total = N * nv * Kc;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = t / Kloc, k = t - p * Kloc;
-        if (TO_CANON) {
-            out[(p * 2 + 0) * Kloc + k] = in[t * 2 + 0];
-            out[(p * 2 + 1) * Kloc + k] = in[t * 2 + 1];
-        } else {
-            out[t * 2 + 0] = in[(p * 2 + 0) * Kloc + k];
-            out[t * 2 + 1] = in[(p * 2 + 1) * Kloc + k];
-        }
+        const int64_t p = t / (nv * Kc);
+        const int64_t r = t - p * nv * Kc;
+        const int q = (int)(r / Kc);
+        const int64_t k = r - (int64_t)q * Kc;
+        const int64_t k1 = k / ncol, col = k - k1 * ncol;
+        const int64_t si = ((p * n1 + k1) * ncs + col) * nv + q;
+        if (TO_CANON) out[t] = in[si];
+        else out[si] = in[t];
     }
 }
 
@@ -434,8 +497,9 @@ void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
     a.n = c->N_int;
     a.n1 = c->n1;
     a.ncol = c->ncol;
+    a.ncs = c->ncs;
     a.c0 = c->c0;
-    a.Kloc = (int)c->Kloc;
+    a.Ks = (int)c->Ks;
     a.ale = c->cfg.ale;
     a.vmax = c->cfg.vmax;
     a.dv = c->dv;
@@ -451,15 +515,16 @@ void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
 
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
-    dim3 g((unsigned)c->N_b, (unsigned)c->bnd_nch);
+    dim3 g((unsigned)((c->N_b + kBndGroup - 1) / kBndGroup), (unsigned)c->bnd_nch);
+    const size_t smem = ((c->max_nb * 4 + 15) / 16) * 16 + (size_t)c->max_nb * 8;
     if (c->d == 3)
-        k_bnd_interp<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw, fnew,
-                                                c->wallpart, c->bnd_nch, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
-                                                c->dv);
+        k_bnd_interp<3><<<g, kBndChunk, smem, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw,
+                                                   fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0, c->Ks,
+                                                   c->max_nb, c->cfg.vmax, c->dv);
     else
-        k_bnd_interp<2><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw, fnew,
-                                                c->wallpart, c->bnd_nch, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
-                                                c->dv);
+        k_bnd_interp<2><<<g, kBndChunk, smem, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw,
+                                                   fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0, c->Ks,
+                                                   c->max_nb, c->cfg.vmax, c->dv);
     k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart, c->bnd_nch,
                                                                     c->wallnum);
 }
@@ -469,23 +534,23 @@ void launch_boundary_fill(bgk_ctx* c, double* fnew, cudaStream_t s) {
     dim3 g((unsigned)c->N_b, (unsigned)c->bnd_nch);
     if (c->d == 3)
         k_bnd_fill<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->wallnum, c->wall_den, c->Mw, fnew, c->n1,
-                                              c->ncol, c->c0, c->Kloc, c->cfg.vmax, c->dv);
+                                              c->ncol, c->ncs, c->c0, c->Ks, c->cfg.vmax, c->dv);
     else
         k_bnd_fill<2><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->wallnum, c->wall_den, c->Mw, fnew, c->n1,
-                                              c->ncol, c->c0, c->Kloc, c->cfg.vmax, c->dv);
+                                              c->ncol, c->ncs, c->c0, c->Ks, c->cfg.vmax, c->dv);
 }
 
 void launch_wall_tables(bgk_ctx* c, cudaStream_t s) {
     const bgk_config& k = c->cfg;
     const int nw = 2 * c->d;
-    dim3 g((unsigned)std::min<int64_t>((c->Kloc + 255) / 256, 4096), (unsigned)nw);
+    dim3 g((unsigned)std::min<int64_t>((c->Ks + 255) / 256, 4096), (unsigned)nw);
     if (c->d == 3) {
-        k_wall_M<3><<<g, 256, 0, s>>>(c->Mw, c->n1, c->ncol, c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall,
+        k_wall_M<3><<<g, 256, 0, s>>>(c->Mw, c->n1, c->ncol, c->ncs, c->c0, c->Ks, k.vmax, c->dv, k.R, k.T_wall,
                                       k.U_lid[0], k.U_lid[1], k.U_lid[2]);
         k_wall_den<3><<<nw, 256, 0, s>>>(c->wall_den, c->n1, c->ncol_g, k.vmax, c->dv, k.R, k.T_wall, k.U_lid[0],
                                          k.U_lid[1], k.U_lid[2], c->err);
     } else {
-        k_wall_M<2><<<g, 256, 0, s>>>(c->Mw, c->n1, c->ncol, c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall,
+        k_wall_M<2><<<g, 256, 0, s>>>(c->Mw, c->n1, c->ncol, c->ncs, c->c0, c->Ks, k.vmax, c->dv, k.R, k.T_wall,
                                       k.U_lid[0], k.U_lid[1], k.U_lid[2]);
         k_wall_den<2><<<nw, 256, 0, s>>>(c->wall_den, c->n1, c->ncol_g, k.vmax, c->dv, k.R, k.T_wall, k.U_lid[0],
                                          k.U_lid[1], k.U_lid[2], c->err);
@@ -496,18 +561,18 @@ void launch_init_f(bgk_ctx* c, const double* macro0, cudaStream_t s) {
     const bgk_config& k = c->cfg;
     if (c->d == 3)
         k_init_f<3><<<(unsigned)c->N, 256, 0, s>>>(macro0, c->N, c->f[c->fcur], c->macro, c->W, k.ale, c->n1, c->ncol,
-                                                   c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall);
+                                                   c->ncs, c->c0, c->Ks, k.vmax, c->dv, k.R, k.T_wall);
     else
         k_init_f<2><<<(unsigned)c->N, 256, 0, s>>>(macro0, c->N, c->f[c->fcur], c->macro, c->W, k.ale, c->n1, c->ncol,
-                                                   c->c0, c->Kloc, k.vmax, c->dv, k.R, k.T_wall);
+                                                   c->ncs, c->c0, c->Ks, k.vmax, c->dv, k.R, k.T_wall);
 }
 
 void launch_row_moments(bgk_ctx* c, const double* f, cudaStream_t s) {
     if (c->d == 3)
-        k_row_moments<3><<<(unsigned)c->N, 256, 0, s>>>(f, c->N, c->sums, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
+        k_row_moments<3><<<(unsigned)c->N, 256, 0, s>>>(f, c->N, c->sums, c->n1, c->ncol, c->ncs, c->c0, c->Ks, c->cfg.vmax,
                                                         c->dv);
     else
-        k_row_moments<2><<<(unsigned)c->N, 256, 0, s>>>(f, c->N, c->sums, c->n1, c->ncol, c->c0, c->Kloc, c->cfg.vmax,
+        k_row_moments<2><<<(unsigned)c->N, 256, 0, s>>>(f, c->N, c->sums, c->n1, c->ncol, c->ncs, c->c0, c->Ks, c->cfg.vmax,
                                                         c->dv);
 }
 
@@ -518,19 +583,19 @@ void launch_moments_finalize(bgk_ctx* c, double* out, cudaStream_t s) {
 }
 
 void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
-    if (c->nv == 1) {
+    if (c->nv == 1 && c->ncs == c->ncol) {
         cudaMemcpyAsync(fout, fin, sizeof(double) * c->N * c->RS, cudaMemcpyDeviceToDevice, s);
         return;
     }
-    k_transpose2<true><<<4096, 256, 0, s>>>(fin, fout, c->N, c->Kloc);
+    k_transpose<true><<<4096, 256, 0, s>>>(fin, fout, c->N, c->nv, c->n1, c->ncol, c->ncs);
 }
 
 void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
-    if (c->nv == 1) {
+    if (c->nv == 1 && c->ncs == c->ncol) {
         cudaMemcpyAsync(fout, fin, sizeof(double) * c->N * c->RS, cudaMemcpyDeviceToDevice, s);
         return;
     }
-    k_transpose2<false><<<4096, 256, 0, s>>>(fin, fout, c->N, c->Kloc);
+    k_transpose<false><<<4096, 256, 0, s>>>(fin, fout, c->N, c->nv, c->n1, c->ncol, c->ncs);
 }
 
 void launch_check_domain(bgk_ctx* c, cudaStream_t s) {

@@ -224,8 +224,8 @@ def test_c5_full_size_sampled(torch_cuda):
     sample = list(rng.choice(inter, 4, replace=False)) + [int(inter[0]), int(inter[-1])]
     sample += [int(np.nonzero(kind == 6)[0][700]), int(np.nonzero(kind == 1)[0][0])]  # lid, corner
     ref = oracle.sampled_first_step(cfg, cloud, sample)
-    fbuf = g.buffer(_lib.BUF_F).view(g.N, -1)
-    rows = fbuf[torch.tensor(sample, device=fbuf.device)].cpu().numpy()
+    fbuf = g.f_internal()
+    rows = fbuf[torch.tensor(sample, device=fbuf.device)].reshape(len(sample), -1).cpu().numpy()
     macro = g.macro()
     x = g.positions()
     for q, i in enumerate(sample):
