@@ -69,6 +69,7 @@ def load(path: str = LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("BGK_LIB_PATH", path)   # experiment builds (tools/); default is the in-tree library
     if not os.path.exists(path):
         raise ImportError(f"{path} not found: build it with paper_2408_02350_b200.build.build_library() "
                           "(the CUDA path has no CPU fallback)")

@@ -3,6 +3,7 @@
 // interleaves with its two all-reduces), copies and error reporting.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -62,22 +63,32 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->max_nb = cfg->max_neighbors > 0 ? cfg->max_neighbors : (c->d == 2 ? 96 : 256);
     c->cap = N * (int64_t)c->max_nb;
     int nc = (int)std::floor(cfg->L / cfg->h);
-    nc = std::max(1, std::min(nc, kMaxCellsPerAxis));
+    nc = std::max(1, std::min(nc, cfg->dims == 3 ? 1024 : kMaxCellsPerAxis));
     while (nc > 1 && cfg->L / nc < cfg->h * (1.0 + 1e-12)) --nc;   // cell edge strictly >= h
+    int pw = 1;                                  // Morton cell codes span a power-of-two box
+    while (pw < nc) pw <<= 1;
     c->ncell = 1;
     for (int a = 0; a < 3; ++a) {
         c->nc[a] = a < c->d ? nc : 1;
         c->edge[a] = cfg->L / nc;
-        c->ncell *= c->nc[a];
+        c->ncell *= a < c->d ? pw : 1;
     }
     c->dv = 2.0 * cfg->vmax / cfg->Nv;
     c->vmin = -cfg->vmax;
     c->PD = c->d == 2 ? 4 : 10;
     c->R = transport_rows_per_thread(c->d, c->n1);
-    c->nchunk = c->n1 / c->R;
+    c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
     c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
     c->nwpp = c->nchunk * c->ncg;
     c->nslots = c->nwpp * 32;
+    {   // grouped transport: union lists of up to group_size() * max_nb members (power of two for the sort)
+        int u = 1;
+        while (u < group_size() * c->max_nb) u <<= 1;
+        c->ucap = u;
+        const char* e = getenv("BGK_TRANSPORT_GRP");
+        c->grouped = e ? atoi(e) != 0 : false;   // measured slower on C5 (profiles/r01_tuning.md)
+        if ((size_t)c->ucap * 8 > 48 * 1024 || c->ucap > 65535) c->grouped = false;   // sort buffers in smem
+    }
     c->bnd_chunk = 256;
     c->bnd_nch = (int)((c->Ks + 255) / 256);
 }
@@ -103,6 +114,7 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->outbuf = k.take<double>(N * (d + 2));
     c->err = k.take<int64_t>(4);
     c->stab = k.take<unsigned long long>(1);
+    c->work = k.take<unsigned long long>(1);
     c->scan_tmp = k.take<int64_t>(1024);
     c->g.cell_of = k.take<int32_t>(N);
     c->g.cell_cnt = k.take<int32_t>(c->ncell);
@@ -116,6 +128,11 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->g.P = k.take<double>((size_t)c->cap * c->PD);
     c->g.cw = k.take<double>(c->cap);
     c->g.order = k.take<int32_t>(N);
+    const int64_t ng = (N + group_size() - 1) / group_size();
+    c->gU = k.take<int32_t>(c->grouped ? (size_t)ng * c->ucap : 1);
+    c->gUlen = k.take<int32_t>(ng);
+    c->gCnt = k.take<uint8_t>(c->grouped ? (size_t)ng * c->ucap : 1);
+    c->upos = k.take<uint16_t>(c->grouped ? (size_t)c->cap : 1);
     return k.off + 256;
 }
 
@@ -166,6 +183,7 @@ void ensure_geometry(bgk_ctx* c, cudaStream_t s) {
     if (c->cfg.ale || !c->geometry_valid) {
         launch_build_neighbors(c, s);
         launch_wls(c, s);
+        launch_group_union(c, s);
         c->geometry_valid = true;
     }
 }

@@ -70,6 +70,13 @@ struct bgk_ctx {
     double* outbuf;     // [N][d+2] scratch for moments / copies
     int64_t* err;       // [4] code, particle, needed, spare
     unsigned long long* stab;  // [1] max_{i,k} sum_j |C_ijk| as ordered bits
+    unsigned long long* work;  // [1] persistent transport work counter
+    int32_t* gU;        // [groups][ucap] union of the neighbour lists of each particle group (grouped transport)
+    int32_t* gUlen;     // [groups]
+    uint8_t* gCnt;      // [groups][ucap] users of each union member
+    uint16_t* upos;     // [cap] union position of each CSR entry of an interior particle
+    int ucap;
+    bool grouped;       // grouped (block-shared neighbour ring) transport kernel
     int64_t* scan_tmp;  // [1024]
     bgk::Geo g;
     // host-side error state
@@ -140,6 +147,8 @@ __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int
     return k1 * ncs + (t - k1 * ncol);
 }
 int launches_neighbors();
+int group_size();
+void launch_group_union(bgk_ctx* c, cudaStream_t s);
 int launches_wls();
 
 }  // namespace bgk

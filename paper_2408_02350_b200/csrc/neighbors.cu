@@ -20,6 +20,60 @@ namespace {
 
 constexpr int kScanThreads = 1024;
 
+// Cells are numbered along a Morton (Z-order) curve, so consecutive cells -- and the
+// cell-ordered interior list the transport kernel walks -- form compact 3D blobs: the
+// neighbour rows a block of consecutive particles needs stay within a small, L2-resident
+// window.  Up to 10 bits per axis in 3D (1024 cells per axis) and 16 in 2D.
+__host__ __device__ __forceinline__ uint32_t spread3(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__host__ __device__ __forceinline__ uint32_t compact3(uint32_t v) {
+    v &= 0x09249249u;
+    v = (v | (v >> 2)) & 0x030c30c3u;
+    v = (v | (v >> 4)) & 0x0300f00fu;
+    v = (v | (v >> 8)) & 0x030000ffu;
+    v = (v | (v >> 16)) & 0x3ffu;
+    return v;
+}
+__host__ __device__ __forceinline__ uint32_t spread2(uint32_t v) {
+    v &= 0xffffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+__host__ __device__ __forceinline__ uint32_t compact2(uint32_t v) {
+    v &= 0x55555555u;
+    v = (v | (v >> 1)) & 0x33333333u;
+    v = (v | (v >> 2)) & 0x0f0f0f0fu;
+    v = (v | (v >> 4)) & 0x00ff00ffu;
+    v = (v | (v >> 8)) & 0x0000ffffu;
+    return v;
+}
+template <int D>
+__device__ __forceinline__ int cell_code(int cx, int cy, int cz) {
+    if constexpr (D == 3) return (int)(spread3(cx) | (spread3(cy) << 1) | (spread3(cz) << 2));
+    else return (int)(spread2(cx) | (spread2(cy) << 1));
+}
+template <int D>
+__device__ __forceinline__ void cell_decode(int code, int& cx, int& cy, int& cz) {
+    if constexpr (D == 3) {
+        cx = (int)compact3((uint32_t)code);
+        cy = (int)compact3((uint32_t)code >> 1);
+        cz = (int)compact3((uint32_t)code >> 2);
+    } else {
+        cx = (int)compact2((uint32_t)code);
+        cy = (int)compact2((uint32_t)code >> 1);
+        cz = 0;
+    }
+}
+
 // exclusive scan of n int32 counts into out[0..n] (out[n] = total); one block of 1024.
 template <typename Tout>
 __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __restrict__ in, Tout* __restrict__ out,
@@ -77,7 +131,7 @@ __global__ void k_cell_assign(const double* __restrict__ x, int64_t N, double L,
         cidx[a] = min(max(c, 0), nc[a] - 1);
     }
     if (!ok) latch_error(err, BGK_E_OUT_OF_DOMAIN, i);
-    int cell = (D == 3) ? (cidx[2] * nc1 + cidx[1]) * nc0 + cidx[0] : cidx[1] * nc0 + cidx[0];
+    const int cell = cell_code<D>(cidx[0], cidx[1], cidx[2]);
     cell_of[i] = cell;
     atomicAdd(cell_cnt + cell, 1);
 }
@@ -156,7 +210,8 @@ __global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, 
 #pragma unroll
     for (int a = 0; a < D; ++a) xi[a] = x[i * D + a];
     const int cell = cell_of[i];
-    const int cx = cell % nc0, cy = (cell / nc0) % nc1, cz = (D == 3) ? cell / (nc0 * nc1) : 0;
+    int cx, cy, cz;
+    cell_decode<D>(cell, cx, cy, cz);
     int m = 0;
     for (int dz = (D == 3 ? -1 : 0); dz <= (D == 3 ? 1 : 0); ++dz) {
         const int z = cz + dz;
@@ -167,7 +222,7 @@ __global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, 
             for (int dx = -1; dx <= 1; ++dx) {
                 const int xx = cx + dx;
                 if (xx < 0 || xx >= nc0) continue;
-                const int c = (z * nc1 + y) * nc0 + xx;
+                const int c = cell_code<D>(xx, y, z);
                 const int cb = cell_start[c], ce = cell_start[c + 1];
                 for (int base = cb; base < ce; base += 32) {
                     const int t = base + lane;

@@ -33,7 +33,7 @@ namespace bgk {
 
 namespace {
 
-constexpr int kDefaultWarps = 8;   // warps per block (= particles per block); tuned on B200, see DESIGN.md
+constexpr int kDefaultWarps = 4;   // warps per block (= particles per block); tuned on B200 (profiles/r01_tuning.md)
 
 struct TArgs {
     const double* __restrict__ f;
@@ -45,6 +45,12 @@ struct TArgs {
     const double* __restrict__ P;
     double* __restrict__ partials;
     unsigned long long* stab;
+    unsigned long long* work;          // persistent-warp item counter (zeroed before each launch)
+    const int32_t* __restrict__ gU;    // grouped kernel: union neighbour list per particle group
+    const int32_t* __restrict__ gUlen; //                 its length
+    const uint8_t* __restrict__ gCnt;  //                 users of each union member
+    const uint16_t* __restrict__ upos; //                 union position of each CSR entry
+    int ucap;                          //                 capacity per group
     int64_t n_int;
     int n1, ncol, ncs, c0, ncg, nwpp;
     double vmax, dv, dt;
@@ -113,9 +119,22 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
     unsigned char* ring = smem_raw + (size_t)wib * NST * St::BYTES;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)WPB * NST * St::BYTES) + wib * NST;
 
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    // One (particle, chunk x column group) item per warp; gridDim.y (the column group) is the
+    // slowest launch dimension so one group's f slab stays L2-resident.  (A persistent-warp
+    // variant pulling items from a global counter measured 8 % slower on C5; the ring
+    // indexing below keeps the running stage offset g0 so items could be chained.)
+    const uint32_t g0 = 0;
+    {
+    const int w = blockIdx.y;
     const int64_t pos = (int64_t)blockIdx.x * WPB + wib;
     if (pos >= A.n_int) return;                           // warp-uniform
-    const int w = blockIdx.y;
     const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
     const int p = A.order[pos];
     const int col = cg * 32 + lane;
@@ -131,20 +150,16 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
     int nbA = lane < m ? __ldg(nbl + lane) : 0;
     int nbB = 32 + lane < m ? __ldg(nbl + 32 + lane) : 0;
 
-    auto issue = [&](int e, int jn) {      // lane 0 only: stage e % NST <- neighbour e
-        const int s = e % NST;
+    auto issue = [&](int e, int jn) {      // lane 0 only: ring stage of neighbour e <- its box + pair data
+        const int s = (int)((g0 + (uint32_t)e) % NST);
         unsigned char* st = ring + s * St::BYTES;
         mbar_expect_tx(bars + s, St::F_BYTES + St::P_BYTES);
+#ifdef BGK_EXP_SAMEBOX
+        jn = p;   // timing experiment: always the particle's own (L2-hot) box
+#endif
         tma_load_3d(st, &tmap, cg * ROW, k1s, jn, bars + s);
         bulk_load(st + St::F_BYTES, Pp + (int64_t)e * PD, St::P_BYTES, bars + s);
     };
-    if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncwarp();
 #pragma unroll
     for (int s = 0; s < NST; ++s) {
         const int jn = __shfl_sync(0xffffffffu, nbA, s);
@@ -171,16 +186,14 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
 #pragma unroll
         for (int q = 0; q < NV; ++q) Qf[r][q] = 0.0;
     }
-    for (int e = 0; e < m; ++e) {
-        const int s = e % NST;
-        const uint32_t parity = (uint32_t)(e / NST) & 1u;
-        const unsigned char* stb = ring + s * St::BYTES;
-        mbar_wait(bars + s, parity);
+    // per-neighbour coefficients at the chunk's first node: y_e = P_e . c0, dy_e = dv P_e[0],
+    // L = sum_e y_e, dL = sum_e dy_e (read from the stage's pair-data slot)
+    auto coeffs = [&](int e, double (&y)[D], double (&dy)[D], double& Lc, double& dL) {
+        const double* ps =
+            reinterpret_cast<const double*>(ring + ((g0 + (uint32_t)e) % NST) * St::BYTES + St::F_BYTES);
         double pv[PD];
-        const double* ps = reinterpret_cast<const double*>(stb + St::F_BYTES);
 #pragma unroll
         for (int q = 0; q < PD; ++q) pv[q] = ps[q];       // broadcast LDS
-        double y[D], dy[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
             double t = pv[k * D] * c0v[0];
@@ -189,46 +202,78 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
             y[k] = t;
             dy[k] = A.dv * pv[k * D];
         }
-        double Lc = y[0], dL = dy[0];
+        Lc = y[0];
+        dL = dy[0];
 #pragma unroll
         for (int k = 1; k < D; ++k) { Lc += y[k]; dL += dy[k]; }
-        const double* st = reinterpret_cast<const double*>(stb) + lane * NV;
+    };
+    // Neighbours are consumed in pairs: one pass over the R rows applies two neighbour boxes,
+    // so the per-neighbour pipeline overhead (barrier waits, warp sync, refill issue) is paid
+    // once per two neighbours and the two independent coefficient streams double the ILP.
+    // An odd tail pairs the last neighbour with an all-zero coefficient set (C = 0 exactly).
+    auto row_coef = [&](double rr, const double (&y)[D], const double (&dy)[D], double Lc, double dL) {
+        // y_e(r) = y_e(0) + r dy_e: one FMA each with r an immediate -> rows are independent
+        const double Lr = fma(rr, dL, Lc);
+        if constexpr (D == 3) {
+            const double yn = fma(rr, dy[0], y[0]);
+            const double yt = fma(rr, dy[1], y[1]);
+            const double yb = fma(rr, dy[2], y[2]);
+            return (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
+        } else {
+            const double yn = fma(rr, dy[0], y[0]);
+            const double yt = fma(rr, dy[1], y[1]);
+            return (Lr - fabs(yn)) - fabs(yt);
+        }
+    };
+    for (int e = 0; e < m; e += 2) {
+        const bool two = e + 1 < m;
+        const uint32_t ge = g0 + (uint32_t)e;
+        double yA[D], dyA[D], LA, dLA, yB[D], dyB[D], LB = 0.0, dLB = 0.0;
+#pragma unroll
+        for (int k = 0; k < D; ++k) { yB[k] = 0.0; dyB[k] = 0.0; }
+        mbar_wait(bars + ge % NST, (ge / NST) & 1u);
+        coeffs(e, yA, dyA, LA, dLA);
+        const double* stA = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) + lane * NV;
+        const double* stB = stA;
+        if (two) {
+            mbar_wait(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u);
+            coeffs(e + 1, yB, dyB, LB, dLB);
+            stB = reinterpret_cast<const double*>(ring + ((ge + 1) % NST) * St::BYTES) + lane * NV;
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            // y_e(r) = y_e(0) + r dy_e: one FMA each with r an immediate -> rows are independent
-            // (no add chain across r); C = (L - |y_n|) - (|y_t| + |y_b|) keeps the chain 2 deep
             const double rr = (double)r;
-            const double Lr = fma(rr, dL, Lc);
-            double C;
-            if constexpr (D == 3) {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                const double yb = fma(rr, dy[2], y[2]);
-                C = (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
-            } else {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                C = (Lr - fabs(yn)) - fabs(yt);
-            }
+            const double CA = row_coef(rr, yA, dyA, LA, dLA);
+            const double CB = row_coef(rr, yB, dyB, LB, dLB);
             if constexpr (NV == 1) {
-                const double v = st[r * ROW];
-                Qf[r][0] = fma(C, v, Qf[r][0]);
+                Qf[r][0] = fma(CA, stA[r * ROW], Qf[r][0]);
+                Qf[r][0] = fma(CB, stB[r * ROW], Qf[r][0]);
             } else {
-                const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
-                Qf[r][0] = fma(C, v.x, Qf[r][0]);
-                Qf[r][1] = fma(C, v.y, Qf[r][1]);
+                const double2 vA = *reinterpret_cast<const double2*>(stA + r * ROW);
+                const double2 vB = *reinterpret_cast<const double2*>(stB + r * ROW);
+                Qf[r][0] = fma(CA, vA.x, Qf[r][0]);
+                Qf[r][1] = fma(CA, vA.y, Qf[r][1]);
+                Qf[r][0] = fma(CB, vB.x, Qf[r][0]);
+                Qf[r][1] = fma(CB, vB.y, Qf[r][1]);
             }
-            Sc[r] += C;
+            Sc[r] += CA + CB;
         }
-        // refill stage s with neighbour e + NST (index from the register batches)
-        const int t = e + NST;
-        if ((t & 31) == 0) {                               // warp-uniform batch rotation
-            nbA = nbB;
-            nbB = t + 32 + lane < m ? __ldg(nbl + t + 32 + lane) : 0;
+        // refill the two consumed stages with neighbours e+NST, e+1+NST
+        int jr[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int t = e + q + NST;
+            if ((t & 31) == 0) {                           // warp-uniform batch rotation
+                nbA = nbB;
+                nbB = t + 32 + lane < m ? __ldg(nbl + t + 32 + lane) : 0;
+            }
+            jr[q] = __shfl_sync(0xffffffffu, nbA, t & 31);
         }
-        const int jn = __shfl_sync(0xffffffffu, nbA, t & 31);
-        __syncwarp();   // every lane has consumed stage s before it is refilled
-        if (lane == 0 && t < m) issue(t, jn);
+        __syncwarp();   // every lane has consumed both stages before they are refilled
+        if (lane == 0) {
+            if (e + NST < m) issue(e + NST, jr[0]);
+            if (e + 1 + NST < m) issue(e + 1 + NST, jr[1]);
+        }
     }
     // epilogue: ftilde, moment partials, stability bound
     const int64_t rowstride = (int64_t)A.ncs * NV;
@@ -246,6 +291,271 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, sE = 0.0, amax = 0.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
+        if (k1s + r >= A.n1) break;                      // ragged last chunk (rows past Nv are TMA zero-fill)
+        const double v1 = axis_node(A.vmax, A.dv, k1s + r);
+        const double vv = (D == 3) ? v1 * v1 + v2v * v2v + v3v * v3v : v1 * v1 + v2v * v2v;
+        double out[NV];
+        if constexpr (NV == 1) {
+            const double fv = __ldg(fi + r * rowstride);
+            out[0] = fv - A.dt * (Qf[r][0] - fv * Sc[r]);
+            if (valid) fto[r * rowstride] = out[0];
+        } else {
+            const double2 fv = __ldg(reinterpret_cast<const double2*>(fi + r * rowstride));
+            out[0] = fv.x - A.dt * (Qf[r][0] - fv.x * Sc[r]);
+            out[1] = fv.y - A.dt * (Qf[r][1] - fv.y * Sc[r]);
+            if (valid) *reinterpret_cast<double2*>(fto + r * rowstride) = make_double2(out[0], out[1]);
+        }
+        if (valid) {
+            s0 += out[0];
+            s1 += v1 * out[0];
+            s2 += v2v * out[0];
+            if constexpr (D == 3) s3 += v3v * out[0];
+            sE += vv * out[0];
+            if constexpr (NV == 2) sE += out[1];
+            amax = fmax(amax, -Sc[r]);
+        }
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    s3 = warp_sum(s3);
+    sE = warp_sum(sE);
+    amax = warp_max(amax);
+    if (lane == 0) {
+        double* pp = A.partials + ((int64_t)p * A.nwpp + w) * kPM;
+        pp[0] = s0;
+        pp[1] = s1;
+        pp[2] = s2;
+        if constexpr (D == 3) {
+            pp[3] = s3;
+            pp[4] = sE;
+        } else {
+            pp[3] = sE;
+            pp[4] = 0.0;
+        }
+        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+    }
+    }
+}
+// ============================================================================
+// Grouped transport: one block = G particles (consecutive in the Morton-ordered interior
+// list) x one (chunk, column group).  The block walks the sorted UNION of the G neighbour
+// lists (precomputed per step by k_group_union); every union neighbour's box is fetched
+// ONCE by TMA into a block-shared ring and consumed by every warp whose particle has it.
+// On C5 the union of 8 Morton-consecutive particles has ~276 members against 947
+// per-particle neighbours, so the L2 -> SM traffic that bounded the per-warp ring
+// (~12-13 TB/s, the chip's L2 throughput cap) drops 3.4x.
+//   stage fill  : cp.async.bulk.tensor.3d, complete_tx on full[s]
+//   stage reuse : each warp, after waiting full[s] and (if the neighbour is its own)
+//                 applying it, bumps rel[s]; the G-th release re-arms and refills the stage
+//                 NST union members ahead.  Warps may drift up to NST members apart.
+//   pair data   : per warp, batches of 8 pair records by cp.async.bulk into a 2-deep ring.
+// ============================================================================
+constexpr int kGroup = 8;
+constexpr int kPBatch = 8;
+#ifndef BGK_GRP_MAX_STAGES
+#define BGK_GRP_MAX_STAGES 32
+#endif
+constexpr int kMaxGrpStages = BGK_GRP_MAX_STAGES;   // shared ring depth cap (smem bound: ~30 at R = 25)
+
+template <int D, int R>
+struct GStage {
+    static constexpr int NV = (D == 2) ? 2 : 1;
+    static constexpr int PD = (D == 2) ? 4 : 10;
+    static constexpr int ROW = 32 * NV;
+    static constexpr uint32_t F_BYTES = R * ROW * sizeof(double);           // multiple of 128 (R*256)
+    static constexpr uint32_t PB_BYTES = kPBatch * PD * sizeof(double);    // 640 B (3D) / 256 B (2D)
+};
+
+template <int D, int R, int NST>
+constexpr size_t grp_smem_bytes(int ucap) {
+    using St = GStage<D, R>;
+    return (size_t)NST * St::F_BYTES + (size_t)kGroup * 2 * St::PB_BYTES + (size_t)ucap * 5 +
+           (NST + 2 * kGroup) * 8 + NST * 8 + 256;
+}
+
+template <int D, int R, int NST>
+__global__ void __launch_bounds__(kGroup * 32, 1) k_transport_grp(const __grid_constant__ CUtensorMap tmap,
+                                                                  const TArgs A) {
+    using St = GStage<D, R>;
+    constexpr int NV = St::NV;
+    constexpr int PD = St::PD;
+    constexpr int ROW = St::ROW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char* ring = smem_raw;
+    double* pring = reinterpret_cast<double*>(smem_raw + (size_t)NST * St::F_BYTES);
+    int32_t* sU = reinterpret_cast<int32_t*>(smem_raw + (size_t)NST * St::F_BYTES + (size_t)kGroup * 2 * St::PB_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sU + A.ucap + ((A.ucap & 1) ? 1 : 0));
+    uint64_t* pbar = full + NST;                            // [kGroup][2]
+    int* rel = reinterpret_cast<int*>(pbar + 2 * kGroup);   // [NST]
+    volatile int* smem_member = rel + NST;                  // [NST] union member a stage holds / will hold
+    uint8_t* sCnt = reinterpret_cast<uint8_t*>(rel + 2 * NST);  // [ucap]
+
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int group = blockIdx.x;
+    const int w = blockIdx.y;
+    const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
+    const int k1s = chunk * R;
+    const int ulen = A.gUlen[group];
+    const int32_t* gU = A.gU + (int64_t)group * A.ucap;
+    for (int q = threadIdx.x; q < ulen; q += blockDim.x) {
+        sU[q] = gU[q];
+        sCnt[q] = A.gCnt[(int64_t)group * A.ucap + q];
+    }
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(full + s, 1);
+            rel[s] = 0;
+            smem_member[s] = s;
+        }
+        for (int g = 0; g < 2 * kGroup; ++g) mbar_init(pbar + g, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int s = 0; s < NST && s < ulen; ++s) {
+            mbar_expect_tx(full + s, St::F_BYTES);
+            tma_load_3d(ring + s * St::F_BYTES, &tmap, cg * ROW, k1s, sU[s], full + s);
+        }
+
+    // this warp's particle (an idle warp of a short last group still releases every stage)
+    const int64_t pos = (int64_t)group * kGroup + wib;
+    const bool active = pos < A.n_int;
+    const int p = active ? A.order[pos] : 0;
+    const int64_t off = active ? A.nb_off[p] : 0;
+    const int m = active ? (int)(A.nb_off[p + 1] - off) : 0;
+    const double* Pp = A.P + off * PD;
+    const int col = cg * 32 + lane;
+    const bool valid = active && col < A.ncol;
+    const int colc = col < A.ncol ? col : 0;
+    const int gc = A.c0 + colc;
+    const uint16_t* upl = A.upos + off;
+    int nbA = lane < m ? (int)__ldg(upl + lane) : 0;       // union positions of my neighbours, 32 per batch
+    int nbB = 32 + lane < m ? (int)__ldg(upl + 32 + lane) : 0;
+    double* myP = pring + (size_t)wib * 2 * kPBatch * PD;
+    auto issue_pbatch = [&](int b) {          // lane 0: pair records [8b, 8b+8) -> buffer b & 1
+        const int n = min(kPBatch, m - b * kPBatch);
+        if (n <= 0) return;
+        uint64_t* bar = pbar + wib * 2 + (b & 1);
+        mbar_expect_tx(bar, (uint32_t)(n * PD * sizeof(double)));
+        bulk_load(myP + (b & 1) * kPBatch * PD, Pp + (int64_t)b * kPBatch * PD, (uint32_t)(n * PD * sizeof(double)),
+                  bar);
+    };
+    if (lane == 0) {
+        issue_pbatch(0);
+        issue_pbatch(1);
+    }
+
+    double Wp[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) Wp[a] = active ? A.W[(int64_t)p * D + a] : 0.0;
+    double c0v[D];
+    c0v[0] = axis_node(A.vmax, A.dv, k1s) - Wp[0];
+    if constexpr (D == 3) {
+        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+        c0v[1] = axis_node(A.vmax, A.dv, k2) - Wp[1];
+        c0v[2] = axis_node(A.vmax, A.dv, k3) - Wp[2];
+    } else {
+        c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
+    }
+    double Qf[R][NV], Sc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        Sc[r] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) Qf[r][q] = 0.0;
+    }
+    // Each warp visits only its own neighbours; neighbour e sits at union position u.  A
+    // member's stage is refilled (NST members ahead) by the last of its sCnt[u] users.
+    for (int e = 0; e < m; ++e) {
+        const int u = __shfl_sync(0xffffffffu, nbA, e & 31);
+        if ((e & 31) == 31) {                               // warp-uniform batch rotation
+            nbA = nbB;
+            nbB = e + 33 + lane < m ? (int)__ldg(upl + e + 33 + lane) : 0;
+        }
+        const int s = u % NST;
+        const int b = e / kPBatch, eb = e - b * kPBatch;
+        if (eb == 0) {
+            mbar_wait(pbar + wib * 2 + (b & 1), (uint32_t)(b >> 1) & 1u);
+            if (b >= 1 && lane == 0) issue_pbatch(b + 1);  // buffer (b+1)&1 held batch b-1: done
+        }
+        const double* ps = myP + (b & 1) * kPBatch * PD + eb * PD;
+        double pv[PD];
+#pragma unroll
+        for (int q = 0; q < PD; ++q) pv[q] = ps[q];
+        double y[D], dy[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            double t = pv[k * D] * c0v[0];
+#pragma unroll
+            for (int a = 1; a < D; ++a) t = fma(pv[k * D + a], c0v[a], t);
+            y[k] = t;
+            dy[k] = A.dv * pv[k * D];
+        }
+        double Lc = y[0], dL = dy[0];
+#pragma unroll
+        for (int k = 1; k < D; ++k) { Lc += y[k]; dL += dy[k]; }
+        // a warp may run many members ahead of a slow one: wait until stage s has been armed for
+        // member u (parity waits alone cannot tell rounds two phases apart), then for the data
+        while (smem_member[s] != u) __nanosleep(64);
+        mbar_wait(full + s, (uint32_t)(u / NST) & 1u);
+        const double* st = reinterpret_cast<const double*>(ring + s * St::F_BYTES) + lane * NV;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double rr = (double)r;
+            const double Lr = fma(rr, dL, Lc);
+            double C;
+            if constexpr (D == 3) {
+                const double yn = fma(rr, dy[0], y[0]);
+                const double yt = fma(rr, dy[1], y[1]);
+                const double yb = fma(rr, dy[2], y[2]);
+                C = (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
+            } else {
+                const double yn = fma(rr, dy[0], y[0]);
+                const double yt = fma(rr, dy[1], y[1]);
+                C = (Lr - fabs(yn)) - fabs(yt);
+            }
+            if constexpr (NV == 1) {
+                Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
+            } else {
+                const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
+                Qf[r][0] = fma(C, v.x, Qf[r][0]);
+                Qf[r][1] = fma(C, v.y, Qf[r][1]);
+            }
+            Sc[r] += C;
+        }
+        __syncwarp();
+        if (lane == 0) {                                    // release; the member's last user refills
+            if (atomicAdd(rel + s, 1) == (int)sCnt[u] - 1) {
+                rel[s] = 0;
+                if (u + NST < ulen) {
+                    smem_member[s] = u + NST;
+                    __threadfence_block();
+                    mbar_expect_tx(full + s, St::F_BYTES);
+                    tma_load_3d(ring + s * St::F_BYTES, &tmap, cg * ROW, k1s, sU[u + NST], full + s);
+                }
+            }
+        }
+    }
+    if (!active) return;
+    // epilogue (as k_transport): ftilde, moment partials, stability bound
+    const int64_t rowstride = (int64_t)A.ncs * NV;
+    const int64_t lane_off = (int64_t)k1s * rowstride + (int64_t)colc * NV;
+    const double* fi = A.f + (int64_t)p * A.n1 * rowstride + lane_off;
+    double* fto = A.ft + (int64_t)p * A.n1 * rowstride + lane_off;
+    double v2v = 0.0, v3v = 0.0;
+    if constexpr (D == 3) {
+        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+        v2v = axis_node(A.vmax, A.dv, k2);
+        v3v = axis_node(A.vmax, A.dv, k3);
+    } else {
+        v2v = axis_node(A.vmax, A.dv, gc);
+    }
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, sE = 0.0, amax = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (k1s + r >= A.n1) break;
         const double v1 = axis_node(A.vmax, A.dv, k1s + r);
         const double vv = (D == 3) ? v1 * v1 + v2v * v2v + v3v * v3v : v1 * v1 + v2v * v2v;
         double out[NV];
@@ -291,32 +601,384 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
     }
 }
 
+// Union of the neighbour lists of each group of kGroup consecutive particles of `order`:
+// bitonic sort of the concatenated lists in shared memory, then drop duplicates.
+__global__ void __launch_bounds__(256) k_group_union(const int32_t* __restrict__ order, int64_t n_int,
+                                                     const int64_t* __restrict__ nb_off,
+                                                     const int32_t* __restrict__ nb_idx, int ucap,
+                                                     int32_t* __restrict__ gU, int32_t* __restrict__ gUlen,
+                                                     uint8_t* __restrict__ gCnt, uint16_t* __restrict__ upos) {
+    extern __shared__ int32_t sa[];                         // [ucap] sort buffer, then [ucap] union
+    int32_t* su = sa + ucap;
+    __shared__ int s_len[kGroup + 1];
+    __shared__ int wsum[8];
+    const int group = blockIdx.x;
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int g = 0; g < kGroup; ++g) {
+            const int64_t pos = (int64_t)group * kGroup + g;
+            s_len[g] = tot;
+            if (pos < n_int) {
+                const int p = order[pos];
+                tot += (int)(nb_off[p + 1] - nb_off[p]);
+            }
+        }
+        s_len[kGroup] = tot;
+    }
+    __syncthreads();
+    const int tot = s_len[kGroup];
+    int n2 = 1;
+    while (n2 < tot) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) sa[i] = INT_MAX;
+    __syncthreads();
+    for (int g = 0; g < kGroup; ++g) {
+        const int64_t pos = (int64_t)group * kGroup + g;
+        if (pos >= n_int) break;
+        const int p = order[pos];
+        const int64_t off = nb_off[p];
+        const int m = (int)(nb_off[p + 1] - off);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) sa[s_len[g] + i] = nb_idx[off + i];
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int a = sa[i], b = sa[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        sa[i] = b;
+                        sa[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    // compaction of first occurrences, in order: per-thread contiguous chunk + block scan
+    const int per = (n2 + blockDim.x - 1) / blockDim.x;
+    const int b0 = threadIdx.x * per, b1 = min(n2, b0 + per);
+    int cnt = 0;
+    for (int i = b0; i < b1; ++i) cnt += (sa[i] != INT_MAX && (i == 0 || sa[i] != sa[i - 1]));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int v = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) wsum[wid] = v;
+    __syncthreads();
+    int base = v - cnt;
+    for (int q = 0; q < wid; ++q) base += wsum[q];
+    int32_t* out = gU + (int64_t)group * ucap;
+    uint8_t* cnt_out = gCnt + (int64_t)group * ucap;
+    for (int i = b0; i < b1; ++i)
+        if (sa[i] != INT_MAX && (i == 0 || sa[i] != sa[i - 1])) {
+            int run = 1;                                    // users of this member (<= kGroup)
+            while (i + run < n2 && sa[i + run] == sa[i]) ++run;
+            su[base] = sa[i];
+            out[base] = sa[i];
+            cnt_out[base] = (uint8_t)run;
+            ++base;
+        }
+    __shared__ int s_ulen;
+    if (threadIdx.x == blockDim.x - 1) {
+        gUlen[group] = base;
+        s_ulen = base;
+    }
+    __syncthreads();
+    const int ulen = s_ulen;
+    // position of every neighbour entry of the group's particles inside the union (binary search)
+    for (int g = 0; g < kGroup; ++g) {
+        const int64_t pos = (int64_t)group * kGroup + g;
+        if (pos >= n_int) break;
+        const int p = order[pos];
+        const int64_t off = nb_off[p];
+        const int m = (int)(nb_off[p + 1] - off);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+            const int v = nb_idx[off + i];
+            int lo = 0, hi = ulen - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (su[mid] < v) lo = mid + 1;
+                else hi = mid;
+            }
+            upos[off + i] = (uint16_t)lo;
+        }
+    }
+}
+
+// ============================================================================
+// Warp-specialised transport: the block's last warp is a TMA producer for the other
+// kWsConsumers warps (one particle each).  Producer lane c walks consumer c's neighbour
+// list, waits for the consumer to release a ring stage (empty[c][s]) and refills it
+// (box + pair record on full[c][s]).  Consumers only wait on full, apply the neighbour and
+// arrive on empty -- no refill issue, no warp-wide issue path in the hot loop.
+// ============================================================================
+constexpr int kWsConsumers = 7;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int D, int R, int NST>
+__global__ void __launch_bounds__((kWsConsumers + 1) * 32, 1) k_transport_ws(const __grid_constant__ CUtensorMap tmap,
+                                                                             const TArgs A) {
+    using St = Stage<D, R>;
+    constexpr int NV = St::NV;
+    constexpr int PD = St::PD;
+    constexpr int ROW = St::ROW;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kWsConsumers * NST * St::BYTES);
+    uint64_t* empty = full + kWsConsumers * NST;
+    const int w = blockIdx.y;
+    const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
+    const int k1s = chunk * R;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kWsConsumers * NST; ++q) {
+            mbar_init(full + q, 1);
+            mbar_init(empty + q, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (wib == kWsConsumers) {                              // ---------------- producer warp
+        const int c = lane;
+        if (c >= kWsConsumers) return;
+        const int64_t pos = (int64_t)blockIdx.x * kWsConsumers + c;
+        if (pos >= A.n_int) return;
+        const int p = A.order[pos];
+        const int64_t off = A.nb_off[p];
+        const int m = (int)(A.nb_off[p + 1] - off);
+        unsigned char* ring = smem_raw + (size_t)c * NST * St::BYTES;
+        for (int e = 0; e < m; ++e) {
+            const int s = e % NST;
+            const int jn = __ldg(A.nb_idx + off + e);
+            if (e >= NST) mbar_wait(empty + c * NST + s, (uint32_t)((e / NST) - 1) & 1u);
+            unsigned char* st = ring + s * St::BYTES;
+            mbar_expect_tx(full + c * NST + s, St::F_BYTES + St::P_BYTES);
+            tma_load_3d(st, &tmap, cg * ROW, k1s, jn, full + c * NST + s);
+            bulk_load(st + St::F_BYTES, A.P + (off + e) * PD, St::P_BYTES, full + c * NST + s);
+        }
+        return;
+    }
+    // ---------------------------------------------------------------- consumer warps
+    const int64_t pos = (int64_t)blockIdx.x * kWsConsumers + wib;
+    if (pos >= A.n_int) return;
+    const int p = A.order[pos];
+    const int col = cg * 32 + lane;
+    const bool valid = col < A.ncol;
+    const int colc = valid ? col : 0;
+    const int gc = A.c0 + colc;
+    const int64_t off = A.nb_off[p];
+    const int m = (int)(A.nb_off[p + 1] - off);
+    const unsigned char* ring = smem_raw + (size_t)wib * NST * St::BYTES;
+    double Wp[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) Wp[a] = A.W[(int64_t)p * D + a];
+    double c0v[D];
+    c0v[0] = axis_node(A.vmax, A.dv, k1s) - Wp[0];
+    if constexpr (D == 3) {
+        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+        c0v[1] = axis_node(A.vmax, A.dv, k2) - Wp[1];
+        c0v[2] = axis_node(A.vmax, A.dv, k3) - Wp[2];
+    } else {
+        c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
+    }
+    double Qf[R][NV], Sc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        Sc[r] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) Qf[r][q] = 0.0;
+    }
+    for (int e = 0; e < m; ++e) {
+        const int s = e % NST;
+        const unsigned char* stb = ring + s * St::BYTES;
+        mbar_wait(full + wib * NST + s, (uint32_t)(e / NST) & 1u);
+        const double* ps = reinterpret_cast<const double*>(stb + St::F_BYTES);
+        double pv[PD];
+#pragma unroll
+        for (int q = 0; q < PD; ++q) pv[q] = ps[q];
+        double y[D], dy[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            double t = pv[k * D] * c0v[0];
+#pragma unroll
+            for (int a = 1; a < D; ++a) t = fma(pv[k * D + a], c0v[a], t);
+            y[k] = t;
+            dy[k] = A.dv * pv[k * D];
+        }
+        double Lc = y[0], dL = dy[0];
+#pragma unroll
+        for (int k = 1; k < D; ++k) { Lc += y[k]; dL += dy[k]; }
+        const double* st = reinterpret_cast<const double*>(stb) + lane * NV;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double rr = (double)r;
+            const double Lr = fma(rr, dL, Lc);
+            double C;
+            if constexpr (D == 3) {
+                const double yn = fma(rr, dy[0], y[0]);
+                const double yt = fma(rr, dy[1], y[1]);
+                const double yb = fma(rr, dy[2], y[2]);
+                C = (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
+            } else {
+                const double yn = fma(rr, dy[0], y[0]);
+                const double yt = fma(rr, dy[1], y[1]);
+                C = (Lr - fabs(yn)) - fabs(yt);
+            }
+            if constexpr (NV == 1) {
+                Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
+            } else {
+                const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
+                Qf[r][0] = fma(C, v.x, Qf[r][0]);
+                Qf[r][1] = fma(C, v.y, Qf[r][1]);
+            }
+            Sc[r] += C;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + wib * NST + s);  // stage s free for the producer
+    }
+    // epilogue (as k_transport)
+    const int64_t rowstride = (int64_t)A.ncs * NV;
+    const int64_t lane_off = (int64_t)k1s * rowstride + (int64_t)colc * NV;
+    const double* fi = A.f + (int64_t)p * A.n1 * rowstride + lane_off;
+    double* fto = A.ft + (int64_t)p * A.n1 * rowstride + lane_off;
+    double v2v = 0.0, v3v = 0.0;
+    if constexpr (D == 3) {
+        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+        v2v = axis_node(A.vmax, A.dv, k2);
+        v3v = axis_node(A.vmax, A.dv, k3);
+    } else {
+        v2v = axis_node(A.vmax, A.dv, gc);
+    }
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, sE = 0.0, amax = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (k1s + r >= A.n1) break;
+        const double v1 = axis_node(A.vmax, A.dv, k1s + r);
+        const double vv = (D == 3) ? v1 * v1 + v2v * v2v + v3v * v3v : v1 * v1 + v2v * v2v;
+        double out[NV];
+        if constexpr (NV == 1) {
+            const double fv = __ldg(fi + r * rowstride);
+            out[0] = fv - A.dt * (Qf[r][0] - fv * Sc[r]);
+            if (valid) fto[r * rowstride] = out[0];
+        } else {
+            const double2 fv = __ldg(reinterpret_cast<const double2*>(fi + r * rowstride));
+            out[0] = fv.x - A.dt * (Qf[r][0] - fv.x * Sc[r]);
+            out[1] = fv.y - A.dt * (Qf[r][1] - fv.y * Sc[r]);
+            if (valid) *reinterpret_cast<double2*>(fto + r * rowstride) = make_double2(out[0], out[1]);
+        }
+        if (valid) {
+            s0 += out[0];
+            s1 += v1 * out[0];
+            s2 += v2v * out[0];
+            if constexpr (D == 3) s3 += v3v * out[0];
+            sE += vv * out[0];
+            if constexpr (NV == 2) sE += out[1];
+            amax = fmax(amax, -Sc[r]);
+        }
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    s3 = warp_sum(s3);
+    sE = warp_sum(sE);
+    amax = warp_max(amax);
+    if (lane == 0) {
+        double* pp = A.partials + ((int64_t)p * A.nwpp + w) * kPM;
+        pp[0] = s0;
+        pp[1] = s1;
+        pp[2] = s2;
+        if constexpr (D == 3) {
+            pp[3] = s3;
+            pp[4] = sE;
+        } else {
+            pp[3] = sE;
+            pp[4] = 0.0;
+        }
+        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+    }
+}
+
+template <int D, int R>
+void launch_ws_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
+    constexpr int B = Stage<D, R>::BYTES;
+    constexpr int NST = []() {
+        int n = 2;
+        while (n < 8 && (size_t)kWsConsumers * (n + 1) * B + 2 * kWsConsumers * (n + 1) * 8 <= 220 * 1024) ++n;
+        return n;
+    }();
+    constexpr size_t smem = (size_t)kWsConsumers * NST * B + 2 * kWsConsumers * NST * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_transport_ws<D, R, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    const unsigned gx = (unsigned)((a.n_int + kWsConsumers - 1) / kWsConsumers);
+    k_transport_ws<D, R, NST><<<dim3(gx, (unsigned)a.nwpp), (kWsConsumers + 1) * 32, smem, s>>>(tm, a);
+}
+
+template <int D>
+void dispatch_ws(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
+    if constexpr (D == 3) {
+        switch (R) {
+            case 25: launch_ws_one<D, 25>(tm, a, s); return;
+            case 21: launch_ws_one<D, 21>(tm, a, s); return;
+            case 17: launch_ws_one<D, 17>(tm, a, s); return;
+            default: break;
+        }
+    }
+    switch (R) {
+        case 13: launch_ws_one<D, 13>(tm, a, s); break;
+        case 11: launch_ws_one<D, 11>(tm, a, s); break;
+        case 9: launch_ws_one<D, 9>(tm, a, s); break;
+        case 7: launch_ws_one<D, 7>(tm, a, s); break;
+        case 5: launch_ws_one<D, 5>(tm, a, s); break;
+        case 3: launch_ws_one<D, 3>(tm, a, s); break;
+        default: launch_ws_one<D, 1>(tm, a, s); break;
+    }
+}
+
 template <int D, int R, int WPB>
 constexpr int stages_for() {
     // ring depth: keep NST-1 neighbour boxes in flight; bounded by 227 KB of shared memory
-    constexpr int n = (220 * 1024) / (WPB * Stage<D, R>::BYTES);
-    return n > 4 ? 4 : (n < 2 ? 2 : n);
+    // (sized for 8 resident warps per SM: blocks of WPB warps, 8 / WPB blocks per SM)
+    constexpr int blocks = WPB >= 8 ? 1 : 8 / WPB;
+    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R>::BYTES);
+    return n > 8 ? 8 : (n < 2 ? 2 : n);
 }
 
 template <int D, int R, int WPB>
 void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     constexpr int NST = stages_for<D, R, WPB>();
     constexpr size_t smem = (size_t)WPB * NST * Stage<D, R>::BYTES + WPB * NST * 8;
-    static bool configured = false;
-    if (!configured) {
+    static int grid = 0;
+    if (!grid) {
         cudaFuncSetAttribute(k_transport<D, R, NST, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_transport<D, R, NST, WPB>, WPB * 32, smem);
+        grid = sms * (per_sm > 0 ? per_sm : 1);
     }
+    (void)grid;
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
     k_transport<D, R, NST, WPB><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
 }
 
 template <int D, int R>
 void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    if constexpr (D == 3 && (R == 25 || R == 17)) {
+    if constexpr (D == 3 && (R == 25 || R == 17 || R == 13 || R == 9)) {
         if (wpb == 12) return launch_one<D, R, 12>(tm, a, s);
         if (wpb == 16) return launch_one<D, R, 16>(tm, a, s);
         if (wpb == 4) return launch_one<D, R, 4>(tm, a, s);
+        if (wpb == 2) return launch_one<D, R, 2>(tm, a, s);
     }
     launch_one<D, R, kDefaultWarps>(tm, a, s);
 }
@@ -342,14 +1004,73 @@ void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_
     }
 }
 
+template <int D, int R>
+void launch_grp_one(const CUtensorMap& tm, const TArgs& a, int n_groups, cudaStream_t s) {
+    // ring depth from the shared-memory budget (one block per SM), 4..16 stages
+    constexpr int F = GStage<D, R>::F_BYTES;
+    constexpr int NST = []() {
+        int n = 4;
+        while (n < kMaxGrpStages && grp_smem_bytes<D, R, 16>(0) - 16 * F + (n + 1) * F + 16384 <= 225 * 1024) ++n;
+        return n;
+    }();
+    const size_t smem = grp_smem_bytes<D, R, NST>(a.ucap);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_transport_grp<D, R, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    k_transport_grp<D, R, NST><<<dim3((unsigned)n_groups, (unsigned)a.nwpp), kGroup * 32, smem, s>>>(tm, a);
+}
+
+template <int D>
+void dispatch_grp(int R, const CUtensorMap& tm, const TArgs& a, int n_groups, cudaStream_t s) {
+    if constexpr (D == 3) {
+        switch (R) {
+            case 25: launch_grp_one<D, 25>(tm, a, n_groups, s); return;
+            case 21: launch_grp_one<D, 21>(tm, a, n_groups, s); return;
+            case 17: launch_grp_one<D, 17>(tm, a, n_groups, s); return;
+            default: break;
+        }
+    }
+    switch (R) {
+        case 13: launch_grp_one<D, 13>(tm, a, n_groups, s); break;
+        case 11: launch_grp_one<D, 11>(tm, a, n_groups, s); break;
+        case 9: launch_grp_one<D, 9>(tm, a, n_groups, s); break;
+        case 7: launch_grp_one<D, 7>(tm, a, n_groups, s); break;
+        case 5: launch_grp_one<D, 5>(tm, a, n_groups, s); break;
+        case 3: launch_grp_one<D, 3>(tm, a, n_groups, s); break;
+        default: launch_grp_one<D, 1>(tm, a, n_groups, s); break;
+    }
+}
+
 constexpr int kRChoices3[] = {25, 21, 17, 13, 11, 9, 7, 5, 3, 1};
 constexpr int kRChoices2[] = {13, 11, 9, 7, 5, 3, 1};
 
 }  // namespace
 
+int group_size() { return kGroup; }
+
+void launch_group_union(bgk_ctx* c, cudaStream_t s) {
+    if (!c->grouped || c->N_int == 0) return;
+    const int n_groups = (int)((c->N_int + kGroup - 1) / kGroup);
+    k_group_union<<<n_groups, 256, 2 * sizeof(int32_t) * c->ucap, s>>>(c->g.order, c->N_int, c->g.nb_off,
+                                                                        c->g.nb_idx, c->ucap, c->gU, c->gUlen,
+                                                                        c->gCnt, c->upos);
+}
+
 // rows per thread: the largest divisor of n1 among the instantiated R (2D keeps three
 // accumulators per row, so it stops at 13)
 int transport_rows_per_thread(int d, int n1) {
+    if (const char* e = getenv("BGK_TRANSPORT_R")) {    // tuning knob: any instantiated R (ragged chunks OK)
+        const int r = atoi(e);
+        if (d == 3) {
+            for (int R : kRChoices3)
+                if (R == r) return R;
+        } else {
+            for (int R : kRChoices2)
+                if (R == r) return R;
+        }
+    }
     if (d == 3) {
         for (int R : kRChoices3)
             if (n1 % R == 0) return R;
@@ -397,6 +1118,7 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.P = c->g.P;
     a.partials = c->partials;
     a.stab = c->stab;
+    a.work = c->work;
     a.n_int = c->N_int;
     a.n1 = c->n1;
     a.ncol = c->ncol;
@@ -407,7 +1129,27 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.vmax = c->cfg.vmax;
     a.dv = c->dv;
     a.dt = c->cfg.dt;
+    a.gU = c->gU;
+    a.gUlen = c->gUlen;
+    a.gCnt = c->gCnt;
+    a.upos = c->upos;
+    a.ucap = c->ucap;
     const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
+    static const int variant = [] {     // 0: per-warp ring, 1: warp-specialised producer (tuning knob)
+        const char* e = getenv("BGK_TRANSPORT_WS");
+        return e ? atoi(e) : 0;
+    }();
+    if (variant == 1 && !c->grouped) {
+        if (c->d == 3) dispatch_ws<3>(c->R, tm, a, s);
+        else dispatch_ws<2>(c->R, tm, a, s);
+        return;
+    }
+    if (c->grouped) {
+        const int n_groups = (int)((c->N_int + kGroup - 1) / kGroup);
+        if (c->d == 3) dispatch_grp<3>(c->R, tm, a, n_groups, s);
+        else dispatch_grp<2>(c->R, tm, a, n_groups, s);
+        return;
+    }
     static const int wpb = [] {
         const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (4, 8, 12, 16); default 8
         return e ? atoi(e) : kDefaultWarps;

@@ -277,3 +277,24 @@ def test_set_get_f_roundtrip(torch_cuda):
         f = np.random.default_rng(0).uniform(size=(g.N, g.nval, g.Kloc))
         g.set_f(f)
         assert np.array_equal(g.get_f(), f)
+
+
+def test_cuda_graph_capture_matches_eager(torch_cuda):
+    """bgk_step enqueues no host synchronisation: three steps captured in a CUDA graph and
+    replayed give the bitwise result of three eager steps."""
+    import torch
+    cfg = bi.C4
+    eager, cloud = gpu(cfg)
+    eager.step(1)                       # warm-up (one-time kernel attribute setup) outside capture
+    eager.step(3)
+    g, _ = gpu(cfg, cloud)
+    g.step(1)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            g.step(3)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(g.get_f(), eager.get_f())
