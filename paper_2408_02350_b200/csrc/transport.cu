@@ -81,6 +81,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// one elected lane of a fully active warp (elect.sync): the TMA operands it uses are warp-uniform,
+// so the compiler issues them from uniform registers without a per-lane serialisation loop
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+// non-blocking phase test: 1 if the phase with the given parity has completed
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok;
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
                                             uint64_t* bar) {
     asm volatile(
@@ -207,72 +236,63 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
 #pragma unroll
         for (int k = 1; k < D; ++k) { Lc += y[k]; dL += dy[k]; }
     };
-    // Neighbours are consumed in pairs: one pass over the R rows applies two neighbour boxes,
-    // so the per-neighbour pipeline overhead (barrier waits, warp sync, refill issue) is paid
-    // once per two neighbours and the two independent coefficient streams double the ILP.
-    // An odd tail pairs the last neighbour with an all-zero coefficient set (C = 0 exactly).
-    auto row_coef = [&](double rr, const double (&y)[D], const double (&dy)[D], double Lc, double dL) {
-        // y_e(r) = y_e(0) + r dy_e: one FMA each with r an immediate -> rows are independent
-        const double Lr = fma(rr, dL, Lc);
-        if constexpr (D == 3) {
-            const double yn = fma(rr, dy[0], y[0]);
-            const double yt = fma(rr, dy[1], y[1]);
-            const double yb = fma(rr, dy[2], y[2]);
-            return (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
-        } else {
-            const double yn = fma(rr, dy[0], y[0]);
-            const double yt = fma(rr, dy[1], y[1]);
-            return (Lr - fabs(yn)) - fabs(yt);
-        }
-    };
-    for (int e = 0; e < m; e += 2) {
-        const bool two = e + 1 < m;
+    // The readiness of the NEXT stage is tested (non-blocking mbarrier.test_wait) before this
+    // neighbour's rows, so the barrier check's latency overlaps the row arithmetic; only if the
+    // next box has not landed by the end of the rows does the warp spin on try_wait.
+    double y[D], dy[D], Lc = 0.0, dL = 0.0;
+    if (m > 0) {
+        mbar_wait(bars + g0 % NST, (g0 / NST) & 1u);
+        coeffs(0, y, dy, Lc, dL);
+    }
+    for (int e = 0; e < m; ++e) {
         const uint32_t ge = g0 + (uint32_t)e;
-        double yA[D], dyA[D], LA, dLA, yB[D], dyB[D], LB = 0.0, dLB = 0.0;
-#pragma unroll
-        for (int k = 0; k < D; ++k) { yB[k] = 0.0; dyB[k] = 0.0; }
-        mbar_wait(bars + ge % NST, (ge / NST) & 1u);
-        coeffs(e, yA, dyA, LA, dLA);
-        const double* stA = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) + lane * NV;
-        const double* stB = stA;
-        if (two) {
-            mbar_wait(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u);
-            coeffs(e + 1, yB, dyB, LB, dLB);
-            stB = reinterpret_cast<const double*>(ring + ((ge + 1) % NST) * St::BYTES) + lane * NV;
-        }
+        const bool more = e + 1 < m;
+        const uint32_t nready = more ? mbar_test(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u) : 1u;
+        const double* st = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) + lane * NV;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            // y_e(r) = y_e(0) + r dy_e: one FMA each with r an immediate -> rows are independent
             const double rr = (double)r;
-            const double CA = row_coef(rr, yA, dyA, LA, dLA);
-            const double CB = row_coef(rr, yB, dyB, LB, dLB);
-            if constexpr (NV == 1) {
-                Qf[r][0] = fma(CA, stA[r * ROW], Qf[r][0]);
-                Qf[r][0] = fma(CB, stB[r * ROW], Qf[r][0]);
+            const double Lr = fma(rr, dL, Lc);
+            double C;
+            if constexpr (D == 3) {
+                const double yn = fma(rr, dy[0], y[0]);
+                const double yt = fma(rr, dy[1], y[1]);
+                const double yb = fma(rr, dy[2], y[2]);
+                C = (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
             } else {
-                const double2 vA = *reinterpret_cast<const double2*>(stA + r * ROW);
-                const double2 vB = *reinterpret_cast<const double2*>(stB + r * ROW);
-                Qf[r][0] = fma(CA, vA.x, Qf[r][0]);
-                Qf[r][1] = fma(CA, vA.y, Qf[r][1]);
-                Qf[r][0] = fma(CB, vB.x, Qf[r][0]);
-                Qf[r][1] = fma(CB, vB.y, Qf[r][1]);
+                const double yn = fma(rr, dy[0], y[0]);
+                const double yt = fma(rr, dy[1], y[1]);
+                C = (Lr - fabs(yn)) - fabs(yt);
             }
-            Sc[r] += CA + CB;
-        }
-        // refill the two consumed stages with neighbours e+NST, e+1+NST
-        int jr[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int t = e + q + NST;
-            if ((t & 31) == 0) {                           // warp-uniform batch rotation
-                nbA = nbB;
-                nbB = t + 32 + lane < m ? __ldg(nbl + t + 32 + lane) : 0;
+            if constexpr (NV == 1) {
+                Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
+            } else {
+                const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
+                Qf[r][0] = fma(C, v.x, Qf[r][0]);
+                Qf[r][1] = fma(C, v.y, Qf[r][1]);
             }
-            jr[q] = __shfl_sync(0xffffffffu, nbA, t & 31);
+            Sc[r] += C;
         }
-        __syncwarp();   // every lane has consumed both stages before they are refilled
-        if (lane == 0) {
-            if (e + NST < m) issue(e + NST, jr[0]);
-            if (e + 1 + NST < m) issue(e + 1 + NST, jr[1]);
+        // refill stage of neighbour e with neighbour e + NST (index from the register batches)
+        const int t = e + NST;
+        if ((t & 31) == 0) {                               // warp-uniform batch rotation
+            nbA = nbB;
+            nbB = t + 32 + lane < m ? __ldg(nbl + t + 32 + lane) : 0;
+        }
+        const int jn = __shfl_sync(0xffffffffu, nbA, t & 31);
+        __syncwarp();   // every lane has consumed the stage before it is refilled
+#ifndef BGK_EXP_NOPIPE   // timing experiment: no refills, no waits (stale data; compute ceiling)
+        if (t < m && elect_one()) issue(t, jn);
+#endif
+        if (more) {
+#ifndef BGK_EXP_NOPIPE
+            if (!nready) mbar_wait(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u);
+#else
+            (void)nready;
+#endif
+            asm volatile("" ::: "memory");                 // order the stage reads after the test
+            coeffs(e + 1, y, dy, Lc, dL);
         }
     }
     // epilogue: ftilde, moment partials, stability bound
@@ -716,14 +736,15 @@ __global__ void __launch_bounds__(256) k_group_union(const int32_t* __restrict__
 // (box + pair record on full[c][s]).  Consumers only wait on full, apply the neighbour and
 // arrive on empty -- no refill issue, no warp-wide issue path in the hot loop.
 // ============================================================================
-constexpr int kWsConsumers = 7;
+constexpr int kWsConsumers = 8;
+constexpr int kWsThreads = (kWsConsumers + 4) * 32;   // two consumer warpgroups + one producer warpgroup
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 template <int D, int R, int NST>
-__global__ void __launch_bounds__((kWsConsumers + 1) * 32, 1) k_transport_ws(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(kWsThreads, 1) k_transport_ws(const __grid_constant__ CUtensorMap tmap,
                                                                              const TArgs A) {
     using St = Stage<D, R>;
     constexpr int NV = St::NV;
@@ -746,9 +767,11 @@ __global__ void __launch_bounds__((kWsConsumers + 1) * 32, 1) k_transport_ws(con
     }
     __syncthreads();
 
-    if (wib == kWsConsumers) {                              // ---------------- producer warp
+    if (wib >= kWsConsumers) {                              // ---------------- producer warpgroup
+        // registers move from the producer warpgroup to the consumers (setmaxnreg)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
         const int c = lane;
-        if (c >= kWsConsumers) return;
+        if (wib != kWsConsumers || c >= kWsConsumers) return;
         const int64_t pos = (int64_t)blockIdx.x * kWsConsumers + c;
         if (pos >= A.n_int) return;
         const int p = A.order[pos];
@@ -767,6 +790,7 @@ __global__ void __launch_bounds__((kWsConsumers + 1) * 32, 1) k_transport_ws(con
         return;
     }
     // ---------------------------------------------------------------- consumer warps
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
     const int64_t pos = (int64_t)blockIdx.x * kWsConsumers + wib;
     if (pos >= A.n_int) return;
     const int p = A.order[pos];
@@ -921,7 +945,7 @@ void launch_ws_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
         configured = true;
     }
     const unsigned gx = (unsigned)((a.n_int + kWsConsumers - 1) / kWsConsumers);
-    k_transport_ws<D, R, NST><<<dim3(gx, (unsigned)a.nwpp), (kWsConsumers + 1) * 32, smem, s>>>(tm, a);
+    k_transport_ws<D, R, NST><<<dim3(gx, (unsigned)a.nwpp), kWsThreads, smem, s>>>(tm, a);
 }
 
 template <int D>
