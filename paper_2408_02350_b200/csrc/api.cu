@@ -127,6 +127,9 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->g.S = k.take<double>(N * d * d);
     c->g.P = k.take<double>((size_t)c->cap * c->PD);
     c->g.cw = k.take<double>(c->cap);
+    c->g.bidx = k.take<int32_t>(c->cap);
+    c->g.bcw = k.take<double>(c->cap);
+    c->g.bcnt = k.take<int32_t>(N);
     c->g.order = k.take<int32_t>(N);
     const int64_t ng = (N + group_size() - 1) / group_size();
     c->gU = k.take<int32_t>(c->grouped ? (size_t)ng * c->ucap : 1);

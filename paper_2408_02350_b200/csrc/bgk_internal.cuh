@@ -29,7 +29,10 @@ struct Geo {                    // per-step geometry arrays (device)
     int32_t* nb_idx;            // [cap]
     double* S;                  // [N][d*d]
     double* P;                  // [cap][PD] pair data p_n, p_t[, p_b] = abar n, bbar t[, gbar b]
-    double* cw;                 // [cap] boundary interpolation weights
+    double* cw;                 // [cap] boundary interpolation weights (aligned with the CSR)
+    int32_t* bidx;              // [cap] per boundary particle: its interior neighbours, compacted at the row start
+    double* bcw;                // [cap]   and their weights
+    int32_t* bcnt;              // [N]     count
     int32_t* order;             // [N_int] interior particles in cell order (transport processing order)
 };
 

@@ -289,47 +289,23 @@ template <int D>
 __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restrict__ bids, int64_t nb,
                                                           const int8_t* __restrict__ kind,
                                                           const int64_t* __restrict__ nb_off,
-                                                          const int32_t* __restrict__ nb_idx,
-                                                          const double* __restrict__ cw, double* __restrict__ f,
+                                                          const int32_t* __restrict__ bidx,
+                                                          const double* __restrict__ bcw,
+                                                          const int32_t* __restrict__ bcnt, double* __restrict__ f,
                                                           double* __restrict__ wallpart, int nch, int n1, int ncol,
-                                                          int ncs, int c0, int64_t Kloc, int max_nb, double vmax,
-                                                          double dv) {
+                                                          int ncs, int c0, int64_t Kloc, double vmax, double dv) {
     // Kloc here is the STORED node count per row (n1 * ncs)
     constexpr int NV = (D == 2) ? 2 : 1;
     __shared__ double sh[32];
-    __shared__ int s_cnt;
-    extern __shared__ unsigned char bsm[];
-    int32_t* sj = reinterpret_cast<int32_t*>(bsm);                 // interior neighbours of b (compacted)
-    double* sc = reinterpret_cast<double*>(bsm + ((max_nb * 4 + 15) / 16) * 16);
     const int64_t t = (int64_t)blockIdx.y * kBndChunk + threadIdx.x;
     double v[3] = {0.0, 0.0, 0.0};
     const bool in_range = t < Kloc && node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v);
-    const int lane = threadIdx.x & 31;
     for (int g = 0; g < kBndGroup; ++g) {
         const int64_t bi = (int64_t)blockIdx.x * kBndGroup + g;
         if (bi >= nb) break;                                // block-uniform
         const int b = bids[bi];
         const int64_t off = nb_off[b];
-        const int m = (int)(nb_off[b + 1] - off);
-        __syncthreads();                                    // previous particle's list fully consumed
-        if (threadIdx.x < 32) {                             // warp 0 compacts the nonzero weights, in order
-            int base = 0;
-            for (int e0 = 0; e0 < m; e0 += 32) {
-                const int e = e0 + lane;
-                const double c = e < m ? cw[off + e] : 0.0;
-                const bool keep = c != 0.0;
-                const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (keep) {
-                    const int slot = base + __popc(bal & ((1u << lane) - 1u));
-                    sj[slot] = nb_idx[off + e];
-                    sc[slot] = c;
-                }
-                base += __popc(bal);
-            }
-            if (lane == 0) s_cnt = base;
-        }
-        __syncthreads();
-        const int mi = s_cnt;
+        const int mi = bcnt[b];                             // interior neighbours (compacted by k_wls_boundary)
         const int wid = kind[b];
         const int axis = (wid - 1) / 2;
         const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
@@ -341,8 +317,8 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restr
         if (incoming) {
 #pragma unroll 8
             for (int e = 0; e < mi; ++e) {
-                const int64_t j = sj[e];
-                const double c = sc[e];
+                const int64_t j = __ldg(bidx + off + e);
+                const double c = __ldg(bcw + off + e);
                 if constexpr (NV == 1) {
                     acc[0] = fma(c, __ldg(f + j * Kloc + t), acc[0]);
                 } else {
@@ -379,19 +355,21 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_fill(const int32_t* __restric
                                                         double* __restrict__ f, int n1, int ncol, int ncs, int c0,
                                                         int64_t Kloc, double vmax, double dv) {
     constexpr int NV = (D == 2) ? 2 : 1;
+    // block per boundary particle, threads stride over the stored nodes of its row
     const int b = bids[blockIdx.x];
     const int wid = kind[b];
     const int axis = (wid - 1) / 2;
     const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
-    const int64_t t = (int64_t)blockIdx.y * kBndChunk + threadIdx.x;
-    if (t >= Kloc) return;
-    double v[3];
-    if (!node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) return;
-    if (!(sgn * v[axis] > 0.0)) return;
     const double rho_w = -wallnum[b] / den[wid - 1];
-    const double* M = Mw + ((int64_t)(wid - 1) * Kloc + t) * NV;
+    const double* Mrow = Mw + (int64_t)(wid - 1) * Kloc * NV;
+    double* frow = f + (int64_t)b * Kloc * NV;
+    for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
+        double v[3];
+        if (!node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) continue;
+        if (!(sgn * v[axis] > 0.0)) continue;
 #pragma unroll
-    for (int q = 0; q < NV; ++q) f[((int64_t)b * Kloc + t) * NV + q] = rho_w * M[q];
+        for (int q = 0; q < NV; ++q) frow[t * NV + q] = rho_w * Mrow[t * NV + q];
+    }
 }
 
 // moments of every row (diagnostics, bgk_moments): sums[p] = (s0, s_v, s_E[+g2])
@@ -516,22 +494,21 @@ void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
     dim3 g((unsigned)((c->N_b + kBndGroup - 1) / kBndGroup), (unsigned)c->bnd_nch);
-    const size_t smem = ((c->max_nb * 4 + 15) / 16) * 16 + (size_t)c->max_nb * 8;
     if (c->d == 3)
-        k_bnd_interp<3><<<g, kBndChunk, smem, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw,
-                                                   fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0, c->Ks,
-                                                   c->max_nb, c->cfg.vmax, c->dv);
+        k_bnd_interp<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.bidx, c->g.bcw,
+                                                c->g.bcnt, fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0,
+                                                c->Ks, c->cfg.vmax, c->dv);
     else
-        k_bnd_interp<2><<<g, kBndChunk, smem, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.nb_idx, c->g.cw,
-                                                   fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0, c->Ks,
-                                                   c->max_nb, c->cfg.vmax, c->dv);
+        k_bnd_interp<2><<<g, kBndChunk, 0, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.bidx, c->g.bcw,
+                                                c->g.bcnt, fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0,
+                                                c->Ks, c->cfg.vmax, c->dv);
     k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart, c->bnd_nch,
                                                                     c->wallnum);
 }
 
 void launch_boundary_fill(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
-    dim3 g((unsigned)c->N_b, (unsigned)c->bnd_nch);
+    const unsigned g = (unsigned)c->N_b;
     if (c->d == 3)
         k_bnd_fill<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->kind, c->wallnum, c->wall_den, c->Mw, fnew, c->n1,
                                               c->ncol, c->ncs, c->c0, c->Ks, c->cfg.vmax, c->dv);

@@ -219,7 +219,8 @@ template <int D>
 __global__ void k_wls_boundary(const double* __restrict__ x, const int8_t* __restrict__ kind,
                                const int32_t* __restrict__ ids, int64_t n_ids, const int64_t* __restrict__ nb_off,
                                const int32_t* __restrict__ nb_idx, double h, double h2, double alpha,
-                               double* __restrict__ cw, int64_t* err) {
+                               double* __restrict__ cw, int32_t* __restrict__ bidx, double* __restrict__ bcw,
+                               int32_t* __restrict__ bcnt, int64_t* err) {
     constexpr int n = D + 1;
     const int lane = threadIdx.x & 31;
     const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -262,10 +263,13 @@ __global__ void k_wls_boundary(const double* __restrict__ x, const int8_t* __res
         if (lane == 0) latch_error(err, BGK_E_DEFICIENT_STENCIL, b);
         return;
     }
-    for (int e = lane; e < m; e += 32) {
-        const int j = nb_idx[off + e];
+    int base = 0;   // compacted (interior neighbour, weight) list for the interpolation kernel
+    for (int e0 = 0; e0 < m; e0 += 32) {
+        const int e = e0 + lane;
+        const int j = e < m ? nb_idx[off + e] : 0;
         double c = 0.0;
-        if (kind[j] == 0) {
+        const bool inter = e < m && kind[j] == 0;
+        if (inter) {
             double xj[D], Pv[n];
             Pv[0] = 1.0;
 #pragma unroll
@@ -276,8 +280,16 @@ __global__ void k_wls_boundary(const double* __restrict__ x, const int8_t* __res
             for (int q = 0; q < n; ++q) s += Bi[0][q] * Pv[q];
             c = wgt * s;
         }
-        cw[off + e] = c;
+        if (e < m) cw[off + e] = c;
+        const unsigned bal = __ballot_sync(0xffffffffu, inter);
+        if (inter) {
+            const int slot = base + __popc(bal & ((1u << lane) - 1u));
+            bidx[off + slot] = j;
+            bcw[off + slot] = c;
+        }
+        base += __popc(bal);
     }
+    if (lane == 0) bcnt[b] = base;
 }
 
 }  // namespace
@@ -294,13 +306,13 @@ static void run_wls(bgk_ctx* c, double* rot, double* frames, cudaStream_t s) {
                                                          al, c->g.S, c->g.P, rot, frames, c->err);
         if (gb && !rot)
             k_wls_boundary<3><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
-                                                     h2, al, c->g.cw, c->err);
+                                                     h2, al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
     } else {
         if (gi) k_wls_interior<2><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2,
                                                          al, c->g.S, c->g.P, rot, frames, c->err);
         if (gb && !rot)
             k_wls_boundary<2><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
-                                                     h2, al, c->g.cw, c->err);
+                                                     h2, al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
     }
 }
 
