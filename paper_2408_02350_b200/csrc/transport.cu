@@ -126,6 +126,34 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         : "memory");
 }
 
+
+// Per (neighbour, lane) coefficients at the chunk's first node k1s:
+//   y_e = P_e . c0 (c0 = v(k1s, col) - W), dy_e = dv P_e[0] (increment per v_1 node),
+//   L = sum_e y_e, dL = sum_e dy_e.
+// In 3D the pair record already holds dy_e in slot 3e and dL in slot 9 (k_wls_interior), and
+// P_e[0] c1 = dy_e (c1 / dv) with c1dv = c0[0] / dv precomputed per lane.
+template <int D>
+__device__ __forceinline__ void pair_coeffs(const double* pv, const double (&c0v)[D], double c1dv, double dv,
+                                            double (&y)[D], double (&dy)[D], double& Lc, double& dL) {
+    if constexpr (D == 3) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            dy[k] = pv[k * 3];
+            y[k] = fma(pv[k * 3], c1dv, fma(pv[k * 3 + 1], c0v[1], pv[k * 3 + 2] * c0v[2]));
+        }
+        Lc = (y[0] + y[1]) + y[2];
+        dL = pv[9];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            y[k] = fma(pv[k * 2 + 1], c0v[1], pv[k * 2] * c0v[0]);
+            dy[k] = dv * pv[k * 2];
+        }
+        Lc = y[0] + y[1];
+        dL = dy[0] + dy[1];
+    }
+}
+
 // One ring stage: the neighbour's box of f (R rows x 32 columns x nv) and its pair data P_e.
 template <int D, int R>
 struct Stage {
@@ -217,24 +245,14 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
     }
     // per-neighbour coefficients at the chunk's first node: y_e = P_e . c0, dy_e = dv P_e[0],
     // L = sum_e y_e, dL = sum_e dy_e (read from the stage's pair-data slot)
+    const double c1dv = c0v[0] / A.dv;
     auto coeffs = [&](int e, double (&y)[D], double (&dy)[D], double& Lc, double& dL) {
         const double* ps =
             reinterpret_cast<const double*>(ring + ((g0 + (uint32_t)e) % NST) * St::BYTES + St::F_BYTES);
         double pv[PD];
 #pragma unroll
         for (int q = 0; q < PD; ++q) pv[q] = ps[q];       // broadcast LDS
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            double t = pv[k * D] * c0v[0];
-#pragma unroll
-            for (int a = 1; a < D; ++a) t = fma(pv[k * D + a], c0v[a], t);
-            y[k] = t;
-            dy[k] = A.dv * pv[k * D];
-        }
-        Lc = y[0];
-        dL = dy[0];
-#pragma unroll
-        for (int k = 1; k < D; ++k) { Lc += y[k]; dL += dy[k]; }
+        pair_coeffs<D>(pv, c0v, c1dv, A.dv, y, dy, Lc, dL);
     };
     // The readiness of the NEXT stage is tested (non-blocking mbarrier.test_wait) before this
     // neighbour's rows, so the barrier check's latency overlaps the row arithmetic; only if the
@@ -479,6 +497,7 @@ __global__ void __launch_bounds__(kGroup * 32, 1) k_transport_grp(const __grid_c
     } else {
         c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
     }
+    const double c1dv = c0v[0] / A.dv;
     double Qf[R][NV], Sc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -504,18 +523,8 @@ __global__ void __launch_bounds__(kGroup * 32, 1) k_transport_grp(const __grid_c
         double pv[PD];
 #pragma unroll
         for (int q = 0; q < PD; ++q) pv[q] = ps[q];
-        double y[D], dy[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            double t = pv[k * D] * c0v[0];
-#pragma unroll
-            for (int a = 1; a < D; ++a) t = fma(pv[k * D + a], c0v[a], t);
-            y[k] = t;
-            dy[k] = A.dv * pv[k * D];
-        }
-        double Lc = y[0], dL = dy[0];
-#pragma unroll
-        for (int k = 1; k < D; ++k) { Lc += y[k]; dL += dy[k]; }
+        double y[D], dy[D], Lc, dL;
+        pair_coeffs<D>(pv, c0v, c1dv, A.dv, y, dy, Lc, dL);
         // a warp may run many members ahead of a slow one: wait until stage s has been armed for
         // member u (parity waits alone cannot tell rounds two phases apart), then for the data
         while (smem_member[s] != u) __nanosleep(64);
@@ -813,6 +822,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_transport_ws(const __grid_con
     } else {
         c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
     }
+    const double c1dv = c0v[0] / A.dv;
     double Qf[R][NV], Sc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -828,18 +838,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_transport_ws(const __grid_con
         double pv[PD];
 #pragma unroll
         for (int q = 0; q < PD; ++q) pv[q] = ps[q];
-        double y[D], dy[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            double t = pv[k * D] * c0v[0];
-#pragma unroll
-            for (int a = 1; a < D; ++a) t = fma(pv[k * D + a], c0v[a], t);
-            y[k] = t;
-            dy[k] = A.dv * pv[k * D];
-        }
-        double Lc = y[0], dL = dy[0];
-#pragma unroll
-        for (int k = 1; k < D; ++k) { Lc += y[k]; dL += dy[k]; }
+        double y[D], dy[D], Lc, dL;
+        pair_coeffs<D>(pv, c0v, c1dv, A.dv, y, dy, Lc, dL);
         const double* st = reinterpret_cast<const double*>(stb) + lane * NV;
 #pragma unroll
         for (int r = 0; r < R; ++r) {

@@ -129,7 +129,7 @@ __device__ __forceinline__ void frame_of(const double (&d)[D], double (&F)[D][D]
 template <int D>
 __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __restrict__ ids, int64_t n_ids,
                                const int64_t* __restrict__ nb_off, const int32_t* __restrict__ nb_idx, double h,
-                               double h2, double alpha, double* __restrict__ S_out, double* __restrict__ P,
+                               double h2, double alpha, double dv, double* __restrict__ S_out, double* __restrict__ P,
                                double* __restrict__ rot_out, double* __restrict__ frame_out, int64_t* err) {
     constexpr int PD = (D == 2) ? 4 : 10;
     const int lane = threadIdx.x & 31;
@@ -203,7 +203,17 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
         for (int k = 0; k < D; ++k)
 #pragma unroll
             for (int a = 0; a < D; ++a) pe[k * D + a] = rot[k] * F[k][a];
-        if (PD > D * D) pe[PD - 1] = 0.0;
+        if constexpr (D == 3) {
+            // transport walks v_1 in steps of dv: store dy_e = dv * P_e[0] in place of P_e[0]
+            // and dL = sum_e dy_e in the pad slot (lane-independent, saves 5 DP per neighbour)
+            double dl = 0.0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                pe[k * D] = dv * pe[k * D];
+                dl += pe[k * D];
+            }
+            pe[PD - 1] = dl;
+        }
         if (rot_out) {
 #pragma unroll
             for (int k = 0; k < D; ++k) rot_out[(off + e) * D + k] = rot[k];
@@ -303,13 +313,13 @@ static void run_wls(bgk_ctx* c, double* rot, double* frames, cudaStream_t s) {
     const double h = c->cfg.h, h2 = c->cfg.h2, al = c->cfg.alpha_w;
     if (c->d == 3) {
         if (gi) k_wls_interior<3><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2,
-                                                         al, c->g.S, c->g.P, rot, frames, c->err);
+                                                         al, c->dv, c->g.S, c->g.P, rot, frames, c->err);
         if (gb && !rot)
             k_wls_boundary<3><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
                                                      h2, al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
     } else {
         if (gi) k_wls_interior<2><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2,
-                                                         al, c->g.S, c->g.P, rot, frames, c->err);
+                                                         al, c->dv, c->g.S, c->g.P, rot, frames, c->err);
         if (gb && !rot)
             k_wls_boundary<2><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
                                                      h2, al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
