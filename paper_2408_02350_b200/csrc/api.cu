@@ -90,7 +90,7 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
         if ((size_t)c->ucap * 8 > 48 * 1024 || c->ucap > 65535) c->grouped = false;   // sort buffers in smem
     }
     c->bnd_chunk = 256;
-    c->bnd_nch = (int)((c->Ks + 255) / 256);
+    c->bnd_nch = (int)((c->Ks + 511) / 512);   // k_bnd_interp: 256 threads x 2 nodes per block
 }
 
 size_t carve(bgk_ctx* c, char* base, bool dry) {

@@ -284,6 +284,7 @@ constexpr int kBndChunk = 256;
 // 256 stored nodes).  Neighbouring boundary particles share most interior neighbours, so the
 // rows loaded for one particle of the group are L1 hits for the next.
 constexpr int kBndGroup = 8;
+constexpr int kBndNPT = 2;   // nodes per thread in k_bnd_interp
 
 template <int D>
 __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restrict__ bids, int64_t nb,
@@ -294,12 +295,19 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restr
                                                           const int32_t* __restrict__ bcnt, double* __restrict__ f,
                                                           double* __restrict__ wallpart, int nch, int n1, int ncol,
                                                           int ncs, int c0, int64_t Kloc, double vmax, double dv) {
-    // Kloc here is the STORED node count per row (n1 * ncs)
+    // Kloc here is the STORED node count per row (n1 * ncs).  Each thread owns kBndNPT nodes of
+    // the block's chunk (independent load/FMA streams for memory-level parallelism).
     constexpr int NV = (D == 2) ? 2 : 1;
     __shared__ double sh[32];
-    const int64_t t = (int64_t)blockIdx.y * kBndChunk + threadIdx.x;
-    double v[3] = {0.0, 0.0, 0.0};
-    const bool in_range = t < Kloc && node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v);
+    int64_t t[kBndNPT];
+    double v[kBndNPT][3];
+    bool in_range[kBndNPT];
+#pragma unroll
+    for (int q = 0; q < kBndNPT; ++q) {
+        t[q] = (int64_t)blockIdx.y * kBndChunk * kBndNPT + q * kBndChunk + threadIdx.x;
+        v[q][0] = v[q][1] = v[q][2] = 0.0;
+        in_range[q] = t[q] < Kloc && node_vel_s<D>(t[q], ncs, ncol, c0, n1, vmax, dv, v[q]);
+    }
     for (int g = 0; g < kBndGroup; ++g) {
         const int64_t bi = (int64_t)blockIdx.x * kBndGroup + g;
         if (bi >= nb) break;                                // block-uniform
@@ -309,30 +317,39 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restr
         const int wid = kind[b];
         const int axis = (wid - 1) / 2;
         const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
-        const double vn = sgn * v[axis];
-        const bool incoming = in_range && vn <= 0.0;
-        double acc[NV];
+        double vn[kBndNPT];
+        bool incoming[kBndNPT];
+        double acc[kBndNPT][NV];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
-        if (incoming) {
-#pragma unroll 8
-            for (int e = 0; e < mi; ++e) {
-                const int64_t j = __ldg(bidx + off + e);
-                const double c = __ldg(bcw + off + e);
+        for (int q = 0; q < kBndNPT; ++q) {
+            vn[q] = sgn * v[q][axis];
+            incoming[q] = in_range[q] && vn[q] <= 0.0;
+#pragma unroll
+            for (int c = 0; c < NV; ++c) acc[q][c] = 0.0;
+        }
+#pragma unroll 4
+        for (int e = 0; e < mi; ++e) {
+            const int64_t j = __ldg(bidx + off + e);
+            const double c = __ldg(bcw + off + e);
+#pragma unroll
+            for (int q = 0; q < kBndNPT; ++q) {
+                if (!incoming[q]) continue;
                 if constexpr (NV == 1) {
-                    acc[0] = fma(c, __ldg(f + j * Kloc + t), acc[0]);
+                    acc[q][0] = fma(c, __ldg(f + j * Kloc + t[q]), acc[q][0]);
                 } else {
-                    const double2 gv = __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t);
-                    acc[0] = fma(c, gv.x, acc[0]);
-                    acc[1] = fma(c, gv.y, acc[1]);
+                    const double2 gv = __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t[q]);
+                    acc[q][0] = fma(c, gv.x, acc[q][0]);
+                    acc[q][1] = fma(c, gv.y, acc[q][1]);
                 }
             }
         }
         double flux = 0.0;
-        if (incoming) {
-            if constexpr (NV == 1) f[(int64_t)b * Kloc + t] = acc[0];
-            else reinterpret_cast<double2*>(f)[(int64_t)b * Kloc + t] = make_double2(acc[0], acc[1]);
-            if (vn < 0.0) flux = vn * acc[0];
+#pragma unroll
+        for (int q = 0; q < kBndNPT; ++q) {
+            if (!incoming[q]) continue;
+            if constexpr (NV == 1) f[(int64_t)b * Kloc + t[q]] = acc[q][0];
+            else reinterpret_cast<double2*>(f)[(int64_t)b * Kloc + t[q]] = make_double2(acc[q][0], acc[q][1]);
+            if (vn[q] < 0.0) flux += vn[q] * acc[q][0];
         }
         const double tot = block_sum<kBndChunk>(flux, sh);
         if (threadIdx.x == 0) wallpart[bi * nch + blockIdx.y] = tot;
