@@ -267,12 +267,24 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
         const bool more = e + 1 < m;
         const uint32_t nready = more ? mbar_test(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u) : 1u;
         const double* st = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) + lane * NV;
+#ifdef BGK_EXP_INCR
+        double yi[D], Li = Lc;                             // experiment: y += dy increments along the row
+#pragma unroll
+        for (int k = 0; k < D; ++k) yi[k] = y[k];
+#endif
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            double C;
+#ifdef BGK_EXP_INCR
+            if constexpr (D == 3) C = Li - fabs(yi[0]) - fabs(yi[1]) - fabs(yi[2]);
+            else C = Li - fabs(yi[0]) - fabs(yi[1]);
+#pragma unroll
+            for (int k = 0; k < D; ++k) yi[k] += dy[k];
+            Li += dL;
+#else
             // y_e(r) = y_e(0) + r dy_e: one FMA each with r an immediate -> rows are independent
             const double rr = (double)r;
             const double Lr = fma(rr, dL, Lc);
-            double C;
             if constexpr (D == 3) {
                 const double yn = fma(rr, dy[0], y[0]);
                 const double yt = fma(rr, dy[1], y[1]);
@@ -283,6 +295,7 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
                 const double yt = fma(rr, dy[1], y[1]);
                 C = (Lr - fabs(yn)) - fabs(yt);
             }
+#endif
             if constexpr (NV == 1) {
                 Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
             } else {

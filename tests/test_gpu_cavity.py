@@ -1,0 +1,91 @@
+"""Driven cavity to steady state on the GPU (Fig. 2).
+
+Qualitative, parity-unpinned physics checks on the 2D Chu-reduced cavity (101² particles,
+33² velocities, ALE): run from the paper's equilibrium start with the lid at 1 m/s until the
+velocity field is steady (relative L² change over 200 steps < 1e-3), then
+  * exactly one vortex: the velocity angle winds by ±2π along a square loop around the
+    cavity centre (acceptance 7);
+  * the gas under the lid moves with the lid (mean u of the top interior row > 0);
+  * zero net mass flux through every wall particle (diffuse reflection);
+  * total mass drift below 5 % (tripwire).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import bgk_inputs as bi
+
+pytestmark = pytest.mark.gpu
+
+
+def winding_number(x, U, L, frac=0.3, n=64):
+    """Net rotation (in turns) of the velocity direction along a square loop of half-width
+    frac*L around the cavity centre, sampled at the nearest particles."""
+    c = 0.5 * L
+    pts = []
+    for s in np.linspace(0, 4, n, endpoint=False):
+        side, t = int(s), s - int(s)
+        a = frac * L
+        if side == 0:
+            p = (c - a + 2 * a * t, c - a)
+        elif side == 1:
+            p = (c + a, c - a + 2 * a * t)
+        elif side == 2:
+            p = (c + a - 2 * a * t, c + a)
+        else:
+            p = (c - a, c + a - 2 * a * t)
+        pts.append(p)
+    ang = []
+    for p in pts:
+        k = int(np.argmin(((x - np.array(p)) ** 2).sum(1)))
+        ang.append(math.atan2(U[k, 1], U[k, 0]))
+    ang = np.unwrap(np.array(ang + [ang[0]]))
+    return (ang[-1] - ang[0]) / (2 * math.pi)
+
+
+@pytest.mark.parametrize("Kn", [1.0, 10.0])
+def test_cavity_single_vortex_steady_state(Kn):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2408_02350_b200 import Bgk
+    cfg = bi.C2.replace(Kn=Kn, init="equilibrium")
+    cloud = bi.make_cloud(cfg)
+    g = Bgk(cfg, cloud, device="cuda:0")
+    inter = cloud["kind"] == 0
+    rho0, _, _ = g.moments()
+    mass0 = rho0[inter].sum()
+    prev = None
+    steady = False
+    for it in range(60):                       # up to 12 000 steps
+        g.step(200)
+        g.sync()
+        U = g.macro()[:, 1:3]
+        if prev is not None:
+            num = np.linalg.norm(U[inter] - prev[inter])
+            den = np.linalg.norm(U[inter])
+            if den > 0 and num / den < 1e-3:
+                steady = True
+                break
+        prev = U.copy()
+    assert steady, "no steady state within 12 000 steps"
+    x = g.positions()
+    U = g.macro()[:, 1:3]
+    w = winding_number(x, U, cfg.L)
+    assert abs(abs(w) - 1.0) < 1e-6, w
+    ii = np.rint(cloud["x"] / cfg.dx).astype(int)
+    top = inter & (ii[:, 1] == cfg.n_per_axis - 2)
+    assert U[top, 0].mean() > 0
+    rho, _, _ = g.moments()
+    assert abs(rho[inter].sum() / mass0 - 1) < 0.05
+    # zero net wall flux at every boundary particle
+    f = g.get_f()[:, 0, :]
+    n1 = cfg.Nv + 1
+    ax = np.array([-cfg.vmax + j * (2 * cfg.vmax / cfg.Nv) for j in range(n1)])
+    V = np.stack(np.meshgrid(ax, ax, indexing="ij"), -1).reshape(-1, 2)
+    for b in np.nonzero(~inter)[0][::7]:
+        wid = cloud["kind"][b]
+        a, sgn = (wid - 1) // 2, (1.0 if (wid - 1) % 2 == 0 else -1.0)
+        vn = sgn * V[:, a]
+        assert abs((vn * f[b]).sum()) <= 1e-12 * (np.abs(vn) * f[b]).sum()
