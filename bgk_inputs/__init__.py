@@ -65,6 +65,7 @@ class CavityConfig:
     init: str = "stress"      # "stress" | "equilibrium"
     vmax: float = VMAX_DEFAULT
     lid: float = 1.0          # lid speed; 0 gives an all-stationary box
+    wls_order: int = 1        # Taylor order of the WLS derivative (1: the paper's scheme; 2: P:368-369)
     L: float = L_CAVITY
 
     @property

@@ -44,7 +44,7 @@ class OrCfg(C.Structure):
     _fields_ = [("dims", C.c_int32), ("Nv", C.c_int32), ("vmax", C.c_double), ("L", C.c_double),
                 ("h", C.c_double), ("h2", C.c_double), ("alpha_w", C.c_double), ("dt", C.c_double),
                 ("R", C.c_double), ("kb", C.c_double), ("dmol", C.c_double), ("Twall", C.c_double),
-                ("Ulid", C.c_double * 3), ("dx", C.c_double), ("ale", C.c_int32), ("pad", C.c_int32)]
+                ("Ulid", C.c_double * 3), ("dx", C.c_double), ("ale", C.c_int32), ("wls_order", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -70,7 +70,8 @@ def lib():
                 "or_wls_one": (C.c_int, [C.c_int, _P, _I64, C.c_int, _P, _D, _D, _P, _P]),
                 "or_frame": (None, [C.c_int, _P, _P]),
                 "or_rotate": (None, [C.c_int, _P, _P, _P]),
-                "or_wls_all": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P]),
+                "or_wls_all": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _D, _D, C.c_int, _P, _P, _P, _P, _P]),
+                "or_wls_one_order": (C.c_int, [C.c_int, _P, _I64, C.c_int, _P, _D, _D, C.c_int, _P, _P]),
                 "or_transport_one": (None, [_P, _P, C.c_int, _P, _P, _P, _P, _P, _I64, _I64]),
                 "or_coef_absmax_one": (_D, [_P, _P, C.c_int, _P, _P]),
                 "or_moments_row": (C.c_int, [_P, _P, _P]),
@@ -117,6 +118,7 @@ def make_cfg(cfg, dt=None) -> OrCfg:
     for a in range(3):
         c.Ulid[a] = cfg.U_lid[a]
     c.dx, c.ale = cfg.dx, cfg.ale
+    c.wls_order = getattr(cfg, "wls_order", 1)
     return c
 
 
@@ -179,14 +181,14 @@ def sym_eigenvalues(A: np.ndarray) -> np.ndarray:
     return lam
 
 
-def wls_one(x, i, nb, h2, alpha=6.0):
+def wls_one(x, i, nb, h2, alpha=6.0, order=1):
     """(S[d,d], a[m,d]) for particle i, or raises OracleError(OR_E_DEFICIENT)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     d = x.shape[1]
     nb = np.ascontiguousarray(nb, dtype=np.int32)
     S = np.zeros((d, d))
     a = np.zeros((max(len(nb), 1), d))
-    st = lib().or_wls_one(d, _p(x), i, len(nb), _p(nb), h2, alpha, _p(S), _p(a))
+    st = lib().or_wls_one_order(d, _p(x), i, len(nb), _p(nb), h2, alpha, order, _p(S), _p(a))
     if st != OR_OK:
         raise OracleError(st, i)
     return S, a[: len(nb)]
@@ -209,7 +211,7 @@ def rotate(a, fr) -> np.ndarray:
     return out
 
 
-def wls_all(x, kind, off, idx, h2, alpha=6.0):
+def wls_all(x, kind, off, idx, h2, alpha=6.0, order=1):
     """S[N,d,d], a[nnz,d], frames[nnz,d,d], rot[nnz,d] for interior particles."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     kind = np.ascontiguousarray(kind, dtype=np.int8)
@@ -220,7 +222,7 @@ def wls_all(x, kind, off, idx, h2, alpha=6.0):
     fr = np.zeros((max(nnz, 1), d, d))
     rot = np.zeros((max(nnz, 1), d))
     bad = C.c_int64(-1)
-    st = lib().or_wls_all(d, _p(x), N, _p(kind), _p(off), _p(np.ascontiguousarray(idx)), h2, alpha,
+    st = lib().or_wls_all(d, _p(x), N, _p(kind), _p(off), _p(np.ascontiguousarray(idx)), h2, alpha, order,
                           _p(S), _p(a), _p(fr), _p(rot), C.byref(bad))
     if st != OR_OK:
         raise OracleError(st, bad.value)
@@ -413,7 +415,7 @@ def sampled_first_step(cfg, cloud, sample, k_range=None):
 
     def interior_f1(i):
         nb = neighbors_of(x, c.h2, i)
-        S, a = wls_one(x, i, nb, c.h2, c.alpha_w)
+        S, a = wls_one(x, i, nb, c.h2, c.alpha_w, c.wls_order)
         frs = np.stack([frame(x[j] - x[i]) for j in nb])
         rot = np.stack([rotate(a[q], frs[q]) for q in range(len(nb))])
         W = cloud["U"][i] if c.ale else np.zeros(d)

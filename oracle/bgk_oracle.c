@@ -55,7 +55,7 @@ typedef struct {
     double Ulid[3];   /* lid velocity */
     double dx;        /* nominal spacing, for the ALE clamp */
     int32_t ale;      /* 1: ALE (W = U^n, particles move), 0: fixed cloud (W = 0, Z21) */
-    int32_t pad;
+    int32_t wls_order;/* 1 (or 0): first-order Taylor WLS; 2: second order */
 } or_cfg;
 
 /* ------------------------------------------------------------------ O1 --- */
@@ -129,10 +129,10 @@ int or_neighbors(int d, const double* x, int64_t N, double h2, int64_t* offsets,
 }
 
 /* ------------------------------------------------------------ linear algebra */
-/* Gauss-Jordan inverse with partial pivoting of an n x n matrix (n <= 4).
+/* Gauss-Jordan inverse with partial pivoting of an n x n matrix (n <= 9).
  * Returns 0 on success, 1 if a pivot is exactly zero. */
 static int inverse(int n, const double* A, double* Ainv) {
-    double M[4][8];
+    double M[9][18];
     for (int r = 0; r < n; ++r)
         for (int c = 0; c < 2 * n; ++c)
             M[r][c] = c < n ? A[r * n + c] : (c - n == r ? 1.0 : 0.0);
@@ -160,7 +160,7 @@ static int inverse(int n, const double* A, double* Ainv) {
 
 /* Eigenvalues of a symmetric n x n matrix by cyclic Jacobi rotations. */
 void or_sym_eigenvalues(int n, const double* A, double* lam) {
-    double a[4][4];
+    double a[9][9];
     for (int r = 0; r < n; ++r)
         for (int c = 0; c < n; ++c) a[r][c] = A[r * n + c];
     for (int sweep = 0; sweep < 100; ++sweep) {
@@ -195,7 +195,7 @@ void or_sym_eigenvalues(int n, const double* A, double* lam) {
 /* Deficiency test of S:253/S:303: m < d+2, or lambda_min < 1e-12 lambda_max. */
 static int deficient(int n_unknown_dim, int m, int n, const double* A) {
     if (m < n_unknown_dim + 2) return 1;
-    double lam[4];
+    double lam[9];
     or_sym_eigenvalues(n, A, lam);
     double lo = lam[0], hi = lam[0];
     for (int r = 1; r < n; ++r) {
@@ -217,6 +217,59 @@ double or_weight(double r2, double h2, double alpha) {
  * M rows d_j = x_j - x_i, W = diag(w_j); S = (M^T W M)^{-1};
  * (alpha_ij, beta_ij, gamma_ij) = w_j S d_j.
  * Outputs: S[d*d], a[m*d]. Returns OR_OK or OR_E_DEFICIENT. */
+/* Second-order Taylor WLS ("higher-order approximations are obtained by using
+ * higher-order Taylor's expansion in (taylor)"): per neighbour
+ *   f_j - f_i = g . d_j + 1/2 d_j^T H d_j + e_j,
+ * unknowns (g, H_11, H_22[, H_33], H_12[, H_13, H_23]) -- nu = 5 (2D) / 9 (3D) -- solved by
+ * weighted least squares with the same Gaussian weights.  Offsets are written in units of h
+ * (dimensionless, O(1) matrix; the rank test is then meaningful) and the gradient rows are
+ * scaled back: a_j = w_j (S^ m^_j)[0:d] / h.  S (output) = leading d x d block / h^2.
+ * Deficient when m < nu + 1 or lambda_min < 1e-12 lambda_max. */
+static int wls_one_order2(int d, const double* x, int64_t i, int m, const int32_t* nb, double h2,
+                          double alpha_w, double* S, double* a) {
+    const int nu = d == 2 ? 5 : 9;
+    const double h = sqrt(h2);
+    double A[81] = {0}, Ai[81];
+    for (int jj = 0; jj < m; ++jj) {
+        const double* xj = x + (int64_t)nb[jj] * d;
+        double q[3], mv[9];
+        for (int r = 0; r < d; ++r) q[r] = (xj[r] - x[i * d + r]) / h;
+        int k = 0;
+        for (int r = 0; r < d; ++r) mv[k++] = q[r];
+        for (int r = 0; r < d; ++r) mv[k++] = 0.5 * q[r] * q[r];
+        for (int r = 0; r < d; ++r)
+            for (int c = r + 1; c < d; ++c) mv[k++] = q[r] * q[c];
+        double w = or_weight(dist2(d, x + i * d, xj), h2, alpha_w);
+        for (int r = 0; r < nu; ++r)
+            for (int c = 0; c < nu; ++c) A[r * nu + c] = A[r * nu + c] + w * mv[r] * mv[c];
+    }
+    if (m < nu + 1) return OR_E_DEFICIENT;
+    if (deficient(0, 2, nu, A)) return OR_E_DEFICIENT;
+    if (inverse(nu, A, Ai)) return OR_E_DEFICIENT;
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) S[r * d + c] = Ai[r * nu + c] / h2;
+    for (int jj = 0; jj < m; ++jj) {
+        const double* xj = x + (int64_t)nb[jj] * d;
+        double q[3], mv[9];
+        for (int r = 0; r < d; ++r) q[r] = (xj[r] - x[i * d + r]) / h;
+        int k = 0;
+        for (int r = 0; r < d; ++r) mv[k++] = q[r];
+        for (int r = 0; r < d; ++r) mv[k++] = 0.5 * q[r] * q[r];
+        for (int r = 0; r < d; ++r)
+            for (int c = r + 1; c < d; ++c) mv[k++] = q[r] * q[c];
+        double w = or_weight(dist2(d, x + i * d, xj), h2, alpha_w);
+        for (int r = 0; r < d; ++r) {
+            double s = 0.0;
+            for (int c = 0; c < nu; ++c) s = s + Ai[r * nu + c] * mv[c];
+            a[jj * d + r] = w * s / h;
+        }
+    }
+    return OR_OK;
+}
+
+int or_wls_one_order(int d, const double* x, int64_t i, int m, const int32_t* nb, double h2,
+                     double alpha_w, int order, double* S, double* a);
+
 int or_wls_one(int d, const double* x, int64_t i, int m, const int32_t* nb,
                double h2, double alpha_w, double* S, double* a) {
     double A[9] = {0};
@@ -242,6 +295,13 @@ int or_wls_one(int d, const double* x, int64_t i, int m, const int32_t* nb,
         }
     }
     return OR_OK;
+}
+
+/* WLS of the requested Taylor order (1 or 0: first order; 2: second order). */
+int or_wls_one_order(int d, const double* x, int64_t i, int m, const int32_t* nb, double h2,
+                     double alpha_w, int order, double* S, double* a) {
+    if (order == 2) return wls_one_order2(d, x, i, m, nb, h2, alpha_w, S, a);
+    return or_wls_one(d, x, i, m, nb, h2, alpha_w, S, a);
 }
 
 /* ------------------------------------------------------------------ O4 --- */
@@ -284,13 +344,13 @@ void or_rotate(int d, const double* a, const double* frame, double* rot) {
  * S[N*d*d] (interior rows), a/rot[nnz*d], frames[nnz*d*d] (interior rows).
  * Returns OR_OK or OR_E_DEFICIENT with *bad = first offending particle. */
 int or_wls_all(int d, const double* x, int64_t N, const int8_t* kind, const int64_t* off,
-               const int32_t* idx, double h2, double alpha_w, double* S, double* a,
+               const int32_t* idx, double h2, double alpha_w, int order, double* S, double* a,
                double* frames, double* rot, int64_t* bad) {
     int64_t first_bad = -1;
     for (int64_t i = 0; i < N; ++i) {
         if (kind[i] != 0) continue;
         int m = (int)(off[i + 1] - off[i]);
-        int st = or_wls_one(d, x, i, m, idx + off[i], h2, alpha_w, S + i * d * d, a + off[i] * d);
+        int st = or_wls_one_order(d, x, i, m, idx + off[i], h2, alpha_w, order, S + i * d * d, a + off[i] * d);
         if (st != OR_OK) {
             if (first_bad < 0) first_bad = i;
             continue;
@@ -592,7 +652,7 @@ int or_step(const or_cfg* c, int64_t N, double* x, const int8_t* kind, double* f
     double* fr = (double*)calloc((size_t)(need * d * d + 1), sizeof(double));
     double* rot = (double*)calloc((size_t)(need * d + 1), sizeof(double));
     double* cw = (double*)calloc((size_t)(need + 1), sizeof(double));
-    int st = or_wls_all(d, x, N, kind, off, idx, c->h2, c->alpha_w, S, a, fr, rot, bad);
+    int st = or_wls_all(d, x, N, kind, off, idx, c->h2, c->alpha_w, c->wls_order, S, a, fr, rot, bad);
     if (st == OR_OK)
         for (int64_t b = 0; b < N; ++b) {
             if (kind[b] == 0) continue;

@@ -245,3 +245,54 @@ def test_boundary_weights_reproduce_linear(oracle_lib, dims, n):
         assert abs(c @ f[nb] - f[b]) < 1e-12 * abs(f).max()
     # corner weights can be negative (SURVEY §7 hard parts)
     assert cw.min() < 0
+
+
+# ------------------------------------------------ second-order WLS (NEXT(3))
+@pytest.mark.parametrize("k", range(4))
+def test_wls_order2_reproduces_quadratics_on_any_stencil(oracle_lib, k):
+    """Second-order Taylor WLS: the gradient of any quadratic is exact on every non-deficient
+    stencil -- walls, jittered clouds included -- not only on symmetric ones."""
+    cfg, x, kind = _clouds()[k]
+    d = cfg.dims
+    off, idx = oracle_lib.neighbors(x, cfg.h2)
+    S, a, fr, rot = oracle_lib.wls_all(x, kind, off, idx, cfg.h2, order=2)
+    rng = np.random.default_rng(10 + k)
+    xs = x / cfg.dx
+    g = rng.normal(size=d)
+    H = rng.normal(size=(d, d))
+    H = H + H.T
+    f = 0.5 + xs @ g + 0.5 * np.einsum("ni,ij,nj->n", xs, H, xs)
+    worst = 0.0
+    for i in np.nonzero(kind == 0)[0]:
+        nb = idx[off[i]:off[i + 1]]
+        grad = (a[off[i]:off[i + 1]] * (f[nb] - f[i])[:, None]).sum(0) * cfg.dx
+        exact = g + H @ xs[i]
+        worst = max(worst, np.abs(grad - exact).max() / np.abs(exact).max())
+    assert worst < 1e-11
+    # first order is NOT quadratic-exact on the same clouds' wall stencils (sanity of the pin)
+    if k in (0, 2):
+        S1, a1, _, _ = oracle_lib.wls_all(x, kind, off, idx, cfg.h2, order=1)
+        errs = []
+        for i in np.nonzero(kind == 0)[0]:
+            nb = idx[off[i]:off[i + 1]]
+            grad = (a1[off[i]:off[i + 1]] * (f[nb] - f[i])[:, None]).sum(0) * cfg.dx
+            exact = g + H @ xs[i]
+            errs.append(np.abs(grad - exact).max() / np.abs(exact).max())
+        assert max(errs) > 1e-3
+
+
+def test_wls_order2_linear_exact_and_deficiency(oracle_lib):
+    cfg, x, kind = _clouds()[3]
+    off, idx = oracle_lib.neighbors(x, cfg.h2)
+    S, a, fr, rot = oracle_lib.wls_all(x, kind, off, idx, cfg.h2, order=2)
+    g = np.array([1.0, -2.0, 0.5]) / cfg.dx
+    f = 3.0 + x @ g
+    for i in np.nonzero(kind == 0)[0][::5]:
+        nb = idx[off[i]:off[i + 1]]
+        grad = (a[off[i]:off[i + 1]] * (f[nb] - f[i])[:, None]).sum(0)
+        np.testing.assert_allclose(grad, g, rtol=1e-11)
+    # a 6-neighbour cross stencil cannot determine 9 second-order unknowns
+    hx = 0.1
+    pts = [np.zeros(3)] + [s * hx * np.eye(3)[a] for a in range(3) for s in (1, -1)]
+    with pytest.raises(oracle_lib.OracleError):
+        oracle_lib.wls_one(np.array(pts), 0, np.arange(1, 7, dtype=np.int32), (1.01 * hx) ** 2, order=2)
