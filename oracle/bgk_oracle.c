@@ -307,7 +307,8 @@ int or_wls_one_order(int d, const double* x, int64_t i, int m, const int32_t* nb
 /* ------------------------------------------------------------------ O4 --- */
 /* Frame of the pair (i, j).
  * 2D: phi = atan2(dy, dx), n = (cos phi, sin phi), t = (-sin phi, cos phi).
- * 3D: phi = atan2(dy, dx) (atan2(+0,+0) = 0, Z10),
+ * 3D: phi = atan2(dy, dx) (atan2(+0,+0) = 0, Z10; phi = 0 also when the pair is
+ *   vertical to rounding, dx^2 + dy^2 <= 1e-16 r^2, Z26),
  *   theta = arccos(dz / r) (argument clamped to [-1, 1]),
  *   rows of A: n = (sin th cos ph, sin th sin ph, cos th),
  *              t = (cos th cos ph, cos th sin ph, -sin th),
@@ -315,6 +316,10 @@ int or_wls_one_order(int d, const double* x, int64_t i, int m, const int32_t* nb
  * frame[0..d-1] = n, [d..2d-1] = t, [2d..3d-1] = b (3D). */
 void or_frame(int d, const double* dj, double* frame) {
     double phi = atan2(dj[1], dj[0]);
+    if (d == 3) {
+        double rxy2 = dj[0] * dj[0] + dj[1] * dj[1];
+        if (rxy2 <= 1e-16 * (rxy2 + dj[2] * dj[2])) phi = 0.0;   /* Z26 */
+    }
     if (d == 2) {
         frame[0] = cos(phi); frame[1] = sin(phi);
         frame[2] = -sin(phi); frame[3] = cos(phi);

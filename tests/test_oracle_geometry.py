@@ -212,6 +212,15 @@ def test_frames_orthonormal_right_handed(oracle_lib):
     np.testing.assert_allclose(F[2], [0, 1, 0], atol=0)
     np.testing.assert_allclose(F[1], [1, 0, 0], atol=1e-16)
     np.testing.assert_allclose(F[0], [0, 0, 1], atol=1e-16)
+    # Z26: vertical to rounding (|dxy| <= 1e-8 r) is treated as vertical, whatever the sign of the
+    # tiny offset; just above the threshold the true azimuth is used
+    for e in ((1e-9, 0.0), (-1e-9, 3e-10), (0.0, -5e-9)):
+        F = oracle_lib.frame([e[0], e[1], 1.0])
+        np.testing.assert_allclose(F[2], [0, 1, 0], atol=0)
+        assert F[0][1] == 0.0 and abs(F[0][2] - 1.0) < 1e-15
+        assert 0.0 <= F[0][0] <= 1e-8   # sin(theta) >= 0 at phi = 0 (acos rounds it to 0 here)
+    F = oracle_lib.frame([-2e-8, 0.0, 1.0])
+    np.testing.assert_allclose(F[2], [0, -1, 0], atol=1e-15)
 
 
 @pytest.mark.parametrize("k", range(4))
