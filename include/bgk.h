@@ -83,6 +83,11 @@ typedef struct bgk_config {
     int32_t col_begin;   /* first velocity column owned by this rank */
     int32_t col_end;     /* one past the last owned column; col_begin = col_end = 0 means all */
     int32_t max_neighbors; /* per-particle neighbour capacity (0: 96 in 2D, 256 in 3D) */
+    int32_t wls_order;   /* Taylor order of the WLS derivative: 0 or 1 = first order (the paper's
+                            scheme); 2 = second order, Hessian terms added to the
+                            least-squares fit: nu = 5 (2D) / 9 (3D) unknowns, deficient
+                            below nu+1 neighbours.  abar may then be negative; the transport applies
+                            the flux formula literally, abar (c.n - |c.n|). */
 } bgk_config;
 
 /* Bytes of device workspace bgk_init_cloud needs for N particles. */

@@ -25,7 +25,8 @@ class BgkConfig(C.Structure):
                 ("h", C.c_double), ("h2", C.c_double), ("alpha_w", C.c_double), ("dt", C.c_double),
                 ("R", C.c_double), ("kb", C.c_double), ("dmol", C.c_double), ("T_wall", C.c_double),
                 ("U_lid", C.c_double * 3), ("dx", C.c_double), ("ale", C.c_int32),
-                ("col_begin", C.c_int32), ("col_end", C.c_int32), ("max_neighbors", C.c_int32)]
+                ("col_begin", C.c_int32), ("col_end", C.c_int32), ("max_neighbors", C.c_int32),
+                ("wls_order", C.c_int32)]
 
 
 _P = C.c_void_p

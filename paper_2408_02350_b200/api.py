@@ -36,6 +36,7 @@ def make_config(cfg, col_range: Optional[Tuple[int, int]] = None, max_neighbors:
     else:
         c.col_begin, c.col_end = col_range
     c.max_neighbors = max_neighbors
+    c.wls_order = getattr(cfg, "wls_order", 1)
     return c
 
 

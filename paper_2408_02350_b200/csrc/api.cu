@@ -37,6 +37,7 @@ bool valid_cfg(const bgk_config* c, int64_t N) {
     if (!(c->vmax > 0.0) || !(c->L > 0.0) || !(c->h > 0.0) || !(c->h2 > 0.0) || !(c->dt >= 0.0)) return false;
     if (!(c->R > 0.0) || !(c->kb > 0.0) || !(c->dmol > 0.0) || !(c->T_wall > 0.0) || !(c->alpha_w > 0.0)) return false;
     if (N > (int64_t)INT32_MAX) return false;
+    if (c->wls_order < 0 || c->wls_order > 2) return false;
     return true;
 }
 
@@ -75,7 +76,8 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     }
     c->dv = 2.0 * cfg->vmax / cfg->Nv;
     c->vmin = -cfg->vmax;
-    c->PD = c->d == 2 ? 4 : 10;
+    c->wls_order = cfg->wls_order == 2 ? 2 : 1;
+    c->PD = (c->d == 2 ? 4 : 10) + (c->wls_order == 2 ? 2 : 0);
     c->R = transport_rows_per_thread(c->d, c->n1);
     c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
     c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour

@@ -52,6 +52,7 @@ struct bgk_ctx {
     double edge[3];
     double dv, vmin;
     int PD;                     // doubles of pair data per CSR entry
+    int wls_order;              // 1 or 2 (second order adds the signed tail to the pair record)
     int R, nchunk, nslots, nwpp; // transport mapping
     int bnd_chunk, bnd_nch;     // boundary node chunking
     bool geometry_valid;

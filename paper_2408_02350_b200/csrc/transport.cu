@@ -51,6 +51,7 @@ struct TArgs {
     const uint8_t* __restrict__ gCnt;  //                 users of each union member
     const uint16_t* __restrict__ upos; //                 union position of each CSR entry
     int ucap;                          //                 capacity per group
+    bool signed_n;                     // second-order WLS: pair record carries s_n = -sign(abar)
     int64_t n_int;
     int n1, ncol, ncs, c0, ncg, nwpp;
     double vmax, dv, dt;
@@ -155,19 +156,22 @@ __device__ __forceinline__ void pair_coeffs(const double* pv, const double (&c0v
 }
 
 // One ring stage: the neighbour's box of f (R rows x 32 columns x nv) and its pair data P_e.
-template <int D, int R>
+// SG (second-order WLS): the pair record carries s_n = -sign(abar) after the first-order fields,
+// and C's n-term is y_n + s_n |y_n| (abar may be negative; P:408-410 applied literally).
+template <int D, int R, bool SG = false>
 struct Stage {
     static constexpr int NV = (D == 2) ? 2 : 1;
-    static constexpr int PD = (D == 2) ? 4 : 10;
+    static constexpr int PD0 = (D == 2) ? 4 : 10;
+    static constexpr int PD = SG ? PD0 + 2 : PD0;
     static constexpr int ROW = 32 * NV;                                  // doubles per staged row
     static constexpr uint32_t F_BYTES = R * ROW * sizeof(double);
     static constexpr uint32_t P_BYTES = PD * sizeof(double);
     static constexpr uint32_t BYTES = (F_BYTES + P_BYTES + 127) / 128 * 128;
 };
 
-template <int D, int R, int NST, int WPB>
+template <int D, int R, int NST, int WPB, bool SG>
 __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
-    using St = Stage<D, R>;
+    using St = Stage<D, R, SG>;
     constexpr int NV = St::NV;
     constexpr int PD = St::PD;
     constexpr int ROW = St::ROW;
@@ -236,66 +240,58 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
     } else {
         c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
     }
-    double Qf[R][NV], Sc[R];
+    double Qf[R][NV], Sc[R], Sa[SG ? R : 1];   // Sa: sum_j |C| (= -Sc when every C <= 0)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         Sc[r] = 0.0;
+        if constexpr (SG) Sa[r] = 0.0;
 #pragma unroll
         for (int q = 0; q < NV; ++q) Qf[r][q] = 0.0;
     }
     // per-neighbour coefficients at the chunk's first node: y_e = P_e . c0, dy_e = dv P_e[0],
     // L = sum_e y_e, dL = sum_e dy_e (read from the stage's pair-data slot)
     const double c1dv = c0v[0] / A.dv;
-    auto coeffs = [&](int e, double (&y)[D], double (&dy)[D], double& Lc, double& dL) {
+    auto coeffs = [&](int e, double (&y)[D], double (&dy)[D], double& Lc, double& dL, double& sn) {
         const double* ps =
             reinterpret_cast<const double*>(ring + ((g0 + (uint32_t)e) % NST) * St::BYTES + St::F_BYTES);
         double pv[PD];
 #pragma unroll
         for (int q = 0; q < PD; ++q) pv[q] = ps[q];       // broadcast LDS
         pair_coeffs<D>(pv, c0v, c1dv, A.dv, y, dy, Lc, dL);
+        if constexpr (SG) sn = pv[St::PD0];
     };
     // The readiness of the NEXT stage is tested (non-blocking mbarrier.test_wait) before this
     // neighbour's rows, so the barrier check's latency overlaps the row arithmetic; only if the
     // next box has not landed by the end of the rows does the warp spin on try_wait.
-    double y[D], dy[D], Lc = 0.0, dL = 0.0;
+    double y[D], dy[D], Lc = 0.0, dL = 0.0, sn = -1.0;
     if (m > 0) {
         mbar_wait(bars + g0 % NST, (g0 / NST) & 1u);
-        coeffs(0, y, dy, Lc, dL);
+        coeffs(0, y, dy, Lc, dL, sn);
     }
     for (int e = 0; e < m; ++e) {
         const uint32_t ge = g0 + (uint32_t)e;
         const bool more = e + 1 < m;
         const uint32_t nready = more ? mbar_test(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u) : 1u;
         const double* st = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) + lane * NV;
-#ifdef BGK_EXP_INCR
-        double yi[D], Li = Lc;                             // experiment: y += dy increments along the row
+        // y_e and L advance by one add per node along v_1 (all DADD: measured ~2 % faster than
+        // the independent-FMA form y_e(r) = fma(r, dy_e, y_e(0)))
+        double yi[D], Li = Lc;
 #pragma unroll
         for (int k = 0; k < D; ++k) yi[k] = y[k];
-#endif
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             double C;
-#ifdef BGK_EXP_INCR
-            if constexpr (D == 3) C = Li - fabs(yi[0]) - fabs(yi[1]) - fabs(yi[2]);
-            else C = Li - fabs(yi[0]) - fabs(yi[1]);
+            if constexpr (SG) {
+                if constexpr (D == 3) C = fma(fabs(yi[0]), sn, Li) - fabs(yi[1]) - fabs(yi[2]);
+                else C = fma(fabs(yi[0]), sn, Li) - fabs(yi[1]);
+                Sa[r] += fabs(C);
+            } else {
+                if constexpr (D == 3) C = Li - fabs(yi[0]) - fabs(yi[1]) - fabs(yi[2]);
+                else C = Li - fabs(yi[0]) - fabs(yi[1]);
+            }
 #pragma unroll
             for (int k = 0; k < D; ++k) yi[k] += dy[k];
             Li += dL;
-#else
-            // y_e(r) = y_e(0) + r dy_e: one FMA each with r an immediate -> rows are independent
-            const double rr = (double)r;
-            const double Lr = fma(rr, dL, Lc);
-            if constexpr (D == 3) {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                const double yb = fma(rr, dy[2], y[2]);
-                C = (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
-            } else {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                C = (Lr - fabs(yn)) - fabs(yt);
-            }
-#endif
             if constexpr (NV == 1) {
                 Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
             } else {
@@ -323,7 +319,7 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
             (void)nready;
 #endif
             asm volatile("" ::: "memory");                 // order the stage reads after the test
-            coeffs(e + 1, y, dy, Lc, dL);
+            coeffs(e + 1, y, dy, Lc, dL, sn);
         }
     }
     // epilogue: ftilde, moment partials, stability bound
@@ -363,7 +359,8 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
             if constexpr (D == 3) s3 += v3v * out[0];
             sE += vv * out[0];
             if constexpr (NV == 2) sE += out[1];
-            amax = fmax(amax, -Sc[r]);
+            if constexpr (SG) amax = fmax(amax, Sa[r]);
+            else amax = fmax(amax, -Sc[r]);
         }
     }
     s0 = warp_sum(s0);
@@ -982,35 +979,31 @@ void dispatch_ws(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     }
 }
 
-template <int D, int R, int WPB>
+template <int D, int R, int WPB, bool SG>
 constexpr int stages_for() {
     // ring depth: keep NST-1 neighbour boxes in flight; bounded by 227 KB of shared memory
     // (sized for 8 resident warps per SM: blocks of WPB warps, 8 / WPB blocks per SM)
     constexpr int blocks = WPB >= 8 ? 1 : 8 / WPB;
-    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R>::BYTES);
+    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R, SG>::BYTES);
     return n > 8 ? 8 : (n < 2 ? 2 : n);
 }
 
-template <int D, int R, int WPB>
+template <int D, int R, int WPB, bool SG = false>
 void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int NST = stages_for<D, R, WPB>();
-    constexpr size_t smem = (size_t)WPB * NST * Stage<D, R>::BYTES + WPB * NST * 8;
-    static int grid = 0;
-    if (!grid) {
-        cudaFuncSetAttribute(k_transport<D, R, NST, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_transport<D, R, NST, WPB>, WPB * 32, smem);
-        grid = sms * (per_sm > 0 ? per_sm : 1);
+    constexpr int NST = stages_for<D, R, WPB, SG>();
+    constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG>::BYTES + WPB * NST * 8;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
     }
-    (void)grid;
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
-    k_transport<D, R, NST, WPB><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
+    k_transport<D, R, NST, WPB, SG><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
 }
 
 template <int D, int R>
 void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
+    if (a.signed_n) return launch_one<D, R, kDefaultWarps, true>(tm, a, s);   // second-order WLS
     if constexpr (D == 3 && (R == 25 || R == 17 || R == 13 || R == 9)) {
         if (wpb == 12) return launch_one<D, R, 12>(tm, a, s);
         if (wpb == 16) return launch_one<D, R, 16>(tm, a, s);
@@ -1176,12 +1169,13 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
         const char* e = getenv("BGK_TRANSPORT_WS");
         return e ? atoi(e) : 0;
     }();
-    if (variant == 1 && !c->grouped) {
+    a.signed_n = c->wls_order == 2;
+    if (variant == 1 && !c->grouped && !a.signed_n) {
         if (c->d == 3) dispatch_ws<3>(c->R, tm, a, s);
         else dispatch_ws<2>(c->R, tm, a, s);
         return;
     }
-    if (c->grouped) {
+    if (c->grouped && !a.signed_n) {
         const int n_groups = (int)((c->N_int + kGroup - 1) / kGroup);
         if (c->d == 3) dispatch_grp<3>(c->R, tm, a, n_groups, s);
         else dispatch_grp<2>(c->R, tm, a, n_groups, s);

@@ -116,8 +116,8 @@ __device__ __forceinline__ void frame_of(const double (&d)[D], double (&F)[D][D]
         const double rxy2 = d[0] * d[0] + d[1] * d[1];
         const double rxy = sqrt(rxy2);
         const double r = sqrt(rxy2 + d[D - 1] * d[D - 1]);
-        double cp = 1.0, sp = 0.0;                  // Z10: phi = atan2(+0,+0) = 0
-        if (rxy > 0.0) { cp = d[0] / rxy; sp = d[1] / rxy; }
+        double cp = 1.0, sp = 0.0;                  // Z10 / Z26: phi = 0 for a pair vertical to rounding
+        if (rxy2 > 1e-16 * (rxy2 + d[D - 1] * d[D - 1])) { cp = d[0] / rxy; sp = d[1] / rxy; }
         const double ct = d[D - 1] / r, st = rxy / r;
         double* f = &F[0][0];
         f[0] = st * cp; f[1] = st * sp; f[2] = ct;       // n
@@ -126,12 +126,38 @@ __device__ __forceinline__ void frame_of(const double (&d)[D], double (&F)[D][D]
     }
 }
 
-template <int D>
+// Taylor monomials of the scaled offset q = d/h: order 1 -> q; order 2 -> (q, q_a^2/2, q_a q_b (a<b))
+// (the second-order expansion adds the Hessian; same ordering as the oracle's)
+template <int D, int ORDER>
+struct Taylor {
+    static constexpr int NU = ORDER == 1 ? D : (D == 2 ? 5 : 9);
+    __device__ static __forceinline__ void mono(const double (&q)[D], double (&mv)[NU]) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) mv[a] = q[a];
+        if constexpr (ORDER == 2) {
+#pragma unroll
+            for (int a = 0; a < D; ++a) mv[D + a] = 0.5 * q[a] * q[a];
+            int k = 2 * D;
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int b = a + 1; b < D; ++b) mv[k++] = q[a] * q[b];
+        }
+    }
+};
+
+template <int D, int ORDER>
 __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __restrict__ ids, int64_t n_ids,
                                const int64_t* __restrict__ nb_off, const int32_t* __restrict__ nb_idx, double h,
                                double h2, double alpha, double dv, double* __restrict__ S_out, double* __restrict__ P,
-                               double* __restrict__ rot_out, double* __restrict__ frame_out, int64_t* err) {
-    constexpr int PD = (D == 2) ? 4 : 10;
+                               double* __restrict__ cw, double* __restrict__ rot_out, double* __restrict__ frame_out,
+                               int64_t* err) {
+    // pair record: 2D (pn, pt) [+ (s_n, 0)], 3D (dy_n, pn1, pn2, dy_t, pt1, pt2, dy_b, pb1, pb2, dL) [+ (s_n, 0)]
+    // -- the signed tail only for second order, where abar may be negative (s_n = -sign(abar))
+    constexpr int PD0 = (D == 2) ? 4 : 10;
+    constexpr int PD = ORDER == 2 ? PD0 + 2 : PD0;
+    using T = Taylor<D, ORDER>;
+    constexpr int NU = T::NU;
     const int lane = threadIdx.x & 31;
     const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
     if (w >= n_ids) return;
@@ -142,28 +168,38 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
     double xi[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) xi[a] = x[(int64_t)p * D + a];
-    double A[D][D];
+    constexpr int NT = NU * (NU + 1) / 2;      // upper triangle of the normal matrix
+    double At[NT];
 #pragma unroll
-    for (int r = 0; r < D; ++r)
-#pragma unroll
-        for (int q = 0; q < D; ++q) A[r][q] = 0.0;
+    for (int t = 0; t < NT; ++t) At[t] = 0.0;
     for (int e = lane; e < m; e += 32) {
         const int j = nb_idx[off + e];
-        double xj[D], dd[D];
+        double xj[D], dd[D], mv[NU];
 #pragma unroll
         for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; dd[a] = (xj[a] - xi[a]) * inv_h; }
+        T::mono(dd, mv);
         const double wgt = exp(-alpha * dist2_rn<D>(xi, xj) / h2);
+        int t = 0;
 #pragma unroll
-        for (int r = 0; r < D; ++r)
+        for (int r = 0; r < NU; ++r)
 #pragma unroll
-            for (int q = 0; q < D; ++q) A[r][q] += wgt * dd[r] * dd[q];
+            for (int q = r; q < NU; ++q) At[t++] += wgt * mv[r] * mv[q];
     }
+    double A[NU][NU];
+    {
+        int t = 0;
 #pragma unroll
-    for (int r = 0; r < D; ++r)
+        for (int r = 0; r < NU; ++r)
 #pragma unroll
-        for (int q = 0; q < D; ++q) A[r][q] = warp_sum(A[r][q]);
-    double Si[D][D];
-    bool ok = (m >= D + 2) && well_conditioned<D>(A) && small_inverse<D>(A, Si);
+            for (int q = r; q < NU; ++q) {
+                const double v = warp_sum(At[t++]);
+                A[r][q] = v;
+                A[q][r] = v;
+            }
+    }
+    double Si[NU][NU];
+    const int m_min = ORDER == 1 ? D + 2 : NU + 1;
+    bool ok = (m >= m_min) && well_conditioned<NU>(A) && small_inverse<NU>(A, Si);
     if (!ok) {
         if (lane == 0) latch_error(err, BGK_E_DEFICIENT_STENCIL, p);
         return;
@@ -176,16 +212,17 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
     }
     for (int e = lane; e < m; e += 32) {
         const int j = nb_idx[off + e];
-        double xj[D], dd[D];
+        double xj[D], dd[D], mv[NU];
 #pragma unroll
         for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; dd[a] = (xj[a] - xi[a]) * inv_h; }
+        T::mono(dd, mv);
         const double wgt = exp(-alpha * dist2_rn<D>(xi, xj) / h2);
-        double av[D];   // a_j = w_j S d_j, physical units 1/m
+        double av[D];   // a_j = w_j [(M^T W M)^{-1} m_j]_{0:d} / h, physical units 1/m
 #pragma unroll
         for (int r = 0; r < D; ++r) {
             double s = 0.0;
 #pragma unroll
-            for (int q = 0; q < D; ++q) s += Si[r][q] * dd[q];
+            for (int q = 0; q < NU; ++q) s += Si[r][q] * mv[q];
             av[r] = wgt * s * inv_h;
         }
         double F[D][D];
@@ -198,6 +235,7 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
             for (int a = 0; a < D; ++a) s += av[a] * F[k][a];
             rot[k] = s;
         }
+        cw[off + e] = 0.0;     // boundary-interpolation weights are defined on boundary rows only
         double* pe = P + (off + e) * PD;
 #pragma unroll
         for (int k = 0; k < D; ++k)
@@ -212,7 +250,11 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
                 pe[k * D] = dv * pe[k * D];
                 dl += pe[k * D];
             }
-            pe[PD - 1] = dl;
+            pe[PD0 - 1] = dl;
+        }
+        if constexpr (ORDER == 2) {
+            pe[PD0] = rot[0] > 0.0 ? -1.0 : 1.0;   // C's n-term = y_n - sign(abar)|y_n| (P:408-410 literal)
+            pe[PD0 + 1] = 0.0;
         }
         if (rot_out) {
 #pragma unroll
@@ -270,7 +312,10 @@ __global__ void k_wls_boundary(const double* __restrict__ x, const int8_t* __res
     double Bi[n][n];
     const bool ok = (mi >= D + 2) && well_conditioned<n>(B) && small_inverse<n>(B, Bi);
     if (!ok) {
-        if (lane == 0) latch_error(err, BGK_E_DEFICIENT_STENCIL, b);
+        if (lane == 0) {
+            latch_error(err, BGK_E_DEFICIENT_STENCIL, b);
+            bcnt[b] = 0;   // keep the interpolation kernel in bounds until the error is reported
+        }
         return;
     }
     int base = 0;   // compacted (interior neighbour, weight) list for the interpolation kernel
@@ -306,20 +351,29 @@ __global__ void k_wls_boundary(const double* __restrict__ x, const int8_t* __res
 
 int launches_wls() { return 2; }
 
+template <int D>
+static void launch_interior(bgk_ctx* c, unsigned gi, int wpb, double* rot, double* frames, cudaStream_t s) {
+    const double h = c->cfg.h, h2 = c->cfg.h2, al = c->cfg.alpha_w;
+    if (c->wls_order == 2)
+        k_wls_interior<D, 2><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2, al,
+                                                     c->dv, c->g.S, c->g.P, c->g.cw, rot, frames, c->err);
+    else
+        k_wls_interior<D, 1><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2, al,
+                                                     c->dv, c->g.S, c->g.P, c->g.cw, rot, frames, c->err);
+}
+
 static void run_wls(bgk_ctx* c, double* rot, double* frames, cudaStream_t s) {
     const int wpb = 4;
     const unsigned gi = (unsigned)((c->N_int + wpb - 1) / wpb);
     const unsigned gb = (unsigned)((c->N_b + wpb - 1) / wpb);
     const double h = c->cfg.h, h2 = c->cfg.h2, al = c->cfg.alpha_w;
     if (c->d == 3) {
-        if (gi) k_wls_interior<3><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2,
-                                                         al, c->dv, c->g.S, c->g.P, rot, frames, c->err);
+        if (gi) launch_interior<3>(c, gi, wpb, rot, frames, s);
         if (gb && !rot)
             k_wls_boundary<3><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
                                                      h2, al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
     } else {
-        if (gi) k_wls_interior<2><<<gi, wpb * 32, 0, s>>>(c->x, c->interior, c->N_int, c->g.nb_off, c->g.nb_idx, h, h2,
-                                                         al, c->dv, c->g.S, c->g.P, rot, frames, c->err);
+        if (gi) launch_interior<2>(c, gi, wpb, rot, frames, s);
         if (gb && !rot)
             k_wls_boundary<2><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h,
                                                      h2, al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
