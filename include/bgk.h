@@ -127,7 +127,9 @@ bgk_status bgk_wls_coeffs(bgk_ctx* ctx, bgk_stream stream);
 /* Copy WLS results out (device or host pointers, NULL to skip):
  *   S[N][dims][dims] (interior rows), rot[nnz][dims] = (abar, bbar[, gbar]),
  *   frames[nnz][dims][dims] = rows n, t[, b], cw[nnz] = boundary weights (0 elsewhere).
- * nnz = offsets[N] of the last neighbour build.  Synchronises. */
+ * nnz = offsets[N] of the last neighbour build.  rot/frames are assembled in the idle f buffer,
+ * or -- when that is smaller than nnz*(dims+dims^2) doubles (tiny velocity grids) -- in a
+ * temporary stream-ordered device allocation freed before return.  Synchronises. */
 bgk_status bgk_get_wls(bgk_ctx* ctx, double* S, double* rot, double* frames, double* cw,
                        bgk_stream stream);
 

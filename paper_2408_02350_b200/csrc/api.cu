@@ -78,18 +78,20 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->vmin = -cfg->vmax;
     c->wls_order = cfg->wls_order == 2 ? 2 : 1;
     c->PD = (c->d == 2 ? 4 : 10) + (c->wls_order == 2 ? 2 : 0);
-    c->R = transport_rows_per_thread(c->d, c->n1);
+    c->np = transport_particles_per_warp(c->d, c->wls_order);
+    c->R = transport_rows_per_thread(c->d, c->n1, c->np);
     c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
     c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
     c->nwpp = c->nchunk * c->ncg;
     c->nslots = c->nwpp * 32;
-    {   // grouped transport: union lists of up to group_size() * max_nb members (power of two for the sort)
-        int u = 1;
-        while (u < group_size() * c->max_nb) u <<= 1;
-        c->ucap = u;
-        const char* e = getenv("BGK_TRANSPORT_GRP");
-        c->grouped = e ? atoi(e) != 0 : false;   // measured slower on C5 (profiles/r01_tuning.md)
-        if ((size_t)c->ucap * 8 > 48 * 1024 || c->ucap > 65535) c->grouped = false;   // sort buffers in smem
+    // particle-pair warps: union of two lists, <= 2 max_nb int2 entries per pair, CSR positions < 2^16
+    c->ucap = 2 * c->max_nb;
+    if (c->np == 2 && c->max_nb >= 65536) {
+        c->np = 1;
+        c->R = transport_rows_per_thread(c->d, c->n1, 1);
+        c->nchunk = (c->n1 + c->R - 1) / c->R;
+        c->nwpp = c->nchunk * c->ncg;
+        c->nslots = c->nwpp * 32;
     }
     c->bnd_chunk = 256;
     c->bnd_nch = (int)((c->Ks + 511) / 512);   // k_bnd_interp: 256 threads x 2 nodes per block
@@ -116,7 +118,6 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->outbuf = k.take<double>(N * (d + 2));
     c->err = k.take<int64_t>(4);
     c->stab = k.take<unsigned long long>(1);
-    c->work = k.take<unsigned long long>(1);
     c->scan_tmp = k.take<int64_t>(1024);
     c->g.cell_of = k.take<int32_t>(N);
     c->g.cell_cnt = k.take<int32_t>(c->ncell);
@@ -133,11 +134,9 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->g.bcw = k.take<double>(c->cap);
     c->g.bcnt = k.take<int32_t>(N);
     c->g.order = k.take<int32_t>(N);
-    const int64_t ng = (N + group_size() - 1) / group_size();
-    c->gU = k.take<int32_t>(c->grouped ? (size_t)ng * c->ucap : 1);
-    c->gUlen = k.take<int32_t>(ng);
-    c->gCnt = k.take<uint8_t>(c->grouped ? (size_t)ng * c->ucap : 1);
-    c->upos = k.take<uint16_t>(c->grouped ? (size_t)c->cap : 1);
+    const int64_t ng = c->np == 2 ? (N + 1) / 2 : 1;
+    c->gU = k.take<int32_t>(c->np == 2 ? (size_t)ng * c->ucap * 2 : 2);   // int2 entries
+    c->gUlen = k.take<int32_t>(4 * ng);
     return k.off + 256;
 }
 
@@ -329,8 +328,15 @@ bgk_status bgk_get_wls(bgk_ctx* c, double* Sout, double* rot, double* frames, do
     if (Sout && (st = copy_out(c, Sout, c->g.S, sizeof(double) * c->N * d * d, s)) != BGK_OK) return st;
     if (cw && nnz && (st = copy_out(c, cw, c->g.cw, sizeof(double) * nnz, s)) != BGK_OK) return st;
     if (rot || frames) {
+        // scratch: the idle f buffer, or (tiny velocity grids) a temporary stream-ordered allocation
         double* scratch = c->f[1 - c->fcur];
-        if ((size_t)nnz * (d + d * d) > (size_t)c->N * c->RS) return BGK_E_CAPACITY;
+        double* tmp = nullptr;
+        const size_t need = (size_t)nnz * (d + d * d);
+        if (need > (size_t)c->N * c->RS) {
+            cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(double) * need, s);
+            if (e != cudaSuccess) return cuda_fail(c, e);
+            scratch = tmp;
+        }
         double* r = scratch;
         double* fr = scratch + (size_t)nnz * d;
         cudaMemsetAsync(scratch, 0, sizeof(double) * nnz * (d + d * d), s);
@@ -338,6 +344,7 @@ bgk_status bgk_get_wls(bgk_ctx* c, double* Sout, double* rot, double* frames, do
         if ((st = check_launch(c)) != BGK_OK) return st;
         if (rot && nnz && (st = copy_out(c, rot, r, sizeof(double) * nnz * d, s)) != BGK_OK) return st;
         if (frames && nnz && (st = copy_out(c, frames, fr, sizeof(double) * nnz * d * d, s)) != BGK_OK) return st;
+        if (tmp) cudaFreeAsync(tmp, s);
     }
     return sync_check(c, s);
 }

@@ -74,13 +74,10 @@ struct bgk_ctx {
     double* outbuf;     // [N][d+2] scratch for moments / copies
     int64_t* err;       // [4] code, particle, needed, spare
     unsigned long long* stab;  // [1] max_{i,k} sum_j |C_ijk| as ordered bits
-    unsigned long long* work;  // [1] persistent transport work counter
-    int32_t* gU;        // [groups][ucap] union of the neighbour lists of each particle group (grouped transport)
+    int32_t* gU;        // [groups][ucap] packed union (j << 4 | member mask) of each particle group's lists
     int32_t* gUlen;     // [groups]
-    uint8_t* gCnt;      // [groups][ucap] users of each union member
-    uint16_t* upos;     // [cap] union position of each CSR entry of an interior particle
     int ucap;
-    bool grouped;       // grouped (block-shared neighbour ring) transport kernel
+    int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)
     int64_t* scan_tmp;  // [1024]
     bgk::Geo g;
     // host-side error state
@@ -143,7 +140,8 @@ void launch_moments_finalize(bgk_ctx* c, double* out, cudaStream_t s);
 void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_check_domain(bgk_ctx* c, cudaStream_t s);
-int transport_rows_per_thread(int d, int n1);
+int transport_rows_per_thread(int d, int n1, int np);
+int transport_particles_per_warp(int d, int wls_order);
 bool make_tensor_maps(bgk_ctx* c);
 // storage index of local node t = k1*ncol + col  ->  k1*ncs + col
 __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int ncs) {
@@ -151,7 +149,6 @@ __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int
     return k1 * ncs + (t - k1 * ncol);
 }
 int launches_neighbors();
-int group_size();
 void launch_group_union(bgk_ctx* c, cudaStream_t s);
 int launches_wls();
 

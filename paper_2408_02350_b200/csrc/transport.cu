@@ -5,14 +5,18 @@
 // For interior particle i and every local velocity node k (c = v_k - W_i,
 // W = U^n in ALE mode, 0 on a fixed cloud):
 //     C_ijk = sum_{e in n,t[,b]} (P_e.c - |P_e.c|)          (P_e = rot_e * frame_e, wls.cu)
-//           = L_j(c) - |y_n| - |y_t| - |y_b|,   L_j(c) = a_j.c = y_n + y_t + y_b
+//           = 2 sum_e min(y_e, 0),   y_e = P_e.c
 //     ftilde_ik = f_ik - dt * sum_j C_ijk (f_jk - f_ik)     (g1 and g2 share C_ijk in 2D)
 //
 // Mapping: a warp owns one particle, one chunk of R nodes along v_1
 // and a group of 32 velocity columns; each lane owns one column and walks the R
-// nodes.  Along v_1 every projection is affine, so y_e and L advance by one add per
-// node.  Per (i, j, k) triple: 4 increments, 3 abs-subtracts (free |.| operand
-// modifier), 1 FMA (sum C f_j), 1 add (sum C) = 9 DP instructions, plus one LDS.
+// nodes.  Along v_1 every projection is affine: y_e(r) = y_e(0) + r dy_e is one DFMA
+// (r an immediate), min(y_e, 0) runs on the integer pipe (neg_part).  Per (i, j, k)
+// triple: 3 DFMA + 2 DADD for C/2, 1 DFMA (sum C f_j), 1 DADD (sum C) = 7 DP
+// instructions, 3 integer min, one LDS.  (The earlier form L - |y_n| - |y_t| - |y_b|
+// with incremental y_e and L took 9 DP; the same C5 time -- the kernel is limited by
+// issue and latency with 2 warps per SM sub-partition, profiles/r01_tuning.md.)
+// The second-order WLS variant (SG) keeps the signed n-term form.
 //
 // Neighbour rows are staged by TMA: for each neighbour j one elected lane issues a
 // cp.async.bulk.tensor.3d of the box f[j][k1s .. k1s+R)[cols .. cols+32) (6.4 KB in 3D)
@@ -33,7 +37,8 @@ namespace bgk {
 
 namespace {
 
-constexpr int kDefaultWarps = 4;   // warps per block (= particles per block); tuned on B200 (profiles/r01_tuning.md)
+constexpr int kDefaultWarps = 4;   // warps per block; tuned on B200 (profiles/r01_tuning.md)
+constexpr int kDefaultNP = 1;      // particles per warp of the 3D first-order transport (BGK_TRANSPORT_NP)
 
 struct TArgs {
     const double* __restrict__ f;
@@ -45,12 +50,9 @@ struct TArgs {
     const double* __restrict__ P;
     double* __restrict__ partials;
     unsigned long long* stab;
-    unsigned long long* work;          // persistent-warp item counter (zeroed before each launch)
-    const int32_t* __restrict__ gU;    // grouped kernel: union neighbour list per particle group
-    const int32_t* __restrict__ gUlen; //                 its length
-    const uint8_t* __restrict__ gCnt;  //                 users of each union member
-    const uint16_t* __restrict__ upos; //                 union position of each CSR entry
-    int ucap;                          //                 capacity per group
+    const int32_t* __restrict__ gU;    // multi-particle warps: packed union list per particle group
+    const int32_t* __restrict__ gUlen; //                       its length
+    int ucap;                          //                       capacity per group
     bool signed_n;                     // second-order WLS: pair record carries s_n = -sign(abar)
     int64_t n_int;
     int n1, ncol, ncs, c0, ncg, nwpp;
@@ -128,6 +130,14 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 
+// min(t, 0) without the fp64 pipe: the high word's sign decides, min(hi, 0) on the integer
+// pipe keeps a negative t exactly and turns a positive one into the denormal lo * 2^-1074
+// (< 2^-1042), which vanishes against the O(|a||c|) terms it is summed with.  y - |y| = 2 min(y, 0),
+// so C_ijk = sum_e (y_e - |y_e|) = 2 sum_e neg_part(y_e).
+__device__ __forceinline__ double neg_part(double t) {
+    return __hiloint2double(min(__double2hiint(t), 0), __double2loint(t));
+}
+
 // Per (neighbour, lane) coefficients at the chunk's first node k1s:
 //   y_e = P_e . c0 (c0 = v(k1s, col) - W), dy_e = dv P_e[0] (increment per v_1 node),
 //   L = sum_e y_e, dL = sum_e dy_e.
@@ -155,6 +165,79 @@ __device__ __forceinline__ void pair_coeffs(const double* pv, const double (&c0v
     }
 }
 
+// Epilogue of one (particle, chunk, column group) item: ftilde = f - dt (sum_j C f_j - f sum_j C)
+// on the lane's R rows, the warp's moment partials (fixed-order shuffles: deterministic) and
+// max_k sum_j |C_ijk| into the stability word.
+template <int D, int R, bool SG, int NV = (D == 2 ? 2 : 1)>
+__device__ __forceinline__ void transport_epilogue(const TArgs& A, int p, int w, int k1s, int colc, int gc,
+                                                   bool valid, const double (&Qf)[R][NV], const double (&Sc)[R],
+                                                   const double (&Sa)[SG ? R : 1]) {
+    const int lane = threadIdx.x & 31;
+    const int64_t rowstride = (int64_t)A.ncs * NV;
+    const int64_t lane_off = (int64_t)k1s * rowstride + (int64_t)colc * NV;
+    const double* fi = A.f + (int64_t)p * A.n1 * rowstride + lane_off;
+    double* fto = A.ft + (int64_t)p * A.n1 * rowstride + lane_off;
+    double v2v = 0.0, v3v = 0.0;
+    if constexpr (D == 3) {
+        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+        v2v = axis_node(A.vmax, A.dv, k2);
+        v3v = axis_node(A.vmax, A.dv, k3);
+    } else {
+        v2v = axis_node(A.vmax, A.dv, gc);
+    }
+    // first order accumulates C/2 (neg_part form): the factor 2 enters through dt and the bound
+    const double dtq = SG ? A.dt : 2.0 * A.dt;
+    const double cq = SG ? 1.0 : 2.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, sE = 0.0, amax = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (k1s + r >= A.n1) break;                      // ragged last chunk (rows past Nv are TMA zero-fill)
+        const double v1 = axis_node(A.vmax, A.dv, k1s + r);
+        const double vv = (D == 3) ? v1 * v1 + v2v * v2v + v3v * v3v : v1 * v1 + v2v * v2v;
+        double out[NV];
+        if constexpr (NV == 1) {
+            const double fv = __ldg(fi + r * rowstride);
+            out[0] = fv - dtq * (Qf[r][0] - fv * Sc[r]);
+            if (valid) fto[r * rowstride] = out[0];
+        } else {
+            const double2 fv = __ldg(reinterpret_cast<const double2*>(fi + r * rowstride));
+            out[0] = fv.x - dtq * (Qf[r][0] - fv.x * Sc[r]);
+            out[1] = fv.y - dtq * (Qf[r][1] - fv.y * Sc[r]);
+            if (valid) *reinterpret_cast<double2*>(fto + r * rowstride) = make_double2(out[0], out[1]);
+        }
+        if (valid) {
+            s0 += out[0];
+            s1 += v1 * out[0];
+            s2 += v2v * out[0];
+            if constexpr (D == 3) s3 += v3v * out[0];
+            sE += vv * out[0];
+            if constexpr (NV == 2) sE += out[1];
+            if constexpr (SG) amax = fmax(amax, Sa[r]);
+            else amax = fmax(amax, -cq * Sc[r]);
+        }
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    s3 = warp_sum(s3);
+    sE = warp_sum(sE);
+    amax = warp_max(amax);
+    if (lane == 0) {
+        double* pp = A.partials + ((int64_t)p * A.nwpp + w) * kPM;
+        pp[0] = s0;
+        pp[1] = s1;
+        pp[2] = s2;
+        if constexpr (D == 3) {
+            pp[3] = s3;
+            pp[4] = sE;
+        } else {
+            pp[3] = sE;
+            pp[4] = 0.0;
+        }
+        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+    }
+}
+
 // One ring stage: the neighbour's box of f (R rows x 32 columns x nv) and its pair data P_e.
 // SG (second-order WLS): the pair record carries s_n = -sign(abar) after the first-order fields,
 // and C's n-term is y_n + s_n |y_n| (abar may be negative; P:408-410 applied literally).
@@ -169,8 +252,8 @@ struct Stage {
     static constexpr uint32_t BYTES = (F_BYTES + P_BYTES + 127) / 128 * 128;
 };
 
-template <int D, int R, int NST, int WPB, bool SG>
-__global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
+template <int D, int R, int NST, int WPB, bool SG, int MINB = 1>
+__global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
     using St = Stage<D, R, SG>;
     constexpr int NV = St::NV;
     constexpr int PD = St::PD;
@@ -275,31 +358,47 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
         const double* st = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) + lane * NV;
         // y_e and L advance by one add per node along v_1 (all DADD: measured ~2 % faster than
         // the independent-FMA form y_e(r) = fma(r, dy_e, y_e(0)))
-        double yi[D], Li = Lc;
+        if constexpr (SG) {
+            // second-order WLS: abar may be negative, C = y_n + s_n |y_n| + sum_{t,b} (y - |y|)
+            double yi[D], Li = Lc;
 #pragma unroll
-        for (int k = 0; k < D; ++k) yi[k] = y[k];
+            for (int k = 0; k < D; ++k) yi[k] = y[k];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            double C;
-            if constexpr (SG) {
+            for (int r = 0; r < R; ++r) {
+                double C;
                 if constexpr (D == 3) C = fma(fabs(yi[0]), sn, Li) - fabs(yi[1]) - fabs(yi[2]);
                 else C = fma(fabs(yi[0]), sn, Li) - fabs(yi[1]);
                 Sa[r] += fabs(C);
-            } else {
-                if constexpr (D == 3) C = Li - fabs(yi[0]) - fabs(yi[1]) - fabs(yi[2]);
-                else C = Li - fabs(yi[0]) - fabs(yi[1]);
-            }
 #pragma unroll
-            for (int k = 0; k < D; ++k) yi[k] += dy[k];
-            Li += dL;
-            if constexpr (NV == 1) {
-                Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
-            } else {
-                const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
-                Qf[r][0] = fma(C, v.x, Qf[r][0]);
-                Qf[r][1] = fma(C, v.y, Qf[r][1]);
+                for (int k = 0; k < D; ++k) yi[k] += dy[k];
+                Li += dL;
+                if constexpr (NV == 1) {
+                    Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
+                } else {
+                    const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
+                    Qf[r][0] = fma(C, v.x, Qf[r][0]);
+                    Qf[r][1] = fma(C, v.y, Qf[r][1]);
+                }
+                Sc[r] += C;
             }
-            Sc[r] += C;
+        } else {
+            // first order: C/2 = sum_e min(y_e, 0), y_e(r) = y_e + r dy_e (one DFMA each), the min on
+            // the integer pipe (neg_part); the factor 2 is applied in the epilogue.  7 DP per triple.
+            (void)Lc;
+            (void)dL;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                double C = neg_part(fma((double)r, dy[0], y[0])) + neg_part(fma((double)r, dy[1], y[1]));
+                if constexpr (D == 3) C += neg_part(fma((double)r, dy[2], y[2]));
+                if constexpr (NV == 1) {
+                    Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
+                } else {
+                    const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
+                    Qf[r][0] = fma(C, v.x, Qf[r][0]);
+                    Qf[r][1] = fma(C, v.y, Qf[r][1]);
+                }
+                Sc[r] += C;
+            }
         }
         // refill stage of neighbour e with neighbour e + NST (index from the register batches)
         const int t = e + NST;
@@ -322,693 +421,266 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
             coeffs(e + 1, y, dy, Lc, dL, sn);
         }
     }
-    // epilogue: ftilde, moment partials, stability bound
-    const int64_t rowstride = (int64_t)A.ncs * NV;
-    const int64_t lane_off = (int64_t)k1s * rowstride + (int64_t)colc * NV;
-    const double* fi = A.f + (int64_t)p * A.n1 * rowstride + lane_off;
-    double* fto = A.ft + (int64_t)p * A.n1 * rowstride + lane_off;
-    double v2v = 0.0, v3v = 0.0;
-    if constexpr (D == 3) {
-        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-        v2v = axis_node(A.vmax, A.dv, k2);
-        v3v = axis_node(A.vmax, A.dv, k3);
-    } else {
-        v2v = axis_node(A.vmax, A.dv, gc);
-    }
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, sE = 0.0, amax = 0.0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        if (k1s + r >= A.n1) break;                      // ragged last chunk (rows past Nv are TMA zero-fill)
-        const double v1 = axis_node(A.vmax, A.dv, k1s + r);
-        const double vv = (D == 3) ? v1 * v1 + v2v * v2v + v3v * v3v : v1 * v1 + v2v * v2v;
-        double out[NV];
-        if constexpr (NV == 1) {
-            const double fv = __ldg(fi + r * rowstride);
-            out[0] = fv - A.dt * (Qf[r][0] - fv * Sc[r]);
-            if (valid) fto[r * rowstride] = out[0];
-        } else {
-            const double2 fv = __ldg(reinterpret_cast<const double2*>(fi + r * rowstride));
-            out[0] = fv.x - A.dt * (Qf[r][0] - fv.x * Sc[r]);
-            out[1] = fv.y - A.dt * (Qf[r][1] - fv.y * Sc[r]);
-            if (valid) *reinterpret_cast<double2*>(fto + r * rowstride) = make_double2(out[0], out[1]);
-        }
-        if (valid) {
-            s0 += out[0];
-            s1 += v1 * out[0];
-            s2 += v2v * out[0];
-            if constexpr (D == 3) s3 += v3v * out[0];
-            sE += vv * out[0];
-            if constexpr (NV == 2) sE += out[1];
-            if constexpr (SG) amax = fmax(amax, Sa[r]);
-            else amax = fmax(amax, -Sc[r]);
-        }
-    }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    s3 = warp_sum(s3);
-    sE = warp_sum(sE);
-    amax = warp_max(amax);
-    if (lane == 0) {
-        double* pp = A.partials + ((int64_t)p * A.nwpp + w) * kPM;
-        pp[0] = s0;
-        pp[1] = s1;
-        pp[2] = s2;
-        if constexpr (D == 3) {
-            pp[3] = s3;
-            pp[4] = sE;
-        } else {
-            pp[3] = sE;
-            pp[4] = 0.0;
-        }
-        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
-    }
+    transport_epilogue<D, R, SG>(A, p, w, k1s, colc, gc, valid, Qf, Sc, Sa);
     }
 }
-// ============================================================================
-// Grouped transport: one block = G particles (consecutive in the Morton-ordered interior
-// list) x one (chunk, column group).  The block walks the sorted UNION of the G neighbour
-// lists (precomputed per step by k_group_union); every union neighbour's box is fetched
-// ONCE by TMA into a block-shared ring and consumed by every warp whose particle has it.
-// On C5 the union of 8 Morton-consecutive particles has ~276 members against 947
-// per-particle neighbours, so the L2 -> SM traffic that bounded the per-warp ring
-// (~12-13 TB/s, the chip's L2 throughput cap) drops 3.4x.
-//   stage fill  : cp.async.bulk.tensor.3d, complete_tx on full[s]
-//   stage reuse : each warp, after waiting full[s] and (if the neighbour is its own)
-//                 applying it, bumps rel[s]; the G-th release re-arms and refills the stage
-//                 NST union members ahead.  Warps may drift up to NST members apart.
-//   pair data   : per warp, batches of 8 pair records by cp.async.bulk into a 2-deep ring.
-// ============================================================================
-constexpr int kGroup = 8;
-constexpr int kPBatch = 8;
-#ifndef BGK_GRP_MAX_STAGES
-#define BGK_GRP_MAX_STAGES 32
-#endif
-constexpr int kMaxGrpStages = BGK_GRP_MAX_STAGES;   // shared ring depth cap (smem bound: ~30 at R = 25)
 
-template <int D, int R>
-struct GStage {
-    static constexpr int NV = (D == 2) ? 2 : 1;
-    static constexpr int PD = (D == 2) ? 4 : 10;
-    static constexpr int ROW = 32 * NV;
-    static constexpr uint32_t F_BYTES = R * ROW * sizeof(double);           // multiple of 128 (R*256)
-    static constexpr uint32_t PB_BYTES = kPBatch * PD * sizeof(double);    // 640 B (3D) / 256 B (2D)
+// ============================================================================
+// Particle-pair warps (3D, first-order WLS).  A warp owns TWO consecutive particles A, B of the
+// cell-ordered interior list, one chunk of R nodes along v_1 and 32 velocity columns, and walks
+// the UNION of their neighbour lists (k_pair_union, rebuilt with the geometry), sorted into three
+// segments: members of both lists, of A only, of B only (ascending j inside each; the order in
+// which a particle's neighbours are summed is free up to rounding, Z22).  Each member's box
+// f[j][k1s .. k1s+R)[cols] is fetched ONCE by TMA and applied to every particle that has j --
+// on C5 the union of two neighbouring particles has 0.67x their combined members, so the
+// L2 -> SM traffic per (i, j, k) triple (the bound of the one-particle kernel: ~6.6 kB/clk,
+// the chip's L2 throughput cap) drops by a third.  The segment is known from the member's
+// position, so the inner loops carry no per-member mask test; members of both lists run one
+// fused row loop (one LDS of f_jk for two particles).  Warps stay independent.
+// Measured on C5 (profiles/r01_tuning.md): 96 ms against 74 ms for the one-particle kernel --
+// R = 13 (register budget of four accumulator rows) doubles the per-neighbour setup and the
+// L2 traffic was not the binding limit; kept as an opt-in (BGK_TRANSPORT_NP=2), parity-tested.
+// Union entries: int2 {j, eA | eB << 16} (CSR positions of j in A's and B's lists); counts
+// gUlen[4 g + {0, 1, 2}] = (both, A only, B only).
+// ============================================================================
+template <int R>
+struct PStage {
+    static constexpr int PD = 10;
+    static constexpr uint32_t F_BYTES = R * 32 * sizeof(double);
+    static constexpr uint32_t P_BYTES = PD * sizeof(double);
+    static constexpr uint32_t BYTES = (F_BYTES + 2 * P_BYTES + 127) / 128 * 128;
 };
 
-template <int D, int R, int NST>
-constexpr size_t grp_smem_bytes(int ucap) {
-    using St = GStage<D, R>;
-    return (size_t)NST * St::F_BYTES + (size_t)kGroup * 2 * St::PB_BYTES + (size_t)ucap * 5 +
-           (NST + 2 * kGroup) * 8 + NST * 8 + 256;
+// y_e = P_e . c at the chunk's first node and dy_e = dv P_e[0] (pair record slot 3e), 3D
+__device__ __forceinline__ void pair_y(const double* ps, double c1dv, double c2, double c3, double (&y)[3],
+                                       double (&dy)[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        dy[k] = ps[k * 3];
+        y[k] = fma(ps[k * 3], c1dv, fma(ps[k * 3 + 1], c2, ps[k * 3 + 2] * c3));
+    }
 }
 
-template <int D, int R, int NST>
-__global__ void __launch_bounds__(kGroup * 32, 1) k_transport_grp(const __grid_constant__ CUtensorMap tmap,
-                                                                  const TArgs A) {
-    using St = GStage<D, R>;
-    constexpr int NV = St::NV;
+template <int R, int NST, int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) k_transport_pair(const __grid_constant__ CUtensorMap tmap,
+                                                                   const TArgs A) {
+    using St = PStage<R>;
     constexpr int PD = St::PD;
-    constexpr int ROW = St::ROW;
+    constexpr int ROW = 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char* ring = smem_raw;
-    double* pring = reinterpret_cast<double*>(smem_raw + (size_t)NST * St::F_BYTES);
-    int32_t* sU = reinterpret_cast<int32_t*>(smem_raw + (size_t)NST * St::F_BYTES + (size_t)kGroup * 2 * St::PB_BYTES);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sU + A.ucap + ((A.ucap & 1) ? 1 : 0));
-    uint64_t* pbar = full + NST;                            // [kGroup][2]
-    int* rel = reinterpret_cast<int*>(pbar + 2 * kGroup);   // [NST]
-    volatile int* smem_member = rel + NST;                  // [NST] union member a stage holds / will hold
-    uint8_t* sCnt = reinterpret_cast<uint8_t*>(rel + 2 * NST);  // [ucap]
-
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int group = blockIdx.x;
-    const int w = blockIdx.y;
-    const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
-    const int k1s = chunk * R;
-    const int ulen = A.gUlen[group];
-    const int32_t* gU = A.gU + (int64_t)group * A.ucap;
-    for (int q = threadIdx.x; q < ulen; q += blockDim.x) {
-        sU[q] = gU[q];
-        sCnt[q] = A.gCnt[(int64_t)group * A.ucap + q];
-    }
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(full + s, 1);
-            rel[s] = 0;
-            smem_member[s] = s;
-        }
-        for (int g = 0; g < 2 * kGroup; ++g) mbar_init(pbar + g, 1);
+    unsigned char* ring = smem_raw + (size_t)wib * NST * St::BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)WPB * NST * St::BYTES) + wib * NST;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    __syncthreads();
-    if (threadIdx.x == 0)
-        for (int s = 0; s < NST && s < ulen; ++s) {
-            mbar_expect_tx(full + s, St::F_BYTES);
-            tma_load_3d(ring + s * St::F_BYTES, &tmap, cg * ROW, k1s, sU[s], full + s);
-        }
-
-    // this warp's particle (an idle warp of a short last group still releases every stage)
-    const int64_t pos = (int64_t)group * kGroup + wib;
-    const bool active = pos < A.n_int;
-    const int p = active ? A.order[pos] : 0;
-    const int64_t off = active ? A.nb_off[p] : 0;
-    const int m = active ? (int)(A.nb_off[p + 1] - off) : 0;
-    const double* Pp = A.P + off * PD;
-    const int col = cg * 32 + lane;
-    const bool valid = active && col < A.ncol;
-    const int colc = col < A.ncol ? col : 0;
-    const int gc = A.c0 + colc;
-    const uint16_t* upl = A.upos + off;
-    int nbA = lane < m ? (int)__ldg(upl + lane) : 0;       // union positions of my neighbours, 32 per batch
-    int nbB = 32 + lane < m ? (int)__ldg(upl + 32 + lane) : 0;
-    double* myP = pring + (size_t)wib * 2 * kPBatch * PD;
-    auto issue_pbatch = [&](int b) {          // lane 0: pair records [8b, 8b+8) -> buffer b & 1
-        const int n = min(kPBatch, m - b * kPBatch);
-        if (n <= 0) return;
-        uint64_t* bar = pbar + wib * 2 + (b & 1);
-        mbar_expect_tx(bar, (uint32_t)(n * PD * sizeof(double)));
-        bulk_load(myP + (b & 1) * kPBatch * PD, Pp + (int64_t)b * kPBatch * PD, (uint32_t)(n * PD * sizeof(double)),
-                  bar);
-    };
-    if (lane == 0) {
-        issue_pbatch(0);
-        issue_pbatch(1);
-    }
-
-    double Wp[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) Wp[a] = active ? A.W[(int64_t)p * D + a] : 0.0;
-    double c0v[D];
-    c0v[0] = axis_node(A.vmax, A.dv, k1s) - Wp[0];
-    if constexpr (D == 3) {
-        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-        c0v[1] = axis_node(A.vmax, A.dv, k2) - Wp[1];
-        c0v[2] = axis_node(A.vmax, A.dv, k3) - Wp[2];
-    } else {
-        c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
-    }
-    const double c1dv = c0v[0] / A.dv;
-    double Qf[R][NV], Sc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        Sc[r] = 0.0;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) Qf[r][q] = 0.0;
-    }
-    // Each warp visits only its own neighbours; neighbour e sits at union position u.  A
-    // member's stage is refilled (NST members ahead) by the last of its sCnt[u] users.
-    for (int e = 0; e < m; ++e) {
-        const int u = __shfl_sync(0xffffffffu, nbA, e & 31);
-        if ((e & 31) == 31) {                               // warp-uniform batch rotation
-            nbA = nbB;
-            nbB = e + 33 + lane < m ? (int)__ldg(upl + e + 33 + lane) : 0;
-        }
-        const int s = u % NST;
-        const int b = e / kPBatch, eb = e - b * kPBatch;
-        if (eb == 0) {
-            mbar_wait(pbar + wib * 2 + (b & 1), (uint32_t)(b >> 1) & 1u);
-            if (b >= 1 && lane == 0) issue_pbatch(b + 1);  // buffer (b+1)&1 held batch b-1: done
-        }
-        const double* ps = myP + (b & 1) * kPBatch * PD + eb * PD;
-        double pv[PD];
-#pragma unroll
-        for (int q = 0; q < PD; ++q) pv[q] = ps[q];
-        double y[D], dy[D], Lc, dL;
-        pair_coeffs<D>(pv, c0v, c1dv, A.dv, y, dy, Lc, dL);
-        // a warp may run many members ahead of a slow one: wait until stage s has been armed for
-        // member u (parity waits alone cannot tell rounds two phases apart), then for the data
-        while (smem_member[s] != u) __nanosleep(64);
-        mbar_wait(full + s, (uint32_t)(u / NST) & 1u);
-        const double* st = reinterpret_cast<const double*>(ring + s * St::F_BYTES) + lane * NV;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const double rr = (double)r;
-            const double Lr = fma(rr, dL, Lc);
-            double C;
-            if constexpr (D == 3) {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                const double yb = fma(rr, dy[2], y[2]);
-                C = (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
-            } else {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                C = (Lr - fabs(yn)) - fabs(yt);
-            }
-            if constexpr (NV == 1) {
-                Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
-            } else {
-                const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
-                Qf[r][0] = fma(C, v.x, Qf[r][0]);
-                Qf[r][1] = fma(C, v.y, Qf[r][1]);
-            }
-            Sc[r] += C;
-        }
-        __syncwarp();
-        if (lane == 0) {                                    // release; the member's last user refills
-            if (atomicAdd(rel + s, 1) == (int)sCnt[u] - 1) {
-                rel[s] = 0;
-                if (u + NST < ulen) {
-                    smem_member[s] = u + NST;
-                    __threadfence_block();
-                    mbar_expect_tx(full + s, St::F_BYTES);
-                    tma_load_3d(ring + s * St::F_BYTES, &tmap, cg * ROW, k1s, sU[u + NST], full + s);
-                }
-            }
-        }
-    }
-    if (!active) return;
-    // epilogue (as k_transport): ftilde, moment partials, stability bound
-    const int64_t rowstride = (int64_t)A.ncs * NV;
-    const int64_t lane_off = (int64_t)k1s * rowstride + (int64_t)colc * NV;
-    const double* fi = A.f + (int64_t)p * A.n1 * rowstride + lane_off;
-    double* fto = A.ft + (int64_t)p * A.n1 * rowstride + lane_off;
-    double v2v = 0.0, v3v = 0.0;
-    if constexpr (D == 3) {
-        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-        v2v = axis_node(A.vmax, A.dv, k2);
-        v3v = axis_node(A.vmax, A.dv, k3);
-    } else {
-        v2v = axis_node(A.vmax, A.dv, gc);
-    }
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, sE = 0.0, amax = 0.0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        if (k1s + r >= A.n1) break;
-        const double v1 = axis_node(A.vmax, A.dv, k1s + r);
-        const double vv = (D == 3) ? v1 * v1 + v2v * v2v + v3v * v3v : v1 * v1 + v2v * v2v;
-        double out[NV];
-        if constexpr (NV == 1) {
-            const double fv = __ldg(fi + r * rowstride);
-            out[0] = fv - A.dt * (Qf[r][0] - fv * Sc[r]);
-            if (valid) fto[r * rowstride] = out[0];
-        } else {
-            const double2 fv = __ldg(reinterpret_cast<const double2*>(fi + r * rowstride));
-            out[0] = fv.x - A.dt * (Qf[r][0] - fv.x * Sc[r]);
-            out[1] = fv.y - A.dt * (Qf[r][1] - fv.y * Sc[r]);
-            if (valid) *reinterpret_cast<double2*>(fto + r * rowstride) = make_double2(out[0], out[1]);
-        }
-        if (valid) {
-            s0 += out[0];
-            s1 += v1 * out[0];
-            s2 += v2v * out[0];
-            if constexpr (D == 3) s3 += v3v * out[0];
-            sE += vv * out[0];
-            if constexpr (NV == 2) sE += out[1];
-            amax = fmax(amax, -Sc[r]);
-        }
-    }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    s3 = warp_sum(s3);
-    sE = warp_sum(sE);
-    amax = warp_max(amax);
-    if (lane == 0) {
-        double* pp = A.partials + ((int64_t)p * A.nwpp + w) * kPM;
-        pp[0] = s0;
-        pp[1] = s1;
-        pp[2] = s2;
-        if constexpr (D == 3) {
-            pp[3] = s3;
-            pp[4] = sE;
-        } else {
-            pp[3] = sE;
-            pp[4] = 0.0;
-        }
-        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
-    }
-}
-
-// Union of the neighbour lists of each group of kGroup consecutive particles of `order`:
-// bitonic sort of the concatenated lists in shared memory, then drop duplicates.
-__global__ void __launch_bounds__(256) k_group_union(const int32_t* __restrict__ order, int64_t n_int,
-                                                     const int64_t* __restrict__ nb_off,
-                                                     const int32_t* __restrict__ nb_idx, int ucap,
-                                                     int32_t* __restrict__ gU, int32_t* __restrict__ gUlen,
-                                                     uint8_t* __restrict__ gCnt, uint16_t* __restrict__ upos) {
-    extern __shared__ int32_t sa[];                         // [ucap] sort buffer, then [ucap] union
-    int32_t* su = sa + ucap;
-    __shared__ int s_len[kGroup + 1];
-    __shared__ int wsum[8];
-    const int group = blockIdx.x;
-    if (threadIdx.x == 0) {
-        int tot = 0;
-        for (int g = 0; g < kGroup; ++g) {
-            const int64_t pos = (int64_t)group * kGroup + g;
-            s_len[g] = tot;
-            if (pos < n_int) {
-                const int p = order[pos];
-                tot += (int)(nb_off[p + 1] - nb_off[p]);
-            }
-        }
-        s_len[kGroup] = tot;
-    }
-    __syncthreads();
-    const int tot = s_len[kGroup];
-    int n2 = 1;
-    while (n2 < tot) n2 <<= 1;
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) sa[i] = INT_MAX;
-    __syncthreads();
-    for (int g = 0; g < kGroup; ++g) {
-        const int64_t pos = (int64_t)group * kGroup + g;
-        if (pos >= n_int) break;
-        const int p = order[pos];
-        const int64_t off = nb_off[p];
-        const int m = (int)(nb_off[p + 1] - off);
-        for (int i = threadIdx.x; i < m; i += blockDim.x) sa[s_len[g] + i] = nb_idx[off + i];
-    }
-    __syncthreads();
-    for (int k = 2; k <= n2; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const int a = sa[i], b = sa[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        sa[i] = b;
-                        sa[ixj] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    // compaction of first occurrences, in order: per-thread contiguous chunk + block scan
-    const int per = (n2 + blockDim.x - 1) / blockDim.x;
-    const int b0 = threadIdx.x * per, b1 = min(n2, b0 + per);
-    int cnt = 0;
-    for (int i = b0; i < b1; ++i) cnt += (sa[i] != INT_MAX && (i == 0 || sa[i] != sa[i - 1]));
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int v = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-    }
-    if (lane == 31) wsum[wid] = v;
-    __syncthreads();
-    int base = v - cnt;
-    for (int q = 0; q < wid; ++q) base += wsum[q];
-    int32_t* out = gU + (int64_t)group * ucap;
-    uint8_t* cnt_out = gCnt + (int64_t)group * ucap;
-    for (int i = b0; i < b1; ++i)
-        if (sa[i] != INT_MAX && (i == 0 || sa[i] != sa[i - 1])) {
-            int run = 1;                                    // users of this member (<= kGroup)
-            while (i + run < n2 && sa[i + run] == sa[i]) ++run;
-            su[base] = sa[i];
-            out[base] = sa[i];
-            cnt_out[base] = (uint8_t)run;
-            ++base;
-        }
-    __shared__ int s_ulen;
-    if (threadIdx.x == blockDim.x - 1) {
-        gUlen[group] = base;
-        s_ulen = base;
-    }
-    __syncthreads();
-    const int ulen = s_ulen;
-    // position of every neighbour entry of the group's particles inside the union (binary search)
-    for (int g = 0; g < kGroup; ++g) {
-        const int64_t pos = (int64_t)group * kGroup + g;
-        if (pos >= n_int) break;
-        const int p = order[pos];
-        const int64_t off = nb_off[p];
-        const int m = (int)(nb_off[p + 1] - off);
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
-            const int v = nb_idx[off + i];
-            int lo = 0, hi = ulen - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (su[mid] < v) lo = mid + 1;
-                else hi = mid;
-            }
-            upos[off + i] = (uint16_t)lo;
-        }
-    }
-}
-
-// ============================================================================
-// Warp-specialised transport: the block's last warp is a TMA producer for the other
-// kWsConsumers warps (one particle each).  Producer lane c walks consumer c's neighbour
-// list, waits for the consumer to release a ring stage (empty[c][s]) and refills it
-// (box + pair record on full[c][s]).  Consumers only wait on full, apply the neighbour and
-// arrive on empty -- no refill issue, no warp-wide issue path in the hot loop.
-// ============================================================================
-constexpr int kWsConsumers = 8;
-constexpr int kWsThreads = (kWsConsumers + 4) * 32;   // two consumer warpgroups + one producer warpgroup
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <int D, int R, int NST>
-__global__ void __launch_bounds__(kWsThreads, 1) k_transport_ws(const __grid_constant__ CUtensorMap tmap,
-                                                                             const TArgs A) {
-    using St = Stage<D, R>;
-    constexpr int NV = St::NV;
-    constexpr int PD = St::PD;
-    constexpr int ROW = St::ROW;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kWsConsumers * NST * St::BYTES);
-    uint64_t* empty = full + kWsConsumers * NST;
+    __syncwarp();
     const int w = blockIdx.y;
+    const int64_t grp = (int64_t)blockIdx.x * WPB + wib;
+    if (2 * grp >= A.n_int) return;                       // warp-uniform
     const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
-    const int k1s = chunk * R;
-    if (threadIdx.x == 0) {
-        for (int q = 0; q < kWsConsumers * NST; ++q) {
-            mbar_init(full + q, 1);
-            mbar_init(empty + q, 1);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-
-    if (wib >= kWsConsumers) {                              // ---------------- producer warpgroup
-        // registers move from the producer warpgroup to the consumers (setmaxnreg)
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
-        const int c = lane;
-        if (wib != kWsConsumers || c >= kWsConsumers) return;
-        const int64_t pos = (int64_t)blockIdx.x * kWsConsumers + c;
-        if (pos >= A.n_int) return;
-        const int p = A.order[pos];
-        const int64_t off = A.nb_off[p];
-        const int m = (int)(A.nb_off[p + 1] - off);
-        unsigned char* ring = smem_raw + (size_t)c * NST * St::BYTES;
-        for (int e = 0; e < m; ++e) {
-            const int s = e % NST;
-            const int jn = __ldg(A.nb_idx + off + e);
-            if (e >= NST) mbar_wait(empty + c * NST + s, (uint32_t)((e / NST) - 1) & 1u);
-            unsigned char* st = ring + s * St::BYTES;
-            mbar_expect_tx(full + c * NST + s, St::F_BYTES + St::P_BYTES);
-            tma_load_3d(st, &tmap, cg * ROW, k1s, jn, full + c * NST + s);
-            bulk_load(st + St::F_BYTES, A.P + (off + e) * PD, St::P_BYTES, full + c * NST + s);
-        }
-        return;
-    }
-    // ---------------------------------------------------------------- consumer warps
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
-    const int64_t pos = (int64_t)blockIdx.x * kWsConsumers + wib;
-    if (pos >= A.n_int) return;
-    const int p = A.order[pos];
     const int col = cg * 32 + lane;
     const bool valid = col < A.ncol;
+    const int k1s = chunk * R;
     const int colc = valid ? col : 0;
     const int gc = A.c0 + colc;
-    const int64_t off = A.nb_off[p];
-    const int m = (int)(A.nb_off[p + 1] - off);
-    const unsigned char* ring = smem_raw + (size_t)wib * NST * St::BYTES;
-    double Wp[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) Wp[a] = A.W[(int64_t)p * D + a];
-    double c0v[D];
-    c0v[0] = axis_node(A.vmax, A.dv, k1s) - Wp[0];
-    if constexpr (D == 3) {
-        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-        c0v[1] = axis_node(A.vmax, A.dv, k2) - Wp[1];
-        c0v[2] = axis_node(A.vmax, A.dv, k3) - Wp[2];
-    } else {
-        c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
+    const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+    const int pA = A.order[2 * grp];
+    const int pB = 2 * grp + 1 < A.n_int ? A.order[2 * grp + 1] : -1;
+    const double* PA = A.P + A.nb_off[pA] * PD;
+    const double* PB = A.P + (pB >= 0 ? A.nb_off[pB] : 0) * PD;
+    double c1A, c2A, c3A, c1B, c2B, c3B;                  // c = v(k1s, col) - W (c1 in units of dv)
+    {
+        const double v1 = axis_node(A.vmax, A.dv, k1s), v2 = axis_node(A.vmax, A.dv, k2),
+                     v3 = axis_node(A.vmax, A.dv, k3);
+        const double* Wa = A.W + (int64_t)pA * 3;
+        const double* Wb = A.W + (int64_t)(pB >= 0 ? pB : pA) * 3;
+        c1A = (v1 - Wa[0]) / A.dv;
+        c2A = v2 - Wa[1];
+        c3A = v3 - Wa[2];
+        c1B = (v1 - Wb[0]) / A.dv;
+        c2B = v2 - Wb[1];
+        c3B = v3 - Wb[2];
     }
-    const double c1dv = c0v[0] / A.dv;
-    double Qf[R][NV], Sc[R];
+    const int nboth = A.gUlen[4 * grp], nA = A.gUlen[4 * grp + 1], nBo = A.gUlen[4 * grp + 2];
+    const int segA = nboth, segB = nboth + nA, ulen = segB + nBo;
+    const int2* ul = reinterpret_cast<const int2*>(A.gU) + grp * A.ucap;
+    int2 nbA = lane < ulen ? ul[lane] : make_int2(0, 0);   // union entries, 32 per register batch
+    int2 nbB = 32 + lane < ulen ? ul[32 + lane] : make_int2(0, 0);
+
+    auto issue = [&](int t, int j, int ee) {               // one elected lane: stage of member t
+        const int s = t % NST;
+        unsigned char* st = ring + s * St::BYTES;
+        const bool hasA = t < segB, hasB = t < segA || t >= segB;
+        mbar_expect_tx(bars + s, St::F_BYTES + (uint32_t)(hasA + hasB) * St::P_BYTES);
+        tma_load_3d(st, &tmap, cg * ROW, k1s, j, bars + s);
+        if (hasA) bulk_load(st + St::F_BYTES, PA + (int64_t)(ee & 0xffff) * PD, St::P_BYTES, bars + s);
+        if (hasB) bulk_load(st + St::F_BYTES + St::P_BYTES, PB + (int64_t)(ee >> 16) * PD, St::P_BYTES, bars + s);
+    };
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        Sc[r] = 0.0;
-#pragma unroll
-        for (int q = 0; q < NV; ++q) Qf[r][q] = 0.0;
+    for (int s = 0; s < NST; ++s) {
+        const int j = __shfl_sync(0xffffffffu, nbA.x, s), ee = __shfl_sync(0xffffffffu, nbA.y, s);
+        if (s < ulen && elect_one()) issue(s, j, ee);
     }
-    for (int e = 0; e < m; ++e) {
-        const int s = e % NST;
-        const unsigned char* stb = ring + s * St::BYTES;
-        mbar_wait(full + wib * NST + s, (uint32_t)(e / NST) & 1u);
-        const double* ps = reinterpret_cast<const double*>(stb + St::F_BYTES);
-        double pv[PD];
+
+    double QA[R], SA[R], QB[R], SB[R];
 #pragma unroll
-        for (int q = 0; q < PD; ++q) pv[q] = ps[q];
-        double y[D], dy[D], Lc, dL;
-        pair_coeffs<D>(pv, c0v, c1dv, A.dv, y, dy, Lc, dL);
-        const double* st = reinterpret_cast<const double*>(stb) + lane * NV;
+    for (int r = 0; r < R; ++r) QA[r] = SA[r] = QB[r] = SB[r] = 0.0;
+    for (int e = 0; e < ulen; ++e) {
+        const unsigned char* stb = ring + (e % NST) * St::BYTES;
+        mbar_wait(bars + e % NST, (uint32_t)(e / NST) & 1u);
+        const double* st = reinterpret_cast<const double*>(stb) + lane;
+        const double* psA = reinterpret_cast<const double*>(stb + St::F_BYTES);
+        const double* psB = reinterpret_cast<const double*>(stb + St::F_BYTES + St::P_BYTES);
+        double yA[3], dyA[3], yB[3], dyB[3];
+        if (e < segA) {                                    // member of both lists: one fused row loop
+            pair_y(psA, c1A, c2A, c3A, yA, dyA);
+            pair_y(psB, c1B, c2B, c3B, yB, dyB);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const double rr = (double)r;
-            const double Lr = fma(rr, dL, Lc);
-            double C;
-            if constexpr (D == 3) {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                const double yb = fma(rr, dy[2], y[2]);
-                C = (Lr - fabs(yn)) - (fabs(yt) + fabs(yb));
-            } else {
-                const double yn = fma(rr, dy[0], y[0]);
-                const double yt = fma(rr, dy[1], y[1]);
-                C = (Lr - fabs(yn)) - fabs(yt);
+            for (int r = 0; r < R; ++r) {
+                const double fj = st[r * ROW];
+                const double CA = neg_part(fma((double)r, dyA[0], yA[0])) + neg_part(fma((double)r, dyA[1], yA[1])) +
+                                  neg_part(fma((double)r, dyA[2], yA[2]));
+                const double CB = neg_part(fma((double)r, dyB[0], yB[0])) + neg_part(fma((double)r, dyB[1], yB[1])) +
+                                  neg_part(fma((double)r, dyB[2], yB[2]));
+                QA[r] = fma(CA, fj, QA[r]);
+                SA[r] += CA;
+                QB[r] = fma(CB, fj, QB[r]);
+                SB[r] += CB;
             }
-            if constexpr (NV == 1) {
-                Qf[r][0] = fma(C, st[r * ROW], Qf[r][0]);
-            } else {
-                const double2 v = *reinterpret_cast<const double2*>(st + r * ROW);
-                Qf[r][0] = fma(C, v.x, Qf[r][0]);
-                Qf[r][1] = fma(C, v.y, Qf[r][1]);
-            }
-            Sc[r] += C;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + wib * NST + s);  // stage s free for the producer
-    }
-    // epilogue (as k_transport)
-    const int64_t rowstride = (int64_t)A.ncs * NV;
-    const int64_t lane_off = (int64_t)k1s * rowstride + (int64_t)colc * NV;
-    const double* fi = A.f + (int64_t)p * A.n1 * rowstride + lane_off;
-    double* fto = A.ft + (int64_t)p * A.n1 * rowstride + lane_off;
-    double v2v = 0.0, v3v = 0.0;
-    if constexpr (D == 3) {
-        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-        v2v = axis_node(A.vmax, A.dv, k2);
-        v3v = axis_node(A.vmax, A.dv, k3);
-    } else {
-        v2v = axis_node(A.vmax, A.dv, gc);
-    }
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, sE = 0.0, amax = 0.0;
+        } else if (e < segB) {                             // A only
+            pair_y(psA, c1A, c2A, c3A, yA, dyA);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        if (k1s + r >= A.n1) break;
-        const double v1 = axis_node(A.vmax, A.dv, k1s + r);
-        const double vv = (D == 3) ? v1 * v1 + v2v * v2v + v3v * v3v : v1 * v1 + v2v * v2v;
-        double out[NV];
-        if constexpr (NV == 1) {
-            const double fv = __ldg(fi + r * rowstride);
-            out[0] = fv - A.dt * (Qf[r][0] - fv * Sc[r]);
-            if (valid) fto[r * rowstride] = out[0];
-        } else {
-            const double2 fv = __ldg(reinterpret_cast<const double2*>(fi + r * rowstride));
-            out[0] = fv.x - A.dt * (Qf[r][0] - fv.x * Sc[r]);
-            out[1] = fv.y - A.dt * (Qf[r][1] - fv.y * Sc[r]);
-            if (valid) *reinterpret_cast<double2*>(fto + r * rowstride) = make_double2(out[0], out[1]);
+            for (int r = 0; r < R; ++r) {
+                const double CA = neg_part(fma((double)r, dyA[0], yA[0])) + neg_part(fma((double)r, dyA[1], yA[1])) +
+                                  neg_part(fma((double)r, dyA[2], yA[2]));
+                QA[r] = fma(CA, st[r * ROW], QA[r]);
+                SA[r] += CA;
+            }
+        } else {                                           // B only
+            pair_y(psB, c1B, c2B, c3B, yB, dyB);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double CB = neg_part(fma((double)r, dyB[0], yB[0])) + neg_part(fma((double)r, dyB[1], yB[1])) +
+                                  neg_part(fma((double)r, dyB[2], yB[2]));
+                QB[r] = fma(CB, st[r * ROW], QB[r]);
+                SB[r] += CB;
+            }
         }
-        if (valid) {
-            s0 += out[0];
-            s1 += v1 * out[0];
-            s2 += v2v * out[0];
-            if constexpr (D == 3) s3 += v3v * out[0];
-            sE += vv * out[0];
-            if constexpr (NV == 2) sE += out[1];
-            amax = fmax(amax, -Sc[r]);
+        // refill the consumed stage with member e + NST
+        const int t = e + NST;
+        if ((t & 31) == 0) {                               // warp-uniform batch rotation
+            nbA = nbB;
+            nbB = t + 32 + lane < ulen ? ul[t + 32 + lane] : make_int2(0, 0);
         }
+        const int j = __shfl_sync(0xffffffffu, nbA.x, t & 31), ee = __shfl_sync(0xffffffffu, nbA.y, t & 31);
+        __syncwarp();                                      // every lane has consumed the stage
+        if (t < ulen && elect_one()) issue(t, j, ee);
     }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    s3 = warp_sum(s3);
-    sE = warp_sum(sE);
-    amax = warp_max(amax);
+    const double Sa[1] = {0.0};
+    double (&QAv)[R][1] = *reinterpret_cast<double (*)[R][1]>(&QA);
+    double (&QBv)[R][1] = *reinterpret_cast<double (*)[R][1]>(&QB);
+    transport_epilogue<3, R, false>(A, pA, w, k1s, colc, gc, valid, QAv, SA, Sa);
+    if (pB >= 0) transport_epilogue<3, R, false>(A, pB, w, k1s, colc, gc, valid, QBv, SB, Sa);
+}
+
+// Union of the neighbour lists of each particle pair (A, B) = order[2g], order[2g+1], in three
+// segments (both / A only / B only, ascending j in each) with the CSR positions of j in A's and
+// B's lists.  One warp per pair: membership by binary search in the other (ascending) list,
+// positions by ballot prefix counts.
+__global__ void __launch_bounds__(128) k_pair_union(const int32_t* __restrict__ order, int64_t n_int,
+                                                    const int64_t* __restrict__ nb_off,
+                                                    const int32_t* __restrict__ nb_idx, int ucap,
+                                                    int2* __restrict__ gU, int32_t* __restrict__ gUlen) {
+    const int lane = threadIdx.x & 31;
+    const int64_t grp = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (2 * grp >= n_int) return;
+    const int pA = order[2 * grp];
+    const int pB = 2 * grp + 1 < n_int ? order[2 * grp + 1] : -1;
+    const int32_t* LA = nb_idx + nb_off[pA];
+    const int mA = (int)(nb_off[pA + 1] - nb_off[pA]);
+    const int32_t* LB = pB >= 0 ? nb_idx + nb_off[pB] : nullptr;
+    const int mB = pB >= 0 ? (int)(nb_off[pB + 1] - nb_off[pB]) : 0;
+    auto find = [](const int32_t* L, int m, int v) {       // position of v in ascending L, or -1
+        int lo = 0, hi = m;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (L[mid] < v) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo < m && L[lo] == v ? lo : -1;
+    };
+    int nboth = 0;
+    for (int b = 0; b < mA; b += 32) {                     // pass 1: size of the intersection
+        const int i = b + lane;
+        const bool hit = i < mA && find(LB, mB, LA[i]) >= 0;
+        nboth += __popc(__ballot_sync(0xffffffffu, hit));
+    }
+    int2* out = gU + grp * ucap;
+    const unsigned below = (1u << lane) - 1u;
+    int wb = 0, wa = nboth;
+    for (int b = 0; b < mA; b += 32) {                     // pass 2: both + A only
+        const int i = b + lane;
+        const int jb = i < mA ? find(LB, mB, LA[i]) : -1;
+        const unsigned hb = __ballot_sync(0xffffffffu, i < mA && jb >= 0);
+        const unsigned ha = __ballot_sync(0xffffffffu, i < mA && jb < 0);
+        if (i < mA) {
+            if (jb >= 0) out[wb + __popc(hb & below)] = make_int2(LA[i], i | (jb << 16));
+            else out[wa + __popc(ha & below)] = make_int2(LA[i], i);
+        }
+        wb += __popc(hb);
+        wa += __popc(ha);
+    }
+    int wo = mA;                                           // B only after both + A only
+    for (int b = 0; b < mB; b += 32) {
+        const int i = b + lane;
+        const bool only = i < mB && find(LA, mA, LB[i]) < 0;
+        const unsigned ho = __ballot_sync(0xffffffffu, only);
+        if (only) out[wo + __popc(ho & below)] = make_int2(LB[i], i << 16);
+        wo += __popc(ho);
+    }
     if (lane == 0) {
-        double* pp = A.partials + ((int64_t)p * A.nwpp + w) * kPM;
-        pp[0] = s0;
-        pp[1] = s1;
-        pp[2] = s2;
-        if constexpr (D == 3) {
-            pp[3] = s3;
-            pp[4] = sE;
-        } else {
-            pp[3] = sE;
-            pp[4] = 0.0;
-        }
-        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+        gUlen[4 * grp] = nboth;
+        gUlen[4 * grp + 1] = mA - nboth;
+        gUlen[4 * grp + 2] = wo - mA;
+        gUlen[4 * grp + 3] = 0;
     }
 }
 
-template <int D, int R>
-void launch_ws_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int B = Stage<D, R>::BYTES;
-    constexpr int NST = []() {
-        int n = 2;
-        while (n < 8 && (size_t)kWsConsumers * (n + 1) * B + 2 * kWsConsumers * (n + 1) * 8 <= 220 * 1024) ++n;
-        return n;
-    }();
-    constexpr size_t smem = (size_t)kWsConsumers * NST * B + 2 * kWsConsumers * NST * 8;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_transport_ws<D, R, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
-    const unsigned gx = (unsigned)((a.n_int + kWsConsumers - 1) / kWsConsumers);
-    k_transport_ws<D, R, NST><<<dim3(gx, (unsigned)a.nwpp), kWsThreads, smem, s>>>(tm, a);
-}
-
-template <int D>
-void dispatch_ws(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    if constexpr (D == 3) {
-        switch (R) {
-            case 25: launch_ws_one<D, 25>(tm, a, s); return;
-            case 21: launch_ws_one<D, 21>(tm, a, s); return;
-            case 17: launch_ws_one<D, 17>(tm, a, s); return;
-            default: break;
-        }
-    }
-    switch (R) {
-        case 13: launch_ws_one<D, 13>(tm, a, s); break;
-        case 11: launch_ws_one<D, 11>(tm, a, s); break;
-        case 9: launch_ws_one<D, 9>(tm, a, s); break;
-        case 7: launch_ws_one<D, 7>(tm, a, s); break;
-        case 5: launch_ws_one<D, 5>(tm, a, s); break;
-        case 3: launch_ws_one<D, 3>(tm, a, s); break;
-        default: launch_ws_one<D, 1>(tm, a, s); break;
-    }
-}
-
-template <int D, int R, int WPB, bool SG>
+template <int D, int R, int WPB, bool SG, int MINB = 1>
 constexpr int stages_for() {
     // ring depth: keep NST-1 neighbour boxes in flight; bounded by 227 KB of shared memory
-    // (sized for 8 resident warps per SM: blocks of WPB warps, 8 / WPB blocks per SM)
-    constexpr int blocks = WPB >= 8 ? 1 : 8 / WPB;
+    // (sized for max(8, MINB WPB) resident warps per SM: blocks of WPB warps)
+    constexpr int blocks0 = WPB >= 8 ? 1 : 8 / WPB;
+    constexpr int blocks = MINB > blocks0 ? MINB : blocks0;
     constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R, SG>::BYTES);
     return n > 8 ? 8 : (n < 2 ? 2 : n);
 }
 
-template <int D, int R, int WPB, bool SG = false>
+template <int D, int R, int WPB, bool SG = false, int MINB = 1>
 void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int NST = stages_for<D, R, WPB, SG>();
+    constexpr int NST = stages_for<D, R, WPB, SG, MINB>();
     constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG>::BYTES + WPB * NST * 8;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         configured = true;
     }
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
-    k_transport<D, R, NST, WPB, SG><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
+    k_transport<D, R, NST, WPB, SG, MINB><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
 }
 
 template <int D, int R>
 void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     if (a.signed_n) return launch_one<D, R, kDefaultWarps, true>(tm, a, s);   // second-order WLS
-    if constexpr (D == 3 && (R == 25 || R == 17 || R == 13 || R == 9)) {
-        if (wpb == 12) return launch_one<D, R, 12>(tm, a, s);
-        if (wpb == 16) return launch_one<D, R, 16>(tm, a, s);
-        if (wpb == 4) return launch_one<D, R, 4>(tm, a, s);
+    if constexpr (D == 3 && (R == 25 || R == 13)) {
+        if (wpb == 8) return launch_one<D, R, 8>(tm, a, s);
         if (wpb == 2) return launch_one<D, R, 2>(tm, a, s);
+        if (wpb == 43) return launch_one<D, R, 4, false, 3>(tm, a, s);   // 12 resident warps per SM
     }
     launch_one<D, R, kDefaultWarps>(tm, a, s);
 }
@@ -1018,7 +690,6 @@ void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_
     if constexpr (D == 3) {
         switch (R) {
             case 25: launch_wpb<D, 25>(wpb, tm, a, s); return;
-            case 21: launch_wpb<D, 21>(wpb, tm, a, s); return;
             case 17: launch_wpb<D, 17>(wpb, tm, a, s); return;
             default: break;
         }
@@ -1034,81 +705,83 @@ void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_
     }
 }
 
-template <int D, int R>
-void launch_grp_one(const CUtensorMap& tm, const TArgs& a, int n_groups, cudaStream_t s) {
-    // ring depth from the shared-memory budget (one block per SM), 4..16 stages
-    constexpr int F = GStage<D, R>::F_BYTES;
-    constexpr int NST = []() {
-        int n = 4;
-        while (n < kMaxGrpStages && grp_smem_bytes<D, R, 16>(0) - 16 * F + (n + 1) * F + 16384 <= 225 * 1024) ++n;
-        return n;
-    }();
-    const size_t smem = grp_smem_bytes<D, R, NST>(a.ucap);
+template <int R>
+void launch_pair_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
+    constexpr int WPB = kDefaultWarps;
+    constexpr int MINB = R <= 13 ? 3 : 2;                    // 12 (8) resident warps per SM
+    constexpr int B = PStage<R>::BYTES;
+    constexpr int NST0 = (220 * 1024) / (MINB * WPB * B);
+    constexpr int NST = NST0 > 8 ? 8 : (NST0 < 2 ? 2 : NST0);
+    constexpr size_t smem = (size_t)WPB * NST * B + WPB * NST * 8;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_transport_grp<D, R, NST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_transport_pair<R, NST, WPB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
         configured = true;
     }
-    k_transport_grp<D, R, NST><<<dim3((unsigned)n_groups, (unsigned)a.nwpp), kGroup * 32, smem, s>>>(tm, a);
+    const int64_t ng = (a.n_int + 1) / 2;
+    const unsigned gx = (unsigned)((ng + WPB - 1) / WPB);
+    k_transport_pair<R, NST, WPB, MINB><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
 }
 
-template <int D>
-void dispatch_grp(int R, const CUtensorMap& tm, const TArgs& a, int n_groups, cudaStream_t s) {
-    if constexpr (D == 3) {
-        switch (R) {
-            case 25: launch_grp_one<D, 25>(tm, a, n_groups, s); return;
-            case 21: launch_grp_one<D, 21>(tm, a, n_groups, s); return;
-            case 17: launch_grp_one<D, 17>(tm, a, n_groups, s); return;
-            default: break;
-        }
-    }
+constexpr int kPairR[] = {17, 13, 9, 5};   // rows per lane instantiated for particle-pair warps
+
+void dispatch_pair(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     switch (R) {
-        case 13: launch_grp_one<D, 13>(tm, a, n_groups, s); break;
-        case 11: launch_grp_one<D, 11>(tm, a, n_groups, s); break;
-        case 9: launch_grp_one<D, 9>(tm, a, n_groups, s); break;
-        case 7: launch_grp_one<D, 7>(tm, a, n_groups, s); break;
-        case 5: launch_grp_one<D, 5>(tm, a, n_groups, s); break;
-        case 3: launch_grp_one<D, 3>(tm, a, n_groups, s); break;
-        default: launch_grp_one<D, 1>(tm, a, n_groups, s); break;
+        case 17: return launch_pair_one<17>(tm, a, s);
+        case 13: return launch_pair_one<13>(tm, a, s);
+        case 9: return launch_pair_one<9>(tm, a, s);
+        default: return launch_pair_one<5>(tm, a, s);
     }
 }
 
-constexpr int kRChoices3[] = {25, 21, 17, 13, 11, 9, 7, 5, 3, 1};
+constexpr int kRChoices3[] = {25, 17, 13, 11, 9, 7, 5, 3, 1};
 constexpr int kRChoices2[] = {13, 11, 9, 7, 5, 3, 1};
+
+// the R of `choices` with the fewest padded rows (ceil(n1/R) R), ties to the larger R
+template <size_t K>
+int fewest_padded(const int (&choices)[K], int n1) {
+    int best = choices[0], pad = (n1 + best - 1) / best * best;
+    for (int R : choices) {
+        const int p = (n1 + R - 1) / R * R;
+        if (p < pad) best = R, pad = p;
+    }
+    return best;
+}
+
+template <size_t K>
+bool listed(const int (&choices)[K], int R) {
+    for (int x : choices)
+        if (x == R) return true;
+    return false;
+}
 
 }  // namespace
 
-int group_size() { return kGroup; }
-
-void launch_group_union(bgk_ctx* c, cudaStream_t s) {
-    if (!c->grouped || c->N_int == 0) return;
-    const int n_groups = (int)((c->N_int + kGroup - 1) / kGroup);
-    k_group_union<<<n_groups, 256, 2 * sizeof(int32_t) * c->ucap, s>>>(c->g.order, c->N_int, c->g.nb_off,
-                                                                        c->g.nb_idx, c->ucap, c->gU, c->gUlen,
-                                                                        c->gCnt, c->upos);
+// particles per transport warp (3D first-order only): BGK_TRANSPORT_NP (1 or 2), default kDefaultNP
+int transport_particles_per_warp(int d, int wls_order) {
+    if (d != 3 || wls_order != 1) return 1;
+    int np = kDefaultNP;
+    if (const char* e = getenv("BGK_TRANSPORT_NP")) np = atoi(e);
+    return np == 2 ? 2 : 1;
 }
 
-// rows per thread: the largest divisor of n1 among the instantiated R (2D keeps three
-// accumulators per row, so it stops at 13)
-int transport_rows_per_thread(int d, int n1) {
-    if (const char* e = getenv("BGK_TRANSPORT_R")) {    // tuning knob: any instantiated R (ragged chunks OK)
-        const int r = atoi(e);
-        if (d == 3) {
-            for (int R : kRChoices3)
-                if (R == r) return R;
-        } else {
-            for (int R : kRChoices2)
-                if (R == r) return R;
-        }
-    }
-    if (d == 3) {
-        for (int R : kRChoices3)
-            if (n1 % R == 0) return R;
-    } else {
-        for (int R : kRChoices2)
-            if (n1 % R == 0) return R;
-    }
-    return 1;
+void launch_group_union(bgk_ctx* c, cudaStream_t s) {
+    if (c->np != 2 || c->N_int == 0) return;
+    const int64_t ng = (c->N_int + 1) / 2;
+    k_pair_union<<<(unsigned)((ng + 3) / 4), 128, 0, s>>>(c->g.order, c->N_int, c->g.nb_off, c->g.nb_idx, c->ucap,
+                                                          reinterpret_cast<int2*>(c->gU), c->gUlen);
+}
+
+// rows per lane: BGK_TRANSPORT_R if instantiated for the mapping, else the instantiated R with
+// the fewest padded rows (pair warps: R is bounded by the register budget, 4 accumulators per
+// row; 2D keeps three accumulators per row, so it stops at 13)
+int transport_rows_per_thread(int d, int n1, int np) {
+    const char* e = getenv("BGK_TRANSPORT_R");
+    const int want = e ? atoi(e) : 0;
+    if (np == 2) return listed(kPairR, want) ? want : fewest_padded(kPairR, n1);
+    if (d == 3) return listed(kRChoices3, want) ? want : fewest_padded(kRChoices3, n1);
+    return listed(kRChoices2, want) ? want : fewest_padded(kRChoices2, n1);
 }
 
 // TMA descriptors: f[b] viewed as a 3D fp64 tensor {ncs*nv (fastest), n1, N}; box {32*nv, R, 1}.
@@ -1148,7 +821,6 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.P = c->g.P;
     a.partials = c->partials;
     a.stab = c->stab;
-    a.work = c->work;
     a.n_int = c->N_int;
     a.n1 = c->n1;
     a.ncol = c->ncol;
@@ -1161,28 +833,12 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.dt = c->cfg.dt;
     a.gU = c->gU;
     a.gUlen = c->gUlen;
-    a.gCnt = c->gCnt;
-    a.upos = c->upos;
     a.ucap = c->ucap;
-    const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
-    static const int variant = [] {     // 0: per-warp ring, 1: warp-specialised producer (tuning knob)
-        const char* e = getenv("BGK_TRANSPORT_WS");
-        return e ? atoi(e) : 0;
-    }();
     a.signed_n = c->wls_order == 2;
-    if (variant == 1 && !c->grouped && !a.signed_n) {
-        if (c->d == 3) dispatch_ws<3>(c->R, tm, a, s);
-        else dispatch_ws<2>(c->R, tm, a, s);
-        return;
-    }
-    if (c->grouped && !a.signed_n) {
-        const int n_groups = (int)((c->N_int + kGroup - 1) / kGroup);
-        if (c->d == 3) dispatch_grp<3>(c->R, tm, a, n_groups, s);
-        else dispatch_grp<2>(c->R, tm, a, n_groups, s);
-        return;
-    }
+    const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
+    if (c->np == 2) return dispatch_pair(c->R, tm, a, s);
     static const int wpb = [] {
-        const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (4, 8, 12, 16); default 8
+        const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (2, 4, 8); default kDefaultWarps
         return e ? atoi(e) : kDefaultWarps;
     }();
     if (c->d == 3) dispatch<3>(c->R, wpb, tm, a, s);

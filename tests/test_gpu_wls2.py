@@ -58,7 +58,16 @@ def test_wls2_coefficients(torch_cuda, cfg):
     erow = np.repeat(inter, np.diff(off))
     assert rel(S[inter], rS[inter]) < 1e-11
     assert rel(rot[erow], rrot[erow]) < 1e-11
-    assert np.abs(fr[erow] - rfr[erow]).max() < 1e-14
+    # The oracle's theta = arccos(dz/r) carries an error u/sin(theta) near the pole
+    # (d arccos(c)/dc = -1/sin(theta)); jittered 3D clouds have pairs with sin(theta) ~ 1e-3.
+    # Tolerance per pair: 1e-14 + 8u/sin(theta).
+    rows = np.repeat(np.arange(len(x)), np.diff(off))
+    dvec = x[idx] - x[rows]
+    r = np.linalg.norm(dvec, axis=1)
+    sin_t = np.hypot(dvec[:, 0], dvec[:, 1]) / r if cfg.dims == 3 else np.ones_like(r)
+    tol = 1e-14 + 8 * np.finfo(float).eps / np.maximum(sin_t, 1e-300)
+    ferr = np.abs(fr - rfr).reshape(len(r), -1).max(axis=1)
+    assert np.all(ferr[erow] <= tol[erow])
     if cfg.jitter > 0:
         assert (rrot[erow, 0] < 0).any()          # the signed transport path is exercised
 
