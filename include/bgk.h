@@ -65,7 +65,8 @@ typedef enum {
 
 typedef struct bgk_config {
     int32_t dims;        /* 2 = Chu-reduced 2D model (values g1, g2), 3 = full 3D model */
-    int32_t Nv;          /* velocity cells per axis, even, >= 2: Nv+1 nodes per axis */
+    int32_t Nv;          /* velocity cells per axis, 2..63: Nv+1 nodes per axis; odd Nv
+                          * (no zero node) as in the paper's Figs. 6-7 (Nv = 15) */
     double vmax;         /* velocity bound; > 0 */
     double L;            /* cavity edge [m] */
     double h;            /* neighbour radius [m], h = 3.1 dx */
@@ -101,7 +102,7 @@ bgk_status bgk_workspace_size(const bgk_config* cfg, int64_t N, size_t* bytes);
  *            particle; the transport velocity W^0 = U^0 (ALE) or 0 (fixed cloud).
  *   workspace, ws_bytes : caller-owned device memory of at least bgk_workspace_size bytes,
  *            16-byte aligned; it must outlive the context.
- * Errors: BGK_E_INVALID_ARG (dims not 2/3, odd or < 2 Nv, vmax <= 0, N < 1, bad column
+ * Errors: BGK_E_INVALID_ARG (dims not 2/3, Nv < 2 or > 63, vmax <= 0, N < 1, bad column
  * range, workspace too small), BGK_E_OUT_OF_DOMAIN.  Synchronises the stream. */
 bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* kind,
                           const double* macro0, int64_t N, void* workspace, size_t ws_bytes,

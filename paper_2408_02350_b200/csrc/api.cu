@@ -33,7 +33,7 @@ struct Carver {
 bool valid_cfg(const bgk_config* c, int64_t N) {
     if (!c || N < 1) return false;
     if (c->dims != 2 && c->dims != 3) return false;
-    if (c->Nv < 2 || (c->Nv & 1) || c->Nv + 1 > 64) return false;
+    if (c->Nv < 2 || c->Nv + 1 > 64) return false;   // odd Nv allowed: the paper's Figs. 6-7 use Nv = 15
     if (!(c->vmax > 0.0) || !(c->L > 0.0) || !(c->h > 0.0) || !(c->h2 > 0.0) || !(c->dt >= 0.0)) return false;
     if (!(c->R > 0.0) || !(c->kb > 0.0) || !(c->dmol > 0.0) || !(c->T_wall > 0.0) || !(c->alpha_w > 0.0)) return false;
     if (N > (int64_t)INT32_MAX) return false;

@@ -681,6 +681,7 @@ void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) 
         if (wpb == 8) return launch_one<D, R, 8>(tm, a, s);
         if (wpb == 2) return launch_one<D, R, 2>(tm, a, s);
         if (wpb == 43) return launch_one<D, R, 4, false, 3>(tm, a, s);   // 12 resident warps per SM
+        if (wpb == 44) return launch_one<D, R, 4, false, 4>(tm, a, s);   // 16 resident warps per SM
     }
     launch_one<D, R, kDefaultWarps>(tm, a, s);
 }
@@ -690,7 +691,9 @@ void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_
     if constexpr (D == 3) {
         switch (R) {
             case 25: launch_wpb<D, 25>(wpb, tm, a, s); return;
+            case 21: launch_wpb<D, 21>(wpb, tm, a, s); return;
             case 17: launch_wpb<D, 17>(wpb, tm, a, s); return;
+            case 15: launch_wpb<D, 15>(wpb, tm, a, s); return;
             default: break;
         }
     }
@@ -735,16 +738,19 @@ void dispatch_pair(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s)
     }
 }
 
-constexpr int kRChoices3[] = {25, 17, 13, 11, 9, 7, 5, 3, 1};
+constexpr int kRChoices3[] = {25, 21, 17, 15, 13, 11, 9, 7, 5, 3, 1};
 constexpr int kRChoices2[] = {13, 11, 9, 7, 5, 3, 1};
 
-// the R of `choices` with the fewest padded rows (ceil(n1/R) R), ties to the larger R
+// the R of `choices` with the lowest modelled cost ceil(n1/R) (R + kRowsOverhead): padded rows
+// plus the per-neighbour fixed cost (barrier, pair record, setup, refill ~ 5 rows of issue)
+constexpr int kRowsOverhead = 5;
 template <size_t K>
 int fewest_padded(const int (&choices)[K], int n1) {
-    int best = choices[0], pad = (n1 + best - 1) / best * best;
+    int best = choices[0];
+    long cost = (long)((n1 + best - 1) / best) * (best + kRowsOverhead);
     for (int R : choices) {
-        const int p = (n1 + R - 1) / R * R;
-        if (p < pad) best = R, pad = p;
+        const long c = (long)((n1 + R - 1) / R) * (R + kRowsOverhead);
+        if (c < cost) best = R, cost = c;
     }
     return best;
 }

@@ -136,7 +136,8 @@ def test_one_step(torch_cuda, cfg):
 
 
 @pytest.mark.parametrize("cfg", [bi.C1, bi.C1.replace(ale=0), bi.C1.replace(init="equilibrium"),
-                                 bi.C2, bi.C2.replace(Kn=0.1), bi.C2.replace(Kn=10.0), bi.C3, bi.C4])
+                                 bi.C2, bi.C2.replace(Kn=0.1), bi.C2.replace(Kn=10.0), bi.C3, bi.C4,
+                                 bi.C1.replace(Nv=11), bi.CavityConfig("C4odd", 3, 14, 15)])
 def test_ten_steps(torch_cuda, cfg):
     g, _ = gpu(cfg)
     g.step(10)

@@ -46,7 +46,7 @@ def test_grid_spec_example(oracle_lib):
 def test_grid_small_and_symmetric(oracle_lib):
     c = oracle_lib.make_cfg(cfg_of(2, 2, 1.0))
     assert list(oracle_lib.axis_nodes(c)) == [-1.0, 0.0, 1.0]
-    for Nv in (12, 16, 24, 32):
+    for Nv in (12, 15, 16, 23, 24, 32):
         c = oracle_lib.make_cfg(cfg_of(3, Nv, bi.VMAX_DEFAULT))
         v = oracle_lib.axis_nodes(c)
         np.testing.assert_allclose(v, -v[::-1], rtol=0, atol=1e-12)

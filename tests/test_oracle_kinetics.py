@@ -86,10 +86,12 @@ def test_maxwellian_one_axis_decay(oracle_lib):
         assert abs(M[k] / M[_center(12, 3)] - math.exp(-ax[j] ** 2 / (2 * bi.R_GAS * 270.0))) < 1e-15
 
 
-@pytest.mark.parametrize("d,Nv", [(3, 24), (2, 32)])
+@pytest.mark.parametrize("d,Nv", [(3, 24), (2, 32), (3, 23), (2, 31)])
 def test_moment_quadrature_wide_grid_exact(oracle_lib, d, Nv):
     """On a wide fine grid the rectangle rule of a Gaussian is exact to ~1e-15
-    (SURVEY appendix), so moments(M(rho,U,T)) returns (rho,U,T)."""
+    (SURVEY appendix), so moments(M(rho,U,T)) returns (rho,U,T).  Odd Nv (no zero node, the
+    paper's Nv = 15 grids of Figs. 6-7): the trapezoid/rectangle rule of a Gaussian
+    with dv < sigma is exact to exp(-2 pi^2 sigma^2/dv^2) for any grid offset."""
     c = oracle_lib.make_cfg(cfg(d, Nv, 8 * SIG + 1))
     rng = np.random.default_rng(d)
     for _ in range(5):
