@@ -67,6 +67,14 @@ class CavityConfig:
     lid: float = 1.0          # lid speed; 0 gives an all-stationary box
     wls_order: int = 1        # Taylor order of the WLS derivative (1: the paper's scheme; 2: P:368-369)
     L: float = L_CAVITY
+    # particle management (Z28): merge/fill pass at the
+    # start of every ALE step when manage = 1; r_merge <= 0 -> 0.2 dx, m_min <= 0 -> dims + 3
+    # (S:351-352); max_particles <= 0 -> N + N // 8 + 64 (capacity for inserted particles)
+    manage: int = 0
+    r_merge: float = 0.0
+    m_min: int = 0
+    max_particles: int = 0
+    defects: int = 0          # management workloads: `defects` close pairs + `defects` holes (lattice())
 
     @property
     def rho0(self) -> float:
@@ -92,6 +100,19 @@ class CavityConfig:
     @property
     def n_particles(self) -> int:
         return self.n_per_axis ** self.dims
+
+    @property
+    def merge_radius(self) -> float:
+        return self.r_merge if self.r_merge > 0 else 0.2 * self.dx
+
+    @property
+    def min_neighbors(self) -> int:
+        return self.m_min if self.m_min > 0 else self.dims + 3
+
+    @property
+    def capacity(self) -> int:
+        n = self.n_particles
+        return self.max_particles if self.max_particles > 0 else n + n // 8 + 64
 
     @property
     def U_lid(self) -> tuple:
@@ -141,7 +162,47 @@ def lattice(cfg: CavityConfig):
         J = rng.uniform(-cfg.jitter, cfg.jitter, size=(N, d)) * dx
         interior = kind == 0
         x[interior] += J[interior]
+    if cfg.defects > 0:
+        x, kind = _apply_defects(cfg, x, kind, idx)
     return x, kind
+
+
+def _apply_defects(cfg: CavityConfig, x, kind, idx):
+    """Management workload (seeded, PCG64(seed + 1)): `defects` interior particles are moved by
+    0.95 dx along +x towards their interior +x neighbour (a pair 0.05 dx apart, below the
+    default merge radius 0.2 dx), and `defects` holes are cut by removing a 2^d block of
+    interior particles (lattice positions only; the rest of the cloud is untouched)."""
+    n, d, dx = cfg.n_per_axis, cfg.dims, cfg.dx
+    rng = np.random.Generator(np.random.PCG64(cfg.seed + 1))
+    ijk = np.stack(idx, axis=1)                       # (N, d) lattice indices, x first
+    deep = np.all((ijk >= 2) & (ijk <= n - 4), axis=1)
+    cand = np.nonzero(deep)[0]
+    pick = rng.permutation(cand)
+    used = np.zeros(len(x), dtype=bool)
+    moved, holes = 0, []
+    stride = np.array([n ** a for a in range(d)])
+    for i in pick:
+        if moved < cfg.defects:
+            j = i + 1                                  # +x neighbour (x fastest)
+            block = [i, j]
+            if used[block].any():
+                continue
+            x[i, 0] += 0.95 * dx
+            used[np.clip(np.arange(i - 2 * n ** (d - 1), i + 2 * n ** (d - 1) + 1), 0, len(x) - 1)] = True
+            moved += 1
+        elif len(holes) < cfg.defects:
+            corner = ijk[i]
+            offs = np.array(np.meshgrid(*([[0, 1]] * d), indexing="ij")).reshape(d, -1).T
+            block = (corner[None, :] + offs) @ stride
+            if used[block].any():
+                continue
+            holes.extend(block.tolist())
+            used[np.clip(np.arange(i - 3 * n ** (d - 1), i + 3 * n ** (d - 1) + 1), 0, len(x) - 1)] = True
+        else:
+            break
+    keep = np.ones(len(x), dtype=bool)
+    keep[holes] = False
+    return x[keep], kind[keep]
 
 
 def initial_fields(cfg: CavityConfig, x: np.ndarray):

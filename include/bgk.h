@@ -37,7 +37,8 @@
  *    call (bgk_sync, bgk_wls_coeffs, bgk_build_neighbors, bgk_moments,
  *    bgk_get_f).  bgk_last_error gives the message and the particle index.
  *  - All work is enqueued on the caller's stream; bgk_step enqueues no host
- *    synchronisation and is CUDA-graph capturable.
+ *    synchronisation and is CUDA-graph capturable -- unless particle management is on
+ *    (cfg.manage = 1), which reads its decision counts back once per ALE step.
  */
 #ifndef BGK_B200_H
 #define BGK_B200_H
@@ -89,9 +90,19 @@ typedef struct bgk_config {
                             least-squares fit: nu = 5 (2D) / 9 (3D) unknowns, deficient
                             below nu+1 neighbours.  abar may then be negative; the transport applies
                             the flux formula literally, abar (c.n - |c.n|). */
+    int32_t manage;      /* particle management (Z28): 1 = a merge/fill pass at
+                            the start of every ALE step (bgk_step / bgk_step_transport then
+                            synchronise the stream once per step and may change N); 0 = off */
+    int32_t m_min;       /* fill threshold: interior particles with fewer neighbours get candidates
+                            (<= 0: dims + 3) */
+    double r_merge;      /* merge radius [m]: interior pairs closer than this are merged
+                            (<= 0: 0.2 dx) */
+    int64_t max_particles; /* particle capacity of the workspace (<= 0: N); management inserts
+                            stop there (reported) */
 } bgk_config;
 
-/* Bytes of device workspace bgk_init_cloud needs for N particles. */
+/* Bytes of device workspace bgk_init_cloud needs for N particles (sized for
+ * max(N, cfg->max_particles) particles). */
 bgk_status bgk_workspace_size(const bgk_config* cfg, int64_t N, size_t* bytes);
 
 /* Create a context and fill the initial state.
@@ -223,6 +234,34 @@ bgk_status bgk_destroy(bgk_ctx* ctx);
 
 /* Library version string. */
 const char* bgk_version(void);
+
+/* Particle management pass ("Adding and removing points"; SPEC.md:316-358;
+ * DESIGN.md reading Z28) on the current state, with the thresholds of the configuration:
+ *  1. merge: interior pairs closer than r_merge (greedy, ascending index) become ONE particle at
+ *     the midpoint (slot of the smaller index), its f row, transport velocity W and macro state
+ *     interpolated (linear WLS with a constant term, the boundary-interpolation construction of
+ *     Z19) from every other particle within h of the midpoint;
+ *  2. fill: interior particles with fewer than m_min neighbours propose x +- 0.5 h e_a; proposals
+ *     inside the open box and farther than 0.45 dx from every particle are inserted (appended),
+ *     interpolated the same way;
+ *  3. the surviving particles keep their relative order, inserted ones follow.
+ * Deficient interpolation stencils keep the pair / skip the proposal; inserts stop at the
+ * capacity.  report (host, may be NULL) receives int64[6] = {merges, merges kept (deficient),
+ * inserts, inserts skipped (deficient), inserts skipped (capacity), N after the pass}.
+ * Runs on the caller's stream and synchronises it; invalidates cached geometry; the next
+ * bgk_step rebuilds it.  Particle indices change when anything was merged or inserted:
+ * re-query bgk_count and re-read arrays.  Errors: BGK_E_CUDA. */
+bgk_status bgk_manage(bgk_ctx* ctx, int64_t* report, bgk_stream stream);
+
+/* Current particle counts (they change only through particle management): N, interior,
+ * boundary (host pointers, each may be NULL), and the capacity. */
+bgk_status bgk_count(bgk_ctx* ctx, int64_t* N, int64_t* n_interior, int64_t* n_boundary, int64_t* capacity);
+
+/* Kinds of the current particles (host or device int8[N]); synchronises. */
+bgk_status bgk_get_kind(bgk_ctx* ctx, int8_t* kind, bgk_stream stream);
+
+/* Report of the last management pass (int64[6] as bgk_manage), zeros if none ran. */
+bgk_status bgk_manage_report(bgk_ctx* ctx, int64_t* report);
 
 #ifdef __cplusplus
 }

@@ -85,6 +85,9 @@ def lib():
                 "or_init_f": (None, [_P, _I64, _P, _P, _P, _P]),
                 "or_step": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
                 "or_moments_all": (C.c_int, [_P, _I64, _P, _P, _P]),
+                "or_interp_weights": (C.c_int, [C.c_int, _P, _P, C.c_int, _P, _D, _D, _P]),
+                "or_manage": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _D, C.c_int, _I64, _P, _P, _P, _P, _P,
+                                        _P]),
                 "or_omp_threads": (C.c_int, []),
                 "or_set_threads": (None, [C.c_int]),
             }
@@ -340,12 +343,13 @@ def init_f(c: OrCfg, rho, U, T) -> np.ndarray:
 
 
 class State:
-    """Whole-cloud oracle state (x, kind, f, W, macro)."""
+    """Whole-cloud oracle state (x, kind, f, W, macro).  ``manage`` = (r_merge, m_min, capacity)
+    runs the particle-management pass (or_manage) at the start of every ALE step."""
 
-    def __init__(self, c: OrCfg, cloud):
+    def __init__(self, c: OrCfg, cloud, manage=None):
         self.c = c
         self.x = np.ascontiguousarray(cloud["x"], dtype=np.float64).copy()
-        self.kind = np.ascontiguousarray(cloud["kind"], dtype=np.int8)
+        self.kind = np.ascontiguousarray(cloud["kind"], dtype=np.int8).copy()
         self.f = init_f(c, cloud["rho"], cloud["U"], cloud["T"])
         self.W = np.ascontiguousarray(cloud["U"], dtype=np.float64).copy()
         if not c.ale:
@@ -353,11 +357,39 @@ class State:
         N, d = self.x.shape
         self.macro = np.zeros((N, d + 2))
         self.rho_w = np.zeros(N)
+        self.manage_params = manage
+        self.reports = []
+
+    def manage(self, r_merge, m_min, cap):
+        """One particle-management pass (or_manage); returns the report
+        (merges, merges kept, fills, fills deficient, fills over capacity, N_out)."""
+        N, d = self.x.shape
+        RK = self.f.shape[1]
+        xo = np.zeros((cap, d))
+        ko = np.zeros(cap, dtype=np.int8)
+        fo = np.zeros((cap, RK))
+        Wo = np.zeros((cap, d))
+        mo = np.zeros((cap, d + 2))
+        rep = np.zeros(6, dtype=np.int64)
+        st = lib().or_manage(C.byref(self.c), N, _p(self.x), _p(self.kind), _p(self.f), _p(self.W),
+                             _p(self.macro), float(r_merge), int(m_min), int(cap), _p(xo), _p(ko), _p(fo),
+                             _p(Wo), _p(mo), _p(rep))
+        if st != OR_OK:
+            raise OracleError(st)
+        n = int(rep[5])
+        self.x, self.kind, self.f = xo[:n].copy(), ko[:n].copy(), fo[:n].copy()
+        self.W, self.macro = Wo[:n].copy(), mo[:n].copy()
+        self.rho_w = np.zeros(n)
+        rep = tuple(int(v) for v in rep)
+        self.reports.append(rep)
+        return rep
 
     def step(self, n: int = 1):
         bad = C.c_int64(-1)
-        N = self.x.shape[0]
         for _ in range(n):
+            if self.manage_params is not None and self.c.ale:
+                self.manage(*self.manage_params)
+            N = self.x.shape[0]
             st = lib().or_step(C.byref(self.c), N, _p(self.x), _p(self.kind), _p(self.f), _p(self.W),
                                _p(self.macro), _p(self.rho_w), C.byref(bad))
             if st != OR_OK:
@@ -374,12 +406,30 @@ class State:
         return out[:, 0], out[:, 1:1 + d], out[:, 1 + d]
 
 
+def manage_params(cfg):
+    """(r_merge, m_min, capacity) of a CavityConfig with manage = 1, else None."""
+    if not getattr(cfg, "manage", 0):
+        return None
+    return (cfg.merge_radius, cfg.min_neighbors, cfg.capacity)
+
+
 def run_steps(cfg, n_steps: int, cloud=None, dt=None) -> State:
     from bgk_inputs import make_cloud
     c = make_cfg(cfg, dt)
-    s = State(c, cloud if cloud is not None else make_cloud(cfg))
+    s = State(c, cloud if cloud is not None else make_cloud(cfg), manage=manage_params(cfg))
     s.step(n_steps)
     return s
+
+
+def interp_weights(x, S, p, h2, alpha_w):
+    """or_interp_weights: WLS interpolation weights of point p from particles S (status, c)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    d = x.shape[1]
+    S = np.ascontiguousarray(S, dtype=np.int32)
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    cw = np.zeros(max(len(S), 1))
+    st = lib().or_interp_weights(d, _p(x), _p(S), len(S), _p(p), h2, alpha_w, _p(cw))
+    return st, cw[:len(S)]
 
 
 def omp_threads() -> int:

@@ -748,6 +748,220 @@ int or_step(const or_cfg* c, int64_t N, double* x, const int8_t* kind, double* f
     return st;
 }
 
+/* ------------------------------------------------- particle management --- */
+/* Interpolation weights of a new point p from the particles S[0..m) ("update the
+ * distribution function on these new grid points with the help of the least squares
+ * method"; S:283-287 interpolate_value): linear WLS with a constant term, f ~ a0 + a.(x - p),
+ * w_s = exp(-alpha |x_s - p|^2 / h^2), P_s = (1, (x_s - p) / h), B = sum_s w_s P_s P_s^T,
+ * c_s = w_s e0^T B^{-1} P_s (the value at p is sum_s c_s f_s).  Same construction as the
+ * boundary weights (Z19) with every stencil member used.  Deficient: m < d+2 or
+ * lambda_min(B) < 1e-12 lambda_max(B) -> OR_E_DEFICIENT. */
+int or_interp_weights(int d, const double* x, const int32_t* S, int m, const double* p,
+                      double h2, double alpha_w, double* cw) {
+    int n = d + 1;
+    double h = sqrt(h2);
+    double B[16] = {0}, Binv[16];
+    for (int s = 0; s < m; ++s) {
+        const double* xs = x + (int64_t)S[s] * d;
+        double P[4];
+        P[0] = 1.0;
+        for (int r = 0; r < d; ++r) P[1 + r] = (xs[r] - p[r]) / h;
+        double w = or_weight(dist2(d, p, xs), h2, alpha_w);
+        for (int r = 0; r < n; ++r)
+            for (int q = 0; q < n; ++q) B[r * n + q] = B[r * n + q] + w * P[r] * P[q];
+    }
+    if (deficient(d, m, n, B)) return OR_E_DEFICIENT;
+    if (inverse(n, B, Binv)) return OR_E_DEFICIENT;
+    for (int s = 0; s < m; ++s) {
+        const double* xs = x + (int64_t)S[s] * d;
+        double P[4];
+        P[0] = 1.0;
+        for (int r = 0; r < d; ++r) P[1 + r] = (xs[r] - p[r]) / h;
+        double w = or_weight(dist2(d, p, xs), h2, alpha_w);
+        double acc = 0.0;
+        for (int q = 0; q < n; ++q) acc = acc + Binv[0 * n + q] * P[q];
+        cw[s] = w * acc;
+    }
+    return OR_OK;
+}
+
+/* Stencil of a new point p: every particle of the cloud (x, N) within h of p (closed ball,
+ * the O2 distance), ascending, except ex0 / ex1.  Returns the count (writes <= cap). */
+static int stencil_of(int d, const double* x, int64_t N, double h2, const double* p, int64_t ex0,
+                      int64_t ex1, int32_t* S, int cap) {
+    int m = 0;
+    for (int64_t k = 0; k < N; ++k) {
+        if (k == ex0 || k == ex1) continue;
+        if (dist2(d, p, x + k * d) <= h2) {
+            if (m < cap) S[m] = (int32_t)k;
+            ++m;
+        }
+    }
+    return m;
+}
+
+/* Interpolate one new particle at p from the OLD state: f row, W, macro.  Returns status. */
+static int interp_new(const or_cfg* c, int64_t N, const double* x, const double* f, const double* W,
+                      const double* macro, const double* p, int64_t ex0, int64_t ex1, double* f_row,
+                      double* W_row, double* macro_row) {
+    int d = c->dims, nv = nval_of(c);
+    int64_t RK = (int64_t)nv * or_num_nodes(c);
+    int cap = 4096;
+    int32_t* S = (int32_t*)malloc(sizeof(int32_t) * (size_t)cap);
+    int m = stencil_of(d, x, N, c->h2, p, ex0, ex1, S, cap);
+    if (m > cap) { free(S); return OR_E_CAPACITY; }
+    double* cw = (double*)malloc(sizeof(double) * (size_t)(m > 0 ? m : 1));
+    int st = or_interp_weights(d, x, S, m, p, c->h2, c->alpha_w, cw);
+    if (st == OR_OK) {
+        for (int64_t k = 0; k < RK; ++k) {
+            double acc = 0.0;
+            for (int s = 0; s < m; ++s) acc = acc + cw[s] * f[(int64_t)S[s] * RK + k];
+            f_row[k] = acc;
+        }
+        for (int q = 0; q < d; ++q) {
+            double acc = 0.0;
+            for (int s = 0; s < m; ++s) acc = acc + cw[s] * W[(int64_t)S[s] * d + q];
+            W_row[q] = acc;
+        }
+        for (int q = 0; q < d + 2; ++q) {
+            double acc = 0.0;
+            for (int s = 0; s < m; ++s) acc = acc + cw[s] * macro[(int64_t)S[s] * (d + 2) + q];
+            macro_row[q] = acc;
+        }
+    }
+    free(S);
+    free(cw);
+    return st;
+}
+
+/* Particle management pass ("if two points are close to each other, we remove both
+ * of them and introduce a new grid in the mid-point ... when they scatter ... one has to add
+ * new particles"; Z28), at the start of an ALE step, on the state
+ * (x, kind, f, W, macro) of N particles:
+ *  1. merge: for interior i ascending, unprocessed: the first j of N(i) (ascending) with j > i,
+ *     interior, unprocessed and d2(i, j) < r_merge^2 pairs with i; both become processed.  The
+ *     pair is replaced by ONE particle at m = (x_i + x_j) * 0.5 in slot i (slot j is removed);
+ *     its f row, W and macro are interpolated from every other particle of the OLD cloud
+ *     within h of m.  A deficient stencil keeps the pair (reported).
+ *  2. fill: for interior i ascending, not processed in 1, with |N(i)| < m_min: the candidates
+ *     p = x_i + s (0.5 h) e_a (a = 0..d-1; s = +1, then -1) strictly inside (0, L)^d and
+ *     farther than 0.45 dx from every particle of the CURRENT cloud (old particles minus the
+ *     removed slots, merged particles at their midpoints, candidates inserted so far) are
+ *     appended, interpolated from the OLD cloud within h of p.  Deficient candidates are
+ *     skipped; insertion stops at the capacity cap (both reported).
+ *  3. compaction: the surviving slots in ascending old order, then the appended particles.
+ * Outputs (capacity cap): x_out, kind_out, f_out, W_out, macro_out;
+ * report[6] = {merges, merges kept (deficient), fills, fills skipped (deficient),
+ * fills skipped (capacity), N_out}. */
+int or_manage(const or_cfg* c, int64_t N, const double* x, const int8_t* kind, const double* f,
+              const double* W, const double* macro, double r_merge, int m_min, int64_t cap,
+              double* x_out, int8_t* kind_out, double* f_out, double* W_out, double* macro_out,
+              int64_t* report) {
+    int d = c->dims, nv = nval_of(c);
+    int64_t RK = (int64_t)nv * or_num_nodes(c);
+    double rm2 = r_merge * r_merge;
+    double hh = 0.5 * c->h;
+    double thr2 = (0.45 * c->dx) * (0.45 * c->dx);
+    for (int q = 0; q < 6; ++q) report[q] = 0;
+    int64_t* off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(N + 1));
+    int64_t need = 0;
+    or_neighbors(d, x, N, c->h2, off, NULL, 0, &need);
+    int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)(need > 0 ? need : 1));
+    or_neighbors(d, x, N, c->h2, off, idx, need, &need);
+    char* processed = (char*)calloc((size_t)N + 1, 1);
+    char* removed = (char*)calloc((size_t)N + 1, 1);
+    int64_t* partner = (int64_t*)malloc(sizeof(int64_t) * (size_t)(N + 1));
+    double* cur = (double*)malloc(sizeof(double) * (size_t)(N * d + 1));   /* current positions */
+    memcpy(cur, x, sizeof(double) * (size_t)(N * d));
+    double* mf = (double*)malloc(sizeof(double) * (size_t)(N * RK + 1)); /* merged rows (slot i) */
+    double* mW = (double*)malloc(sizeof(double) * (size_t)(N * d + 1));
+    double* mM = (double*)malloc(sizeof(double) * (size_t)(N * (d + 2) + 1));
+    for (int64_t i = 0; i < N; ++i) partner[i] = -1;
+    /* 1. merge */
+    for (int64_t i = 0; i < N; ++i) {
+        if (kind[i] != 0 || processed[i]) continue;
+        int64_t j = -1;
+        for (int64_t e = off[i]; e < off[i + 1]; ++e) {
+            int64_t k = idx[e];
+            if (k > i && kind[k] == 0 && !processed[k] && dist2(d, x + i * d, x + k * d) < rm2) {
+                j = k;
+                break;
+            }
+        }
+        if (j < 0) continue;
+        processed[i] = processed[j] = 1;
+        double mp[3];
+        for (int a = 0; a < d; ++a) mp[a] = (x[i * d + a] + x[j * d + a]) * 0.5;
+        if (interp_new(c, N, x, f, W, macro, mp, i, j, mf + i * RK, mW + i * d, mM + i * (d + 2)) != OR_OK) {
+            ++report[1];
+            continue;
+        }
+        ++report[0];
+        partner[i] = j;
+        removed[j] = 1;
+        for (int a = 0; a < d; ++a) cur[i * d + a] = mp[a];
+    }
+    /* 2. fill */
+    int64_t n_live = N - report[0];
+    int64_t nf = 0, fcap = cap - n_live > 0 ? cap - n_live : 0;
+    double* fx = (double*)malloc(sizeof(double) * (size_t)((fcap > 0 ? fcap : 1) * d));
+    double* ff = (double*)malloc(sizeof(double) * (size_t)((fcap > 0 ? fcap : 1) * RK));
+    double* fW = (double*)malloc(sizeof(double) * (size_t)((fcap > 0 ? fcap : 1) * d));
+    double* fM = (double*)malloc(sizeof(double) * (size_t)((fcap > 0 ? fcap : 1) * (d + 2)));
+    for (int64_t i = 0; i < N; ++i) {
+        if (kind[i] != 0 || processed[i] || off[i + 1] - off[i] >= m_min) continue;
+        for (int a = 0; a < d; ++a)
+            for (int sgn = 0; sgn < 2; ++sgn) {
+                double p[3];
+                for (int q = 0; q < d; ++q) p[q] = x[i * d + q];
+                p[a] = sgn == 0 ? x[i * d + a] + hh : x[i * d + a] - hh;
+                int inside = 1;
+                for (int q = 0; q < d; ++q)
+                    if (!(p[q] > 0.0 && p[q] < c->L)) inside = 0;
+                if (!inside) continue;
+                int clear = 1;
+                for (int64_t k = 0; k < N && clear; ++k)
+                    if (!removed[k] && !(dist2(d, p, cur + k * d) > thr2)) clear = 0;
+                for (int64_t k = 0; k < nf && clear; ++k)
+                    if (!(dist2(d, p, fx + k * d) > thr2)) clear = 0;
+                if (!clear) continue;
+                if (nf >= fcap) { ++report[4]; continue; }
+                if (interp_new(c, N, x, f, W, macro, p, -1, -1, ff + nf * RK, fW + nf * d,
+                               fM + nf * (d + 2)) != OR_OK) {
+                    ++report[3];
+                    continue;
+                }
+                for (int q = 0; q < d; ++q) fx[nf * d + q] = p[q];
+                ++nf;
+            }
+    }
+    report[2] = nf;
+    /* 3. compaction */
+    int64_t t = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        if (removed[i]) continue;
+        int merged = partner[i] >= 0;
+        for (int q = 0; q < d; ++q) x_out[t * d + q] = cur[i * d + q];
+        kind_out[t] = kind[i];
+        memcpy(f_out + t * RK, merged ? mf + i * RK : f + i * RK, sizeof(double) * (size_t)RK);
+        memcpy(W_out + t * d, merged ? mW + i * d : W + i * d, sizeof(double) * (size_t)d);
+        memcpy(macro_out + t * (d + 2), merged ? mM + i * (d + 2) : macro + i * (d + 2),
+               sizeof(double) * (size_t)(d + 2));
+        ++t;
+    }
+    for (int64_t k = 0; k < nf; ++k, ++t) {
+        for (int q = 0; q < d; ++q) x_out[t * d + q] = fx[k * d + q];
+        kind_out[t] = 0;
+        memcpy(f_out + t * RK, ff + k * RK, sizeof(double) * (size_t)RK);
+        memcpy(W_out + t * d, fW + k * d, sizeof(double) * (size_t)d);
+        memcpy(macro_out + t * (d + 2), fM + k * (d + 2), sizeof(double) * (size_t)(d + 2));
+    }
+    report[5] = t;
+    free(off); free(idx); free(processed); free(removed); free(partner); free(cur);
+    free(mf); free(mW); free(mM); free(fx); free(ff); free(fW); free(fM);
+    return OR_OK;
+}
+
 /* Moments of every row of f, interior and boundary. */
 int or_moments_all(const or_cfg* c, int64_t N, const double* f, double* macro, int64_t* bad) {
     int d = c->dims, nv = nval_of(c);

@@ -26,7 +26,8 @@ class BgkConfig(C.Structure):
                 ("R", C.c_double), ("kb", C.c_double), ("dmol", C.c_double), ("T_wall", C.c_double),
                 ("U_lid", C.c_double * 3), ("dx", C.c_double), ("ale", C.c_int32),
                 ("col_begin", C.c_int32), ("col_end", C.c_int32), ("max_neighbors", C.c_int32),
-                ("wls_order", C.c_int32)]
+                ("wls_order", C.c_int32), ("manage", C.c_int32), ("m_min", C.c_int32),
+                ("r_merge", C.c_double), ("max_particles", C.c_int64)]
 
 
 _P = C.c_void_p
@@ -58,6 +59,10 @@ SIGNATURES = {
     "bgk_launches_per_step": [_P, _P],
     "bgk_sync": [_P, _P],
     "bgk_destroy": [_P],
+    "bgk_manage": [_P, _P, _P],
+    "bgk_count": [_P, _P, _P, _P, _P],
+    "bgk_manage_report": [_P, _P],
+    "bgk_get_kind": [_P, _P, _P],
 }
 OTHER = {"bgk_last_error": (C.c_char_p, [_P, _P]), "bgk_version": (C.c_char_p, [])}
 EXPORTED = sorted(list(SIGNATURES) + list(OTHER))

@@ -37,6 +37,10 @@ def make_config(cfg, col_range: Optional[Tuple[int, int]] = None, max_neighbors:
         c.col_begin, c.col_end = col_range
     c.max_neighbors = max_neighbors
     c.wls_order = getattr(cfg, "wls_order", 1)
+    c.manage = getattr(cfg, "manage", 0)
+    c.m_min = getattr(cfg, "m_min", 0)
+    c.r_merge = getattr(cfg, "r_merge", 0.0)
+    c.max_particles = cfg.capacity if getattr(cfg, "manage", 0) else 0
     return c
 
 
@@ -62,7 +66,7 @@ class Bgk:
         self.device = torch.device(device if device is not None else "cuda")
         self.c = make_config(cfg, col_range, max_neighbors, dt)
         N = int(len(cloud["x"]))
-        self.N = N
+        self._N = N
         n1 = cfg.Nv + 1
         ncol_g = n1 ** (cfg.dims - 1)
         self.col_range = (0, ncol_g) if col_range is None else tuple(col_range)
@@ -85,6 +89,38 @@ class Bgk:
         self.kind = kind
 
     # ------------------------------------------------------------ helpers
+    @property
+    def N(self) -> int:
+        """Current particle count (particle management may change it)."""
+        if getattr(self, "ctx", None) and self.c.manage:
+            n = C.c_int64(0)
+            self._check(self.L.bgk_count(self.ctx, C.byref(n), None, None, None))
+            self._N = int(n.value)
+        return self._N
+
+    def counts(self):
+        """(N, interior, boundary, capacity)."""
+        v = [C.c_int64(0) for _ in range(4)]
+        self._check(self.L.bgk_count(self.ctx, *[C.byref(q) for q in v]))
+        return tuple(int(q.value) for q in v)
+
+    def manage(self):
+        """One particle-management pass (bgk_manage); returns its report tuple
+        (merges, merges kept, inserts, inserts deficient, inserts over capacity, N)."""
+        rep = np.zeros(6, dtype=np.int64)
+        self._check(self.L.bgk_manage(self.ctx, _ptr(rep), self.stream))
+        return tuple(int(v) for v in rep)
+
+    def kinds(self):
+        k = np.zeros(self.N, dtype=np.int8)
+        self._check(self.L.bgk_get_kind(self.ctx, _ptr(k), self.stream))
+        return k
+
+    def manage_report(self):
+        rep = np.zeros(6, dtype=np.int64)
+        self._check(self.L.bgk_manage_report(self.ctx, _ptr(rep)))
+        return tuple(int(v) for v in rep)
+
     @property
     def stream(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream

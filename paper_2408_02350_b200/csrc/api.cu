@@ -36,7 +36,8 @@ bool valid_cfg(const bgk_config* c, int64_t N) {
     if (c->Nv < 2 || c->Nv + 1 > 64) return false;   // odd Nv allowed: the paper's Figs. 6-7 use Nv = 15
     if (!(c->vmax > 0.0) || !(c->L > 0.0) || !(c->h > 0.0) || !(c->h2 > 0.0) || !(c->dt >= 0.0)) return false;
     if (!(c->R > 0.0) || !(c->kb > 0.0) || !(c->dmol > 0.0) || !(c->T_wall > 0.0) || !(c->alpha_w > 0.0)) return false;
-    if (N > (int64_t)INT32_MAX) return false;
+    if (N > (int64_t)INT32_MAX || c->max_particles > (int64_t)INT32_MAX) return false;
+    if (c->manage != 0 && c->manage != 1) return false;
     if (c->wls_order < 0 || c->wls_order > 2) return false;
     return true;
 }
@@ -57,12 +58,13 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     }
     c->ncol = c->c1 - c->c0;
     c->N = N;
+    c->Ncap = std::max<int64_t>(N, cfg->max_particles);
     c->Kloc = (int64_t)c->n1 * c->ncol;
     c->ncs = c->d == 3 ? c->ncol + (c->ncol & 1) : c->ncol;
     c->Ks = (int64_t)c->n1 * c->ncs;
     c->RS = c->Ks * c->nv;
     c->max_nb = cfg->max_neighbors > 0 ? cfg->max_neighbors : (c->d == 2 ? 96 : 256);
-    c->cap = N * (int64_t)c->max_nb;
+    c->cap = c->Ncap * (int64_t)c->max_nb;
     int nc = (int)std::floor(cfg->L / cfg->h);
     nc = std::max(1, std::min(nc, cfg->dims == 3 ? 1024 : kMaxCellsPerAxis));
     while (nc > 1 && cfg->L / nc < cfg->h * (1.0 + 1e-12)) --nc;   // cell edge strictly >= h
@@ -97,9 +99,35 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->bnd_nch = (int)((c->Ks + 511) / 512);   // k_bnd_interp: 256 threads x 2 nodes per block
 }
 
+// particle-management scratch (only when cfg.manage): decision arrays over the capacity, the
+// gathered per-particle arrays, and the interpolation stencils of up to kManageMaxNew new particles
+void carve_manage(bgk_ctx* c, Carver& k) {
+    const bool on = c->cfg.manage != 0;
+    const int64_t N = on ? c->Ncap : 1;
+    const int d = c->d;
+    const int64_t nn = on ? kManageMaxNew : 1;
+    Manage& m = c->mg;
+    m.flag = k.take<uint8_t>(N);
+    m.status = k.take<int32_t>(N);
+    m.map = k.take<int32_t>(N);
+    m.x = k.take<double>(N * d);
+    m.W = k.take<double>(N * d);
+    m.macro = k.take<double>(N * (d + 2));
+    m.kind = k.take<int8_t>(N);
+    m.pos = k.take<double>(nn * d);
+    m.nW = k.take<double>(nn * d);
+    m.nM = k.take<double>(nn * (d + 2));
+    m.dst = k.take<int32_t>(nn);
+    m.sm = k.take<int32_t>(nn);
+    m.sidx = k.take<int32_t>(nn * c->max_nb);
+    m.sc = k.take<double>(nn * c->max_nb);
+    m.rep = k.take<int64_t>(8);
+    m.counts = k.take<int32_t>(4);
+}
+
 size_t carve(bgk_ctx* c, char* base, bool dry) {
     Carver k{base, 0, dry};
-    const int64_t N = c->N;
+    const int64_t N = c->Ncap;   // every per-particle buffer is sized for the capacity
     const int d = c->d;
     c->x = k.take<double>(N * d);
     c->kind = k.take<int8_t>(N);
@@ -137,6 +165,7 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     const int64_t ng = c->np == 2 ? (N + 1) / 2 : 1;
     c->gU = k.take<int32_t>(c->np == 2 ? (size_t)ng * c->ucap * 2 : 2);   // int2 entries
     c->gUlen = k.take<int32_t>(4 * ng);
+    carve_manage(c, k);
     return k.off + 256;
 }
 
@@ -183,13 +212,52 @@ bgk_status sync_check(bgk_ctx* c, cudaStream_t s) {
 
 cudaStream_t S(bgk_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
-void ensure_geometry(bgk_ctx* c, cudaStream_t s) {
+}  // namespace
+
+// interior / boundary lists from host kinds and positions (boundary particles sorted by
+// (wall, z, y, x) so face neighbours are adjacent), counts, and the TMA maps (their outer
+// extent is N).  Synchronous host->device copies (the host vectors die on return).
+bgk_status bgk::install_lists(bgk_ctx* c, const int8_t* hk, const double* hx, cudaStream_t s) {
+    const int64_t N = c->N;
+    const int d = c->d;
+    std::vector<int32_t> in, bd;
+    for (int64_t i = 0; i < N; ++i) (hk[i] == 0 ? in : bd).push_back((int32_t)i);
+    std::stable_sort(bd.begin(), bd.end(), [&](int32_t a, int32_t b) {
+        if (hk[a] != hk[b]) return hk[a] < hk[b];
+        for (int q = d - 1; q >= 0; --q)
+            if (hx[(int64_t)a * d + q] != hx[(int64_t)b * d + q]) return hx[(int64_t)a * d + q] < hx[(int64_t)b * d + q];
+        return a < b;
+    });
+    c->N_int = (int64_t)in.size();
+    c->N_b = (int64_t)bd.size();
+    if (!make_tensor_maps(c)) return BGK_E_CUDA;
+    cudaError_t e = cudaSuccess;
+    if (!in.empty()) e = cudaMemcpyAsync(c->interior, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && !bd.empty())
+        e = cudaMemcpyAsync(c->boundary, bd.data(), sizeof(int32_t) * bd.size(), cudaMemcpyHostToDevice, s);
+    // interior ids also serve as the initial processing order (the neighbour build re-sorts it)
+    if (e == cudaSuccess && !in.empty())
+        e = cudaMemcpyAsync(c->g.order, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? BGK_OK : cuda_fail(c, e);
+}
+
+namespace {
+
+bgk_status ensure_geometry(bgk_ctx* c, cudaStream_t s) {
     if (c->cfg.ale || !c->geometry_valid) {
         launch_build_neighbors(c, s);
+        if (c->cfg.manage && c->cfg.ale) {        // particle management on the step-start cloud (Z28)
+            bool changed = false;
+            bgk_status st = manage_pass(c, s, &changed);
+            if (st != BGK_OK) return st;
+            if (changed) launch_build_neighbors(c, s);
+        }
         launch_wls(c, s);
         launch_group_union(c, s);
         c->geometry_valid = true;
     }
+    return BGK_OK;
 }
 
 bgk_status copy_out(bgk_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t s) {
@@ -228,32 +296,17 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
     c->fcur = 0;
     c->geometry_valid = false;
     cudaStream_t s = S(stream);
-    // kinds on the host to build the static interior / boundary lists
+    // kinds and positions on the host to build the interior / boundary lists
     std::vector<int8_t> hk(N);
+    std::vector<double> hx(N * c->d);
     cudaError_t e = cudaMemcpy(hk.data(), kind, N, cudaMemcpyDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(hx.data(), x, sizeof(double) * N * c->d, cudaMemcpyDefault);
     if (e != cudaSuccess) { bgk_status st = cuda_fail(c, e); delete c; return st; }
-    std::vector<int32_t> in, bd;
-    for (int64_t i = 0; i < N; ++i) {
+    for (int64_t i = 0; i < N; ++i)
         if (hk[i] < 0 || hk[i] > 2 * c->d) { delete c; return BGK_E_INVALID_ARG; }
-        (hk[i] == 0 ? in : bd).push_back((int32_t)i);
-    }
-    {   // boundary particles sorted by (wall, z, y, x): neighbours on a face are adjacent in the list
-        std::vector<double> hx(N * c->d);
-        e = cudaMemcpy(hx.data(), x, sizeof(double) * N * c->d, cudaMemcpyDefault);
-        if (e != cudaSuccess) { bgk_status st = cuda_fail(c, e); delete c; return st; }
-        const int d = c->d;
-        std::stable_sort(bd.begin(), bd.end(), [&](int32_t a, int32_t b) {
-            if (hk[a] != hk[b]) return hk[a] < hk[b];
-            for (int q = d - 1; q >= 0; --q)
-                if (hx[(int64_t)a * d + q] != hx[(int64_t)b * d + q]) return hx[(int64_t)a * d + q] < hx[(int64_t)b * d + q];
-            return a < b;
-        });
-    }
-    c->N_int = (int64_t)in.size();
-    c->N_b = (int64_t)bd.size();
-    if (!make_tensor_maps(c)) {
-        delete c;
-        return BGK_E_CUDA;
+    {
+        bgk_status st = install_lists(c, hk.data(), hx.data(), s);
+        if (st != BGK_OK) { delete c; return st; }
     }
     const int64_t reset[4] = {0, INT64_MAX, 0, 0};
     cudaMemcpyAsync(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice, s);
@@ -263,10 +316,6 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
     cudaMemsetAsync(c->stab, 0, sizeof(unsigned long long), s);
     cudaMemcpyAsync(c->x, x, sizeof(double) * N * c->d, cudaMemcpyDefault, s);
     cudaMemcpyAsync(c->kind, hk.data(), N, cudaMemcpyHostToDevice, s);
-    if (!in.empty()) cudaMemcpyAsync(c->interior, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
-    if (!bd.empty()) cudaMemcpyAsync(c->boundary, bd.data(), sizeof(int32_t) * bd.size(), cudaMemcpyHostToDevice, s);
-    // interior ids also serve as the initial processing order
-    if (!in.empty()) cudaMemcpyAsync(c->g.order, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
     const double* m0 = nullptr;
     if (macro0) {
         cudaMemcpyAsync(c->outbuf, macro0, sizeof(double) * N * (c->d + 2), cudaMemcpyDefault, s);
@@ -354,7 +403,11 @@ bgk_status bgk_run_phase(bgk_ctx* c, bgk_phase phase, bgk_stream stream) {
     cudaStream_t s = S(stream);
     double* fn = c->f[1 - c->fcur];
     switch (phase) {
-        case BGK_PHASE_GEOMETRY: ensure_geometry(c, s); break;
+        case BGK_PHASE_GEOMETRY: {
+            bgk_status st = ensure_geometry(c, s);
+            if (st != BGK_OK) return st;
+            break;
+        }
         case BGK_PHASE_TRANSPORT: launch_transport(c, c->f[c->fcur], fn, s); break;
         case BGK_PHASE_MOMENT_SUMS: launch_moment_reduce(c, s); break;
         case BGK_PHASE_RELAX: launch_relax(c, fn, s); break;
@@ -497,7 +550,8 @@ bgk_status bgk_get_neighbors(bgk_ctx* c, int64_t* offsets, int32_t* idx, int64_t
 bgk_status bgk_stable_dt(bgk_ctx* c, double* dt_out, bgk_stream stream) {
     if (!c || !dt_out) return BGK_E_INVALID_ARG;
     cudaStream_t s = S(stream);
-    ensure_geometry(c, s);
+    bgk_status st0 = ensure_geometry(c, s);
+    if (st0 != BGK_OK) return st0;
     cudaMemsetAsync(c->stab, 0, sizeof(unsigned long long), s);
     launch_transport(c, c->f[c->fcur], c->f[1 - c->fcur], s);
     bgk_status st = check_launch(c);
@@ -535,6 +589,42 @@ const char* bgk_last_error(bgk_ctx* c, int64_t* particle) {
 bgk_status bgk_destroy(bgk_ctx* c) {
     delete c;
     return BGK_OK;
+}
+
+bgk_status bgk_manage(bgk_ctx* c, int64_t* report, bgk_stream stream) {
+    if (!c) return BGK_E_INVALID_ARG;
+    if (!c->cfg.manage) return BGK_E_INVALID_ARG;   // no scratch carved
+    cudaStream_t s = S(stream);
+    launch_build_neighbors(c, s);
+    bool changed = false;
+    bgk_status st = manage_pass(c, s, &changed);
+    c->geometry_valid = false;
+    if (st == BGK_OK) st = sync_check(c, s);
+    if (report) std::memcpy(report, c->mg_report, sizeof(c->mg_report));
+    return st;
+}
+
+bgk_status bgk_count(bgk_ctx* c, int64_t* N, int64_t* n_interior, int64_t* n_boundary, int64_t* capacity) {
+    if (!c) return BGK_E_INVALID_ARG;
+    if (N) *N = c->N;
+    if (n_interior) *n_interior = c->N_int;
+    if (n_boundary) *n_boundary = c->N_b;
+    if (capacity) *capacity = c->Ncap;
+    return BGK_OK;
+}
+
+bgk_status bgk_manage_report(bgk_ctx* c, int64_t* report) {
+    if (!c || !report) return BGK_E_INVALID_ARG;
+    std::memcpy(report, c->mg_report, sizeof(c->mg_report));
+    return BGK_OK;
+}
+
+bgk_status bgk_get_kind(bgk_ctx* c, int8_t* kind, bgk_stream stream) {
+    if (!c || !kind) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    bgk_status st = copy_out(c, kind, c->kind, (size_t)c->N, s);
+    if (st != BGK_OK) return st;
+    return sync_check(c, s);
 }
 
 }  // extern "C"

@@ -36,13 +36,35 @@ struct Geo {                    // per-step geometry arrays (device)
     int32_t* order;             // [N_int] interior particles in cell order (transport processing order)
 };
 
+// particle management (manage.cu, Z28)
+constexpr int kManageMaxNew = 4096;   // new particles (merges + inserts) per pass
+struct Manage {
+    uint8_t* flag;      // [Ncap] bit0: merge candidate (a j > i closer than r_merge), bit1: < m_min neighbours
+    int32_t* status;    // [Ncap] 0 live, -1 removed (merged into its partner), q+1: slot holds merged particle q
+    int32_t* map;       // [Ncap] new index t -> old index (>= 0) or -(q+1) for new particle q
+    double* x;          // [Ncap][d]   gathered arrays (copied back after the pass)
+    double* W;          // [Ncap][d]
+    double* macro;      // [Ncap][d+2]
+    int8_t* kind;       // [Ncap]
+    double* pos;        // [kManageMaxNew][d] new particles: position
+    double* nW;         // [kManageMaxNew][d]            interpolated transport velocity
+    double* nM;         // [kManageMaxNew][d+2]          interpolated macro state
+    int32_t* dst;       // [kManageMaxNew]               final index
+    int32_t* sm;        // [kManageMaxNew]               stencil size
+    int32_t* sidx;      // [kManageMaxNew][max_nb]       stencil (old indices)
+    double* sc;         // [kManageMaxNew][max_nb]       interpolation weights
+    int64_t* rep;       // [8] merges, kept, inserts, deficient, capacity, N_out, n_new, changed
+    int32_t* counts;    // [4] flagged particles
+};
+
 }  // namespace bgk
 
 struct bgk_ctx {
     bgk_config cfg;
     int d, nv, n1, ncol_g, c0, c1, ncol;
     int ncs;                           // stored column stride: ncol rounded up to even in 3D (16-B TMA strides)
-    int64_t N, N_int, N_b, Kloc, Ks, RS;   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
+    int64_t N, N_int, N_b, Kloc, Ks, RS;
+    int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
     int ncg;                           // 32-column groups per chunk (transport)
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
     int max_nb;
@@ -77,6 +99,8 @@ struct bgk_ctx {
     int32_t* gU;        // [groups][ucap] packed union (j << 4 | member mask) of each particle group's lists
     int32_t* gUlen;     // [groups]
     int ucap;
+    bgk::Manage mg;     // particle-management scratch (cfg.manage)
+    int64_t mg_report[6];   // host copy of the last pass's report
     int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)
     int64_t* scan_tmp;  // [1024]
     bgk::Geo g;
@@ -151,5 +175,9 @@ __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int
 int launches_neighbors();
 void launch_group_union(bgk_ctx* c, cudaStream_t s);
 int launches_wls();
+// particle management: one pass (synchronises the stream); *changed = N or indices changed
+bgk_status manage_pass(bgk_ctx* c, cudaStream_t s, bool* changed);
+// kinds/positions on the host -> interior / boundary / order lists, counts, TMA maps
+bgk_status install_lists(bgk_ctx* c, const int8_t* hk, const double* hx, cudaStream_t s);
 
 }  // namespace bgk

@@ -1,0 +1,101 @@
+"""Particle management on the GPU (Z28) against the oracle.
+
+Bars: the decisions (which pairs merge, which candidates are inserted, the compaction order) are
+integer outcomes of the same rounded distance tests on both sides -> reports, kinds and positions
+bit-exact after one pass; interpolated rows within 1e-12 of the oracle's (one weighted sum);
+after managed ALE steps the usual 1e-10 bar of the step parity tests.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import bgk_inputs as bi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+SIG = math.sqrt(bi.R_GAS * bi.T0)
+
+M2 = bi.CavityConfig("M2", 2, 21, 12, manage=1, defects=2, m_min=21, jitter=0.05, dt=5e-12)
+M3 = bi.CavityConfig("M3", 3, 12, 6, manage=1, defects=2, m_min=84, jitter=0.05, dt=5e-12)
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    oracle.build()
+    return torch
+
+
+def gpu(cfg, cloud):
+    from paper_2408_02350_b200 import Bgk
+    return Bgk(cfg, cloud, device="cuda:0")
+
+
+def rel(a, b):
+    return np.abs(a - b).max() / np.abs(b).max()
+
+
+@pytest.mark.parametrize("cfg", [M2, M3])
+def test_one_pass_matches_oracle(torch_cuda, cfg):
+    cloud = bi.make_cloud(cfg)
+    g = gpu(cfg, cloud)
+    rep = g.manage()
+    s = oracle.State(oracle.make_cfg(cfg), cloud)
+    ref = s.manage(*oracle.manage_params(cfg))
+    assert rep == ref
+    assert rep[0] >= 1 and rep[2] >= 1
+    N = rep[5]
+    assert g.N == N
+    assert np.array_equal(g.positions(), s.x)
+    assert np.array_equal(g.kinds(), s.kind)
+    f = g.get_f().reshape(N, -1)
+    assert rel(f, s.f) <= 1e-12
+    n_int = int((s.kind == 0).sum())
+    assert g.counts()[:3] == (N, n_int, N - n_int)
+
+
+def test_capacity_limit_reported(torch_cuda):
+    cfg = M2.replace(max_particles=0)
+    cloud = bi.make_cloud(cfg)
+    cap = len(cloud["x"]) + 2
+    cfg = cfg.replace(max_particles=cap)
+    g = gpu(cfg, cloud)
+    rep = g.manage()
+    ref = oracle.State(oracle.make_cfg(cfg), cloud).manage(*oracle.manage_params(cfg))
+    assert rep == ref and rep[4] > 0 and rep[5] <= cap
+
+
+@pytest.mark.parametrize("cfg", [M2, M3])
+def test_managed_steps_match_oracle(torch_cuda, cfg):
+    cloud = bi.make_cloud(cfg)
+    g = gpu(cfg, cloud)
+    g.step(5)
+    g.sync()
+    ref = oracle.run_steps(cfg, 5, cloud)
+    assert g.manage_report() == ref.reports[-1]
+    N = len(ref.x)
+    assert g.N == N
+    assert np.array_equal(g.kinds(), ref.kind)
+    assert np.abs(g.positions() - ref.x).max() <= 1e-12 * cfg.dx
+    f = g.get_f().reshape(N, -1)
+    assert rel(f, ref.f) <= TOL
+    rho, U, T = g.moments()
+    r0, u0, t0 = ref.moments()
+    assert np.abs(rho / r0 - 1).max() <= TOL
+    assert np.abs(U - u0).max() / SIG <= TOL
+    assert np.abs(T / t0 - 1).max() <= TOL
+
+
+def test_management_is_a_noop_on_regular_lattice(torch_cuda):
+    """C4 with management on: nothing merges or fills, so the run is bitwise the unmanaged one."""
+    a = gpu(bi.C4.replace(manage=1), bi.make_cloud(bi.C4))
+    b = gpu(bi.C4, bi.make_cloud(bi.C4))
+    a.step(3)
+    b.step(3)
+    assert a.manage_report() == (0, 0, 0, 0, 0, bi.C4.n_particles)
+    assert np.array_equal(a.get_f(), b.get_f())
