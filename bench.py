@@ -3,8 +3,8 @@
 Workload (BASELINE.json north_star target): 3D driven cavity C5, 40^3 particles x 25^3
 velocity nodes (Nv = 24), Kn = 1, dt = 1e-11, ALE mode (neighbours + WLS rebuilt every
 step), synthetic seeded "stress" initial state (bgk_inputs).  One "step" is the whole hot
-path: neighbour search, WLS, transport, moments, Maxwellian + relaxation, ALE move,
-diffuse-reflection walls.
+path: neighbour search, particle management (merge / fill pass; --manage 0 turns it off), WLS,
+transport, moments, Maxwellian + relaxation, ALE move, diffuse-reflection walls.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
 
@@ -161,6 +161,8 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = bi.CONFIGS[args.config] if args.config in bi.CONFIGS else getattr(bi, args.config)
+    if args.manage and cfg.ale:
+        cfg = cfg.replace(manage=1)      # the paper's step includes "Particle Organization" (Table 3)
     cloud = bi.make_cloud(cfg)
     ncol = (cfg.Nv + 1) ** (cfg.dims - 1)
     shard = bi.column_shards(ncol, world)[rank]
@@ -293,6 +295,7 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "particles": N, "interior": n_int, "velocity_nodes": K,
                    "interior_pairs": sum_m, "ale": bool(cfg.ale), "init": cfg.init, "dt": cfg.dt,
+                   "particle_management": bool(cfg.manage),
                    "parallelism": f"velocity-sharded x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2 (f = {N * K * nval * 8 / 1e9:.1f} GB per buffer)"},
         "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / float(peaks.get("hbm_gbs", 6650.0)),
@@ -349,6 +352,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--manage", type=int, default=1, choices=[0, 1],
+                    help="particle management pass in every ALE step (the paper's Particle Organization)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
