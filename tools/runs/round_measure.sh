@@ -9,3 +9,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/${tag}_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_transport -s 1 -c 1 \
     -o gpurun_out/${tag}_transport python tools/prof_run.py --steps 2 > gpurun_out/${tag}_ncu_full.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log 2>&1; echo SMOKE_RC=$? >> gpurun_out/${tag}_smoke.log
