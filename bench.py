@@ -156,10 +156,17 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # validation knobs for the multi-rank path on a one-GPU box: every rank on device
+    # BGK_BENCH_DEVICE, collectives over BGK_DIST_BACKEND (gloo); production uses NCCL, one GPU per rank
+    local = int(os.environ.get("BGK_BENCH_DEVICE", local))
+    backend = os.environ.get("BGK_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = bi.CONFIGS[args.config] if args.config in bi.CONFIGS else getattr(bi, args.config)
     if args.manage and cfg.ale:
         cfg = cfg.replace(manage=1)      # the paper's step includes "Particle Organization" (Table 3)
