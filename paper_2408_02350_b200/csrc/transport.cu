@@ -708,10 +708,9 @@ void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_
     }
 }
 
-template <int R>
+template <int R, int MINB = (R <= 13 ? 3 : 2)>        // 12 (8) resident warps per SM
 void launch_pair_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     constexpr int WPB = kDefaultWarps;
-    constexpr int MINB = R <= 13 ? 3 : 2;                    // 12 (8) resident warps per SM
     constexpr int B = PStage<R>::BYTES;
     constexpr int NST0 = (220 * 1024) / (MINB * WPB * B);
     constexpr int NST = NST0 > 8 ? 8 : (NST0 < 2 ? 2 : NST0);
