@@ -569,6 +569,9 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
     if (!c || !n) return BGK_E_INVALID_ARG;
     int64_t k = 0;
     if (c->cfg.ale) k += launches_neighbors() + launches_wls() - (c->N_b ? 0 : 1) - (c->N_int ? 0 : 1);
+    if (c->cfg.ale && c->cfg.manage) k += 2;   // k_mg_detect + k_mg_decide (plus 3 more and a neighbour
+                                               // rebuild in the rare steps where the cloud changes)
+    if (c->cfg.ale && c->np == 2) k += 1;      // k_pair_union
     if (c->N_int) k += 3;        // transport, moment reduce, relax
     if (c->N_b) k += 3;          // boundary interp, wall reduce, fill
     *n = k;
