@@ -312,6 +312,29 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if world == 1 and cfg.ale and not args.no_secondary:
+        # the fixed-cloud (Eulerian, W = 0, geometry cached) C5 run as the secondary
+        # number -- the same kernels, without the per-step neighbour search / WLS / management
+        g.close()
+        del g
+        torch.cuda.empty_cache()
+        cfg2 = cfg.replace(ale=0, manage=0)
+        g2 = Bgk(cfg2, cloud, device=dev)
+        for _ in range(max(2, args.warmup)):
+            g2.step(1)
+        g2.sync()
+        barrier()
+        n2 = max(3, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(n2):
+            g2.step(1)
+        e1.record(stream)
+        barrier()
+        ms2 = e0.elapsed_time(e1) / n2
+        g2.sync()
+        out["secondary"] = {"workload": cfg2.name + " fixed cloud (W = 0, geometry cached)", "ms_per_step": ms2,
+                            "value": N * K / (ms2 / 1e3), "unit": UNIT, "steps": n2}
+        g2.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, desc = oracle_sample_rate(cfg, cloud, seconds=args.cpu_seconds)
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
@@ -359,6 +382,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the fixed-cloud secondary number")
     ap.add_argument("--manage", type=int, default=1, choices=[0, 1],
                     help="particle management pass in every ALE step (the paper's Particle Organization)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
