@@ -75,6 +75,7 @@ class CavityConfig:
     m_min: int = 0
     max_particles: int = 0
     defects: int = 0          # management workloads: `defects` close pairs + `defects` holes (lattice())
+    staging: int = 0          # 1: input staging buffer for overlapped host -> device copies (e2e)
 
     @property
     def rho0(self) -> float:

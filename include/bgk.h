@@ -99,6 +99,8 @@ typedef struct bgk_config {
                             (<= 0: 0.2 dx) */
     int64_t max_particles; /* particle capacity of the workspace (<= 0: N); management inserts
                             stop there (reported) */
+    int32_t staging;     /* 1: the workspace also holds an input staging buffer for bgk_stage_f /
+                            bgk_use_staged_f (host -> device copies overlapped with steps); 0: none */
 } bgk_config;
 
 /* Bytes of device workspace bgk_init_cloud needs for N particles (sized for
@@ -234,6 +236,17 @@ bgk_status bgk_destroy(bgk_ctx* ctx);
 
 /* Library version string. */
 const char* bgk_version(void);
+
+/* Overlapped host input (cfg.staging = 1).  bgk_stage_f enqueues the host -> device copy of a
+ * canonical-layout f (as bgk_set_f: host or device, N*nval*K_local doubles) into the staging
+ * buffer on copy_stream, after the previously staged input has been consumed; it returns
+ * without synchronising.  bgk_use_staged_f makes `stream` wait for that copy and converts the
+ * staged state into the current f (the state the next bgk_step advances).  A user loop
+ *   stage(f_0); for n: { use_staged(); stage(f_{n+1}); step(); read results; }
+ * moves step n+1's input while step n computes.  Errors: BGK_E_INVALID_ARG (no staging buffer,
+ * nothing staged), BGK_E_CUDA. */
+bgk_status bgk_stage_f(bgk_ctx* ctx, const double* f, bgk_stream copy_stream);
+bgk_status bgk_use_staged_f(bgk_ctx* ctx, bgk_stream stream);
 
 /* Particle management pass ("Adding and removing points"; SPEC.md:316-358;
  * DESIGN.md reading Z28) on the current state, with the thresholds of the configuration:

@@ -27,7 +27,7 @@ class BgkConfig(C.Structure):
                 ("U_lid", C.c_double * 3), ("dx", C.c_double), ("ale", C.c_int32),
                 ("col_begin", C.c_int32), ("col_end", C.c_int32), ("max_neighbors", C.c_int32),
                 ("wls_order", C.c_int32), ("manage", C.c_int32), ("m_min", C.c_int32),
-                ("r_merge", C.c_double), ("max_particles", C.c_int64)]
+                ("r_merge", C.c_double), ("max_particles", C.c_int64), ("staging", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -63,6 +63,8 @@ SIGNATURES = {
     "bgk_count": [_P, _P, _P, _P, _P],
     "bgk_manage_report": [_P, _P],
     "bgk_get_kind": [_P, _P, _P],
+    "bgk_stage_f": [_P, _P, _P],
+    "bgk_use_staged_f": [_P, _P],
 }
 OTHER = {"bgk_last_error": (C.c_char_p, [_P, _P]), "bgk_version": (C.c_char_p, [])}
 EXPORTED = sorted(list(SIGNATURES) + list(OTHER))

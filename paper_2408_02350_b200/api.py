@@ -41,6 +41,7 @@ def make_config(cfg, col_range: Optional[Tuple[int, int]] = None, max_neighbors:
     c.m_min = getattr(cfg, "m_min", 0)
     c.r_merge = getattr(cfg, "r_merge", 0.0)
     c.max_particles = cfg.capacity if getattr(cfg, "manage", 0) else 0
+    c.staging = getattr(cfg, "staging", 0)
     return c
 
 
@@ -110,6 +111,16 @@ class Bgk:
         rep = np.zeros(6, dtype=np.int64)
         self._check(self.L.bgk_manage(self.ctx, _ptr(rep), self.stream))
         return tuple(int(v) for v in rep)
+
+    def stage_f(self, f, copy_stream=None):
+        """Enqueue the host -> device copy of the next input state (canonical layout) on
+        `copy_stream` (a torch.cuda.Stream); returns at once (bgk_stage_f)."""
+        cs = copy_stream.cuda_stream if copy_stream is not None else self.stream
+        self._check(self.L.bgk_stage_f(self.ctx, _ptr(f), cs))
+
+    def use_staged_f(self):
+        """The next step starts from the staged state (bgk_use_staged_f; stream-ordered)."""
+        self._check(self.L.bgk_use_staged_f(self.ctx, self.stream))
 
     def kinds(self):
         k = np.zeros(self.N, dtype=np.int8)

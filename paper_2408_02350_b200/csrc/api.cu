@@ -38,6 +38,7 @@ bool valid_cfg(const bgk_config* c, int64_t N) {
     if (!(c->R > 0.0) || !(c->kb > 0.0) || !(c->dmol > 0.0) || !(c->T_wall > 0.0) || !(c->alpha_w > 0.0)) return false;
     if (N > (int64_t)INT32_MAX || c->max_particles > (int64_t)INT32_MAX) return false;
     if (c->manage != 0 && c->manage != 1) return false;
+    if (c->staging != 0 && c->staging != 1) return false;
     if (c->wls_order < 0 || c->wls_order > 2) return false;
     return true;
 }
@@ -166,6 +167,7 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->gU = k.take<int32_t>(c->np == 2 ? (size_t)ng * c->ucap * 2 : 2);   // int2 entries
     c->gUlen = k.take<int32_t>(4 * ng);
     carve_manage(c, k);
+    c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     return k.off + 256;
 }
 
@@ -320,6 +322,11 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
     if (macro0) {
         cudaMemcpyAsync(c->outbuf, macro0, sizeof(double) * N * (c->d + 2), cudaMemcpyDefault, s);
         m0 = c->outbuf;
+    }
+    if (c->cfg.staging) {
+        cudaEventCreateWithFlags(&c->ev_staged, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&c->ev_consumed, cudaEventDisableTiming);
+        cudaEventRecord(c->ev_consumed, s);
     }
     launch_check_domain(c, s);
     launch_wall_tables(c, s);
@@ -590,8 +597,36 @@ const char* bgk_last_error(bgk_ctx* c, int64_t* particle) {
 }
 
 bgk_status bgk_destroy(bgk_ctx* c) {
+    if (c && c->cfg.staging) {
+        cudaEventDestroy(c->ev_staged);
+        cudaEventDestroy(c->ev_consumed);
+    }
     delete c;
     return BGK_OK;
+}
+
+bgk_status bgk_stage_f(bgk_ctx* c, const double* f, bgk_stream copy_stream) {
+    if (!c || !f || !c->cfg.staging) return BGK_E_INVALID_ARG;
+    cudaStream_t cs = S(copy_stream);
+    cudaError_t e = cudaStreamWaitEvent(cs, c->ev_consumed, 0);   // the previous staged input is converted
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->stage, f, sizeof(double) * c->N * c->nv * c->Kloc, cudaMemcpyDefault, cs);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_staged, cs);
+    if (e != cudaSuccess) return cuda_fail(c, e);
+    c->stage_pending = true;
+    return BGK_OK;
+}
+
+bgk_status bgk_use_staged_f(bgk_ctx* c, bgk_stream stream) {
+    if (!c || !c->cfg.staging || !c->stage_pending) return BGK_E_INVALID_ARG;
+    cudaStream_t s = S(stream);
+    cudaError_t e = cudaStreamWaitEvent(s, c->ev_staged, 0);
+    if (e != cudaSuccess) return cuda_fail(c, e);
+    launch_from_canonical(c, c->stage, c->f[c->fcur], s);
+    e = cudaEventRecord(c->ev_consumed, s);
+    if (e != cudaSuccess) return cuda_fail(c, e);
+    c->stage_pending = false;
+    return check_launch(c);
 }
 
 bgk_status bgk_manage(bgk_ctx* c, int64_t* report, bgk_stream stream) {

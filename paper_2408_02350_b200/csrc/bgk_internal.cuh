@@ -100,6 +100,9 @@ struct bgk_ctx {
     int32_t* gUlen;     // [groups]
     int ucap;
     bgk::Manage mg;     // particle-management scratch (cfg.manage)
+    double* stage;      // [Ncap][nv*Kloc] canonical input staging buffer (cfg.staging)
+    cudaEvent_t ev_staged, ev_consumed;
+    bool stage_pending;
     int64_t mg_report[6];   // host copy of the last pass's report
     int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)
     int64_t* scan_tmp;  // [1024]

@@ -379,3 +379,20 @@ def test_fixed_cloud_3d_ten_steps(torch_cuda):
     g.step(10)
     g.sync()
     check_state(g, oracle_run(cfg, 10), cfg)
+
+
+def test_staged_input_matches_set_f(torch_cuda):
+    """bgk_stage_f on a copy stream + bgk_use_staged_f is the same state as bgk_set_f: a
+    fixed-cloud run restarted from a staged f^0 reproduces the fresh run bitwise."""
+    import torch
+    cfg = bi.C1.replace(ale=0, staging=1)
+    a, cloud = gpu(cfg)
+    b, _ = gpu(cfg, cloud)
+    f0 = torch.from_numpy(a.get_f()).pin_memory()
+    a.step(3)
+    cs = torch.cuda.Stream()
+    a.stage_f(f0, cs)
+    a.use_staged_f()
+    a.step(2)
+    b.step(2)
+    assert np.array_equal(a.get_f(), b.get_f())
