@@ -344,8 +344,10 @@ def run_ours(args):
         barrier()
         ms2 = e0.elapsed_time(e1) / n2
         g2.sync()
+        info = g2.transport_info()
         out["secondary"] = {"workload": cfg2.name + " fixed cloud (W = 0, geometry cached)", "ms_per_step": ms2,
-                            "value": N * K / (ms2 / 1e3), "unit": UNIT, "steps": n2}
+                            "value": N * K / (ms2 / 1e3), "unit": UNIT, "steps": n2,
+                            "lattice_row_groups": info[2], "general_kernel_particles": info[3]}
         g2.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, desc = oracle_sample_rate(cfg, cloud, seconds=args.cpu_seconds)

@@ -270,6 +270,11 @@ bgk_status bgk_manage(bgk_ctx* ctx, int64_t* report, bgk_stream stream);
  * boundary (host pointers, each may be NULL), and the capacity. */
 bgk_status bgk_count(bgk_ctx* ctx, int64_t* N, int64_t* n_interior, int64_t* n_boundary, int64_t* capacity);
 
+/* Transport mapping in use (diagnostics): info[0] particles per warp (1 or 2), info[1] rows per
+ * lane R of the general kernel, info[2] fixed-cloud lattice-row groups (8 particles each, 0 if
+ * the lattice-row kernel is not used), info[3] interior particles left to the general kernel. */
+bgk_status bgk_transport_info(bgk_ctx* ctx, int64_t* info);
+
 /* Kinds of the current particles (host or device int8[N]); synchronises. */
 bgk_status bgk_get_kind(bgk_ctx* ctx, int8_t* kind, bgk_stream stream);
 

@@ -122,6 +122,12 @@ class Bgk:
         """The next step starts from the staged state (bgk_use_staged_f; stream-ordered)."""
         self._check(self.L.bgk_use_staged_f(self.ctx, self.stream))
 
+    def transport_info(self):
+        """(particles per warp, rows per lane, lattice-row groups, particles left to the general kernel)."""
+        v = np.zeros(4, dtype=np.int64)
+        self._check(self.L.bgk_transport_info(self.ctx, _ptr(v)))
+        return tuple(int(q) for q in v)
+
     def kinds(self):
         k = np.zeros(self.N, dtype=np.int8)
         self._check(self.L.bgk_get_kind(self.ctx, _ptr(k), self.stream))

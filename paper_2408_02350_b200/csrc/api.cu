@@ -96,6 +96,14 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
         c->nwpp = c->nchunk * c->ncg;
         c->nslots = c->nwpp * 32;
     }
+    // fixed-cloud lattice rows (SURVEY §8(d) "the one lever"): partial slots sized for both mappings
+    {
+        const char* e = getenv("BGK_TRANSPORT_ROWS");
+        c->rows_on = !cfg->ale && c->d == 3 && c->wls_order == 1 && c->np == 1 && c->ncol == c->ncol_g &&
+                     !(e && atoi(e) == 0);
+        c->rows_nchunk = (c->n1 + kRowsR - 1) / kRowsR;
+        if (c->rows_on) c->nwpp = std::max(c->nchunk, c->rows_nchunk) * c->ncg;
+    }
     c->bnd_chunk = 256;
     c->bnd_nch = (int)((c->Ks + 511) / 512);   // k_bnd_interp: 256 threads x 2 nodes per block
 }
@@ -168,6 +176,8 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->gUlen = k.take<int32_t>(4 * ng);
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
+    c->rows_p0 = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
+    c->order_rest = k.take<int32_t>(c->rows_on ? (size_t)N : 1);
     return k.off + 256;
 }
 
@@ -258,6 +268,11 @@ bgk_status ensure_geometry(bgk_ctx* c, cudaStream_t s) {
         launch_wls(c, s);
         launch_group_union(c, s);
         c->geometry_valid = true;
+        c->rows_built = false;
+        if (c->rows_on) {                         // fixed cloud: detect the lattice rows once
+            bgk_status st = build_rows(c, s);
+            if (st != BGK_OK) return st;
+        }
     }
     return BGK_OK;
 }
@@ -648,6 +663,15 @@ bgk_status bgk_count(bgk_ctx* c, int64_t* N, int64_t* n_interior, int64_t* n_bou
     if (n_interior) *n_interior = c->N_int;
     if (n_boundary) *n_boundary = c->N_b;
     if (capacity) *capacity = c->Ncap;
+    return BGK_OK;
+}
+
+bgk_status bgk_transport_info(bgk_ctx* c, int64_t* info) {
+    if (!c || !info) return BGK_E_INVALID_ARG;
+    info[0] = c->np;
+    info[1] = c->R;
+    info[2] = c->rows_built ? c->n_rows : 0;
+    info[3] = c->rows_built ? c->n_rest : c->N_int;
     return BGK_OK;
 }
 

@@ -38,6 +38,11 @@ struct Geo {                    // per-step geometry arrays (device)
 
 // particle management (manage.cu, Z28)
 constexpr int kManageMaxNew = 4096;   // new particles (merges + inserts) per pass
+#ifndef BGK_ROWS_R
+#define BGK_ROWS_R 5
+#endif
+constexpr int kRowsG = 8;            // particles per lattice-row group (fixed-cloud transport)
+constexpr int kRowsR = BGK_ROWS_R;   // velocity nodes per lane along v_1 in the lattice-row kernel
 struct Manage {
     uint8_t* flag;      // [Ncap] bit0: merge candidate (a j > i closer than r_merge), bit1: < m_min neighbours
     int32_t* status;    // [Ncap] 0 live, -1 removed (merged into its partner), q+1: slot holds merged particle q
@@ -67,6 +72,7 @@ struct bgk_ctx {
     int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
     int ncg;                           // 32-column groups per chunk (transport)
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
+    CUtensorMap tmap_rows[2];          //   the same with the lattice-row kernel's box {32, kRowsR, 1}
     int max_nb;
     int64_t cap;
     int nc[3];
@@ -104,6 +110,15 @@ struct bgk_ctx {
     cudaEvent_t ev_staged, ev_consumed;
     bool stage_pending;
     int64_t mg_report[6];   // host copy of the last pass's report
+    // fixed-cloud lattice rows (transport_rows.cu): groups of kRowsG consecutive particles along x
+    // with identical neighbour offsets share the pair coefficients and every neighbour box
+    bool rows_on;       // possible for this configuration (fixed cloud, 3D, first order, one particle per warp)
+    bool rows_built;    // groups detected for the cached geometry
+    int64_t n_rows;     // groups
+    int64_t n_rest;     // interior particles left to the general kernel
+    int32_t* rows_p0;   // [Ncap / kRowsG] first particle of each group
+    int32_t* order_rest;// [Ncap] the rest, in cell order
+    int rows_nchunk;    // velocity chunks of kRowsR nodes along v_1
     int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)
     int64_t* scan_tmp;  // [1024]
     bgk::Geo g;
@@ -170,6 +185,9 @@ void launch_check_domain(bgk_ctx* c, cudaStream_t s);
 int transport_rows_per_thread(int d, int n1, int np);
 int transport_particles_per_warp(int d, int wls_order);
 bool make_tensor_maps(bgk_ctx* c);
+// fixed-cloud lattice rows: host-side group detection on the cached geometry, and the kernel
+bgk_status build_rows(bgk_ctx* c, cudaStream_t s);
+void launch_transport_rows(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 // storage index of local node t = k1*ncol + col  ->  k1*ncs + col
 __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int ncs) {
     const int64_t k1 = t / ncol;

@@ -29,7 +29,9 @@
 // one atomicMax.
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdlib>
+#include <vector>
 
 #include "bgk_internal.cuh"
 
@@ -55,7 +57,8 @@ struct TArgs {
     int ucap;                          //                       capacity per group
     bool signed_n;                     // second-order WLS: pair record carries s_n = -sign(abar)
     int64_t n_int;
-    int n1, ncol, ncs, c0, ncg, nwpp;
+    int n1, ncol, ncs, c0, ncg, nwpp;   // nwpp: partial slots per particle (stride)
+    int nw_grid;                        // (chunk x column group) items of this launch
     double vmax, dv, dt;
 };
 
@@ -426,6 +429,134 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
 }
 
 // ============================================================================
+// Fixed-cloud lattice rows (SURVEY §8(d) "the one lever": W = 0 and a cached regular cloud).
+// kRowsG = 8 consecutive particles along x whose neighbour offsets are identical (the same
+// stencil type: build_rows checks every offset on the host) have identical WLS pair data, so
+//   C_{p0+k, j+k, v} = C_{p0, j, v}  for every offset -- ONE coefficient evaluation serves eight
+// particles, and Sc = sum_j C is shared.  The boxes of a run of offsets along x (consecutive
+// neighbour indices j_first .. j_last of p0) are the window j_first .. j_last + 7: every
+// (offset, particle) pair of the run reads it, so each box is fetched once per run instead of
+// once per (particle, offset).  Per warp: (group, chunk of kRowsR nodes, 32 columns); the window
+// of the next run is loaded by TMA (box {32, kRowsR}) into the other of two buffers while the
+// current run is applied.  Per (offset, lane): 9 FMA setup + kRowsR x 7 DP for C + Sc, then
+// 8 x kRowsR (LDS + DFMA) -- ~3.5 instructions per (particle, neighbour, node) triple instead
+// of ~15.7, and ~1/3 of the box bytes.  The pair data are p0's (the other seven particles' agree
+// to rounding: identical offsets).
+// ============================================================================
+constexpr int kRowsMaxWin = 14;          // boxes per window: run span (<= 6 for h = 3.1 dx) + kRowsG
+// per-warp shared memory: two windows, p0's neighbour list (<= 256), two mbarriers; 128-B multiple
+// (TMA destinations need 128-B alignment)
+constexpr int kRowsMaxRun = kRowsMaxWin - kRowsG + 1;          // offsets per run
+constexpr size_t kRowsBuf =
+    ((size_t)kRowsMaxWin * kRowsR * 32 * sizeof(double) + kRowsMaxRun * 10 * sizeof(double) + 127) / 128 * 128;
+constexpr size_t kRowsWarpSmem = (2 * kRowsBuf + 256 * 4 + 16 + 127) / 128 * 128;
+
+struct RowsArgs {
+    TArgs t;
+    const int32_t* p0;
+    int64_t n_rows;
+};
+
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_constant__ CUtensorMap tmap,
+                                                             const RowsArgs RA) {
+    constexpr int R = kRowsR, G = kRowsG, ROW = 32, PD = 10;
+    constexpr uint32_t BOX = R * ROW * sizeof(double);
+    constexpr uint32_t BUF = (uint32_t)kRowsBuf;               // window boxes, then the run's pair records
+    constexpr uint32_t PREC = kRowsMaxWin * BOX;
+    const TArgs& A = RA.t;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* win = smem_raw + (size_t)wib * kRowsWarpSmem;
+    int32_t* snb = reinterpret_cast<int32_t*>(win + 2 * BUF);     // p0's neighbour list (<= 256)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(win + 2 * BUF + 256 * 4);   // BUF, 256*4 are 16-B multiples
+    const int64_t g = (int64_t)blockIdx.x * WPB + wib;
+    if (g >= RA.n_rows) return;
+    if (lane == 0) {
+        mbar_init(bars, 1);
+        mbar_init(bars + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    const int w = blockIdx.y;
+    const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
+    const int k1s = chunk * R;
+    const int col = cg * 32 + lane;
+    const bool valid = col < A.ncol;
+    const int colc = valid ? col : 0;
+    const int gc = A.c0 + colc;
+    const int p0 = RA.p0[g];
+    const int64_t off = A.nb_off[p0];
+    const int m = (int)(A.nb_off[p0 + 1] - off);
+    for (int e = lane; e < m; e += 32) snb[e] = A.nb_idx[off + e];
+    __syncwarp();
+    const double* Pp = A.P + off * PD;
+    // run [e0, e1): consecutive neighbour indices (one x-line of offsets)
+    auto run_end = [&](int e0) {
+        int e1 = e0 + 1;
+        while (e1 < m && snb[e1] == snb[e1 - 1] + 1 && snb[e1] - snb[e0] + G <= kRowsMaxWin) ++e1;
+        return e1;
+    };
+    auto issue = [&](int e0, int e1, int b) {          // window + pair records of run [e0, e1) into buffer b
+        const int nbox = snb[e1 - 1] - snb[e0] + G;
+        if (elect_one()) {
+            const uint32_t prec = (uint32_t)(e1 - e0) * PD * sizeof(double);
+            mbar_expect_tx(bars + b, (uint32_t)nbox * BOX + prec);
+            for (int q = 0; q < nbox; ++q)
+                tma_load_3d(win + b * BUF + q * BOX, &tmap, cg * ROW, k1s, snb[e0] + q, bars + b);
+            bulk_load(win + b * BUF + PREC, Pp + (int64_t)e0 * PD, prec, bars + b);
+        }
+    };
+    const double c1dv = axis_node(A.vmax, A.dv, k1s) / A.dv;   // W = 0 on a fixed cloud
+    const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
+    const double c2 = axis_node(A.vmax, A.dv, k2), c3 = axis_node(A.vmax, A.dv, k3);
+    double Qf[G][R][1], Sc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        Sc[r] = 0.0;
+#pragma unroll
+        for (int k = 0; k < G; ++k) Qf[k][r][0] = 0.0;
+    }
+    int e0 = 0, e1 = m > 0 ? run_end(0) : 0;
+    if (m > 0) issue(e0, e1, 0);
+    uint32_t use[2] = {0u, 0u};
+    for (int L = 0; e0 < m; ++L) {
+        const int b = L & 1;
+        const int n0 = e1, n1 = n0 < m ? run_end(n0) : n0;
+        __syncwarp();
+        if (n0 < m) issue(n0, n1, b ^ 1);               // next window (its buffer finished a run ago)
+        mbar_wait(bars + b, use[b] & 1u);
+        ++use[b];
+        const double* wb = reinterpret_cast<const double*>(win + b * BUF) + lane;
+        const int jf = snb[e0];
+        const double* pr = reinterpret_cast<const double*>(win + b * BUF + PREC);
+        for (int e = e0; e < e1; ++e) {
+            const double* pv = pr + (e - e0) * PD;                 // broadcast LDS
+            double y[3], dy[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                dy[k] = pv[k * 3];
+                y[k] = fma(dy[k], c1dv, fma(pv[k * 3 + 1], c2, pv[k * 3 + 2] * c3));
+            }
+            const double* wj = wb + (snb[e] - jf) * (BOX / sizeof(double));
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double C = neg_part(fma((double)r, dy[0], y[0])) + neg_part(fma((double)r, dy[1], y[1])) +
+                                 neg_part(fma((double)r, dy[2], y[2]));   // C/2 (the epilogue doubles)
+                Sc[r] += C;
+#pragma unroll
+                for (int k = 0; k < G; ++k) Qf[k][r][0] = fma(C, wj[k * (BOX / sizeof(double)) + r * ROW], Qf[k][r][0]);
+            }
+        }
+        e0 = n0;
+        e1 = n1;
+    }
+    const double Sa[1] = {0.0};
+#pragma unroll
+    for (int k = 0; k < G; ++k) transport_epilogue<3, R, false>(A, p0 + k, w, k1s, colc, gc, valid, Qf[k], Sc, Sa);
+}
+
+// ============================================================================
 // Particle-pair warps (3D, first-order WLS).  A warp owns TWO consecutive particles A, B of the
 // cell-ordered interior list, one chunk of R nodes along v_1 and 32 velocity columns, and walks
 // the UNION of their neighbour lists (k_pair_union, rebuilt with the geometry), sorted into three
@@ -671,7 +802,7 @@ void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
         configured = true;
     }
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
-    k_transport<D, R, NST, WPB, SG, MINB><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
+    k_transport<D, R, NST, WPB, SG, MINB><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(tm, a);
 }
 
 template <int D, int R>
@@ -723,7 +854,7 @@ void launch_pair_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     }
     const int64_t ng = (a.n_int + 1) / 2;
     const unsigned gx = (unsigned)((ng + WPB - 1) / WPB);
-    k_transport_pair<R, NST, WPB, MINB><<<dim3(gx, (unsigned)a.nwpp), WPB * 32, smem, s>>>(tm, a);
+    k_transport_pair<R, NST, WPB, MINB><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(tm, a);
 }
 
 constexpr int kPairR[] = {17, 13, 9, 5};   // rows per lane instantiated for particle-pair warps (R = 25: 255
@@ -806,11 +937,18 @@ bool make_tensor_maps(bgk_ctx* c) {
                                    (cuuint64_t)c->ncs * c->nv * c->n1 * sizeof(double)};
     const cuuint32_t box[3] = {(cuuint32_t)(32 * c->nv), (cuuint32_t)c->R, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint32_t box_rows[3] = {(cuuint32_t)(32 * c->nv), (cuuint32_t)kRowsR, 1};
     for (int b = 0; b < 2; ++b) {
         CUresult r = encode(&c->tmap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->f[b], dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return false;
+        if (c->rows_on) {
+            r = encode(&c->tmap_rows[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->f[b], dims, strides, box_rows, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return false;
+        }
     }
     return true;
 }
@@ -834,6 +972,7 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.c0 = c->c0;
     a.ncg = c->ncg;
     a.nwpp = c->nwpp;
+    a.nw_grid = c->nchunk * c->ncg;
     a.vmax = c->cfg.vmax;
     a.dv = c->dv;
     a.dt = c->cfg.dt;
@@ -842,6 +981,12 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.ucap = c->ucap;
     a.signed_n = c->wls_order == 2;
     const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
+    if (c->rows_built && c->n_rows > 0) {          // fixed-cloud lattice rows + the general kernel on the rest
+        launch_transport_rows(c, fin, fout, s);
+        if (c->n_rest == 0) return;
+        a.order = c->order_rest;
+        a.n_int = c->n_rest;
+    }
     if (c->np == 2) return dispatch_pair(c->R, tm, a, s);
     static const int wpb = [] {
         const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (2, 4, 8); default kDefaultWarps
@@ -849,6 +994,118 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     }();
     if (c->d == 3) dispatch<3>(c->R, wpb, tm, a, s);
     else dispatch<2>(c->R, wpb, tm, a, s);
+}
+
+
+// Lattice-row groups of the cached fixed-cloud geometry: runs of kRowsG interior particles with
+// consecutive indices (+x neighbours) in the cell-ordered list whose neighbour lists are the same
+// offsets (nb(p0 + k)[e] = nb(p0)[e] + k and x_j - x_i equal to 1e-12 dx for every e and k).
+// Everything else stays with the general kernel (order_rest keeps the cell order).
+bgk_status build_rows(bgk_ctx* c, cudaStream_t s) {
+    c->rows_built = false;
+    c->n_rows = 0;
+    c->n_rest = c->N_int;
+    if (!c->rows_on || c->N_int < kRowsG) return BGK_OK;
+    const int64_t N = c->N;
+    const int d = c->d;
+    std::vector<double> x(N * d);
+    std::vector<int64_t> off(N + 1);
+    std::vector<int32_t> order(c->N_int);
+    std::vector<int8_t> kind(N);
+    cudaError_t e = cudaMemcpyAsync(x.data(), c->x, sizeof(double) * N * d, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(off.data(), c->g.nb_off, sizeof(int64_t) * (N + 1), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(order.data(), c->g.order, sizeof(int32_t) * c->N_int, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(kind.data(), c->kind, N, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return BGK_E_CUDA;
+    std::vector<int32_t> nb(off[N]);
+    if (!nb.empty()) {
+        e = cudaMemcpy(nb.data(), c->g.nb_idx, sizeof(int32_t) * nb.size(), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return BGK_E_CUDA;
+    }
+    const double tol = 1e-12 * c->cfg.dx;
+    auto same_stencil = [&](int64_t p, int64_t q, int k) {   // q = p + k
+        const int64_t m = off[p + 1] - off[p];
+        if (off[q + 1] - off[q] != m || m > 256) return false;
+        for (int64_t e2 = 0; e2 < m; ++e2) {
+            const int64_t j = nb[off[p] + e2], jq = nb[off[q] + e2];
+            if (jq != j + k) return false;
+            for (int a = 0; a < d; ++a)
+                if (std::fabs((x[jq * d + a] - x[q * d + a]) - (x[j * d + a] - x[p * d + a])) > tol) return false;
+        }
+        return true;
+    };
+    std::vector<char> grouped(N, 0);
+    std::vector<int32_t> p0s;
+    for (int64_t t = 0; t + kRowsG <= c->N_int; ++t) {
+        const int p = order[t];
+        if (grouped[p]) continue;
+        bool ok = p + kRowsG <= N;
+        for (int k = 1; ok && k < kRowsG; ++k) {
+            const int64_t q = p + k;
+            ok = kind[q] == 0 && !grouped[q] && std::fabs(x[q * d] - x[p * d] - (double)k * c->cfg.dx) <= 1e-9 * c->cfg.dx;
+            for (int a = 1; ok && a < d; ++a) ok = x[q * d + a] == x[p * d + a];
+            ok = ok && same_stencil(p, q, k);
+        }
+        if (!ok) continue;
+        for (int k = 0; k < kRowsG; ++k) grouped[p + k] = 1;
+        p0s.push_back(p);
+    }
+    std::vector<int32_t> rest;
+    rest.reserve(c->N_int);
+    for (int32_t p : order)
+        if (!grouped[p]) rest.push_back(p);
+    c->n_rows = (int64_t)p0s.size();
+    c->n_rest = (int64_t)rest.size();
+    if (!p0s.empty()) e = cudaMemcpy(c->rows_p0, p0s.data(), sizeof(int32_t) * p0s.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !rest.empty())
+        e = cudaMemcpy(c->order_rest, rest.data(), sizeof(int32_t) * rest.size(), cudaMemcpyHostToDevice);
+    // partial slots the general kernel never writes stay zero (the moment reduction sums them all)
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->partials, 0, sizeof(double) * N * c->nwpp * kPM, s);
+    if (e != cudaSuccess) return BGK_E_CUDA;
+    c->rows_built = true;
+    return BGK_OK;
+}
+
+void launch_transport_rows(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
+    constexpr int WPB = 2;                     // 8 warps per SM at R = 3 (24 KB of windows per warp)
+    constexpr size_t smem = WPB * kRowsWarpSmem;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_transport_rows<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured = true;
+    }
+    RowsArgs ra;
+    TArgs& a = ra.t;
+    a.f = fin;
+    a.ft = fout;
+    a.W = c->W;
+    a.order = c->g.order;
+    a.nb_off = c->g.nb_off;
+    a.nb_idx = c->g.nb_idx;
+    a.P = c->g.P;
+    a.partials = c->partials;
+    a.stab = c->stab;
+    a.n_int = c->N_int;
+    a.n1 = c->n1;
+    a.ncol = c->ncol;
+    a.ncs = c->ncs;
+    a.c0 = c->c0;
+    a.ncg = c->ncg;
+    a.nwpp = c->nwpp;
+    a.nw_grid = c->rows_nchunk * c->ncg;
+    a.vmax = c->cfg.vmax;
+    a.dv = c->dv;
+    a.dt = c->cfg.dt;
+    a.gU = nullptr;
+    a.gUlen = nullptr;
+    a.ucap = 0;
+    a.signed_n = false;
+    ra.p0 = c->rows_p0;
+    ra.n_rows = c->n_rows;
+    const unsigned gx = (unsigned)((c->n_rows + WPB - 1) / WPB);
+    k_transport_rows<WPB><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(c->tmap_rows[fin == c->f[0] ? 0 : 1],
+                                                                                 ra);
 }
 
 }  // namespace bgk

@@ -396,3 +396,41 @@ def test_staged_input_matches_set_f(torch_cuda):
     a.step(2)
     b.step(2)
     assert np.array_equal(a.get_f(), b.get_f())
+
+
+# ------------------------------------ fixed-cloud lattice rows (SURVEY §8(d) lever)
+@pytest.mark.parametrize("cfg", [bi.C4.replace(ale=0), bi.CavityConfig("C4r", 3, 24, 8, ale=0)])
+def test_lattice_rows_fixed_cloud(torch_cuda, cfg, monkeypatch):
+    """Fixed cloud on the lattice: groups of 8 x-consecutive particles with identical stencils
+    share coefficients and boxes (k_transport_rows); the rest runs the general kernel.  Same
+    oracle bar, and the same state as the general kernel alone (BGK_TRANSPORT_ROWS=0) to 1e-13."""
+    g, cloud = gpu(cfg)
+    g.step(10)
+    g.sync()
+    info = g.transport_info()
+    assert info[2] > 0 and info[2] * 8 + info[3] == int((cloud["kind"] == 0).sum()), info
+    check_state(g, oracle_run(cfg, 10), cfg)
+    monkeypatch.setenv("BGK_TRANSPORT_ROWS", "0")
+    h, _ = gpu(cfg, cloud)
+    h.step(10)
+    assert rel(g.get_f(), h.get_f()) <= 1e-13
+
+
+def test_lattice_rows_c5_sampled(torch_cuda):
+    """The bench's secondary workload (C5 fixed cloud) through the lattice-row kernel: one step,
+    sampled particles against the oracle evaluated one particle at a time."""
+    import torch
+    cfg = bi.C5.replace(ale=0)
+    g, cloud = gpu(cfg)
+    g.step(1)
+    g.sync()
+    assert g.transport_info()[2] > 0
+    kind = cloud["kind"]
+    inter = np.nonzero(kind == 0)[0]
+    rng = np.random.default_rng(9)
+    sample = [int(v) for v in rng.choice(inter, 6, replace=False)] + [int(inter[len(inter) // 2])]
+    ref = oracle.sampled_first_step(cfg, cloud, sample)
+    fbuf = g.f_internal()
+    rows = fbuf[torch.tensor(sample, device=fbuf.device)].reshape(len(sample), -1).cpu().numpy()
+    for q, i in enumerate(sample):
+        assert rel(rows[q], ref[i]["f"]) <= TOL, (i, rel(rows[q], ref[i]["f"]))
