@@ -385,7 +385,7 @@ bgk_status bgk_wls_coeffs(bgk_ctx* c, bgk_stream stream) {
     launch_wls(c, s);
     bgk_status st = check_launch(c);
     if (st == BGK_OK) st = sync_check(c, s);
-    c->geometry_valid = (st == BGK_OK);
+    c->geometry_valid = false;   // the next step rebuilds the full geometry (interpolation groups, rows)
     return st;
 }
 
