@@ -85,7 +85,14 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->R = transport_rows_per_thread(c->d, c->n1, c->np);
     c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
     c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
-    c->nwpp = c->nchunk * c->ncg;
+    // 2D, 33 columns (N_v = 32): a 32-lane group for ONE column would idle 31 lanes -- the few
+    // columns past the last full group go to a thread-per-(particle, chunk) tail kernel instead
+    c->tail_cols = (c->d == 2 && c->ncol > 32 && c->ncol % 32 != 0 && c->ncol % 32 <= 4 &&
+                    (c->R == 17 || c->R == 13 || c->R == 11 || c->R == 9) && c->wls_order == 1)
+                       ? c->ncol % 32
+                       : 0;
+    if (c->tail_cols) c->ncg = c->ncol / 32;
+    c->nwpp = c->nchunk * c->ncg + (c->tail_cols ? c->nchunk : 0);
     c->nslots = c->nwpp * 32;
     // particle-pair warps: union of two lists, <= 2 max_nb int2 entries per pair, CSR positions < 2^16
     c->ucap = 2 * c->max_nb;
@@ -93,7 +100,7 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
         c->np = 1;
         c->R = transport_rows_per_thread(c->d, c->n1, 1);
         c->nchunk = (c->n1 + c->R - 1) / c->R;
-        c->nwpp = c->nchunk * c->ncg;
+        c->nwpp = c->nchunk * c->ncg + (c->tail_cols ? c->nchunk : 0);
         c->nslots = c->nwpp * 32;
     }
     // fixed-cloud lattice rows (SURVEY §8(d) "the one lever"): partial slots sized for both mappings

@@ -71,6 +71,7 @@ struct bgk_ctx {
     int64_t N, N_int, N_b, Kloc, Ks, RS;
     int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
     int ncg;                           // 32-column groups per chunk (transport)
+    int tail_cols;                     // 2D: columns past the last full group, done by k_transport_tail
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
     CUtensorMap tmap_rows[2];          //   the same with the lattice-row kernel's box {32, kRowsR, 1}
     int max_nb;
