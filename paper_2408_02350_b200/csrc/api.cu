@@ -107,6 +107,7 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     {
         const char* e = getenv("BGK_TRANSPORT_ROWS");
         c->rows_on = !cfg->ale && c->d == 3 && c->wls_order == 1 && c->np == 1 && c->ncol == c->ncol_g &&
+                     c->Ncap < (1 << 23) && c->max_nb <= 256 &&
                      !(e && atoi(e) == 0);
         c->rows_nchunk = (c->n1 + kRowsR - 1) / kRowsR;
         if (c->rows_on) c->nwpp = std::max(c->nchunk, c->rows_nchunk) * c->ncg;
@@ -184,6 +185,8 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     c->rows_p0 = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
+    c->rows_stride = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
+    c->rows_perm = k.take<int16_t>(c->rows_on ? ((size_t)N / kRowsG + 1) * 256 : 1);
     c->order_rest = k.take<int32_t>(c->rows_on ? (size_t)N : 1);
     return k.off + 256;
 }

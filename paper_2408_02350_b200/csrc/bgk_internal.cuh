@@ -118,6 +118,8 @@ struct bgk_ctx {
     int64_t n_rows;     // groups
     int64_t n_rest;     // interior particles left to the general kernel
     int32_t* rows_p0;   // [Ncap / kRowsG] first particle of each group
+    int32_t* rows_stride;   // [Ncap / kRowsG] index step between the group's particles (x, y or z line)
+    int16_t* rows_perm;     // [Ncap / kRowsG][256] p0's neighbour entries in run order
     int32_t* order_rest;// [Ncap] the rest, in cell order
     int rows_nchunk;    // velocity chunks of kRowsR nodes along v_1
     int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)

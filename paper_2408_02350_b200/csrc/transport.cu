@@ -29,6 +29,8 @@
 // one atomicMax.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <vector>
@@ -430,7 +432,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
 
 // ============================================================================
 // Fixed-cloud lattice rows (SURVEY §8(d) "the one lever": W = 0 and a cached regular cloud).
-// kRowsG = 8 consecutive particles along x whose neighbour offsets are identical (the same
+// kRowsG = 8 consecutive particles of one lattice line (x, else y, else z; index step S) whose
+// neighbour offsets are identical (the same
 // stencil type: build_rows checks every offset on the host) have identical WLS pair data, so
 //   C_{p0+k, j+k, v} = C_{p0, j, v}  for every offset -- ONE coefficient evaluation serves eight
 // particles, and Sc = sum_j C is shared.  The boxes of a run of offsets along x (consecutive
@@ -454,6 +457,8 @@ constexpr size_t kRowsWarpSmem = (2 * kRowsBuf + 256 * 4 + 16 + 127) / 128 * 128
 struct RowsArgs {
     TArgs t;
     const int32_t* p0;
+    const int32_t* stride;   // per group: index step between its particles (1: x, n: y, n^2: z line)
+    const int16_t* perm;     // per group [256]: p0's neighbour entries in run order (runs step by stride)
     int64_t n_rows;
 };
 
@@ -468,7 +473,8 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned char* win = smem_raw + (size_t)wib * kRowsWarpSmem;
-    int32_t* snb = reinterpret_cast<int32_t*>(win + 2 * BUF);     // p0's neighbour list (<= 256)
+    // p0's neighbours in run order, packed (j << 8) | CSR position (N < 2^23, <= 256 entries)
+    int32_t* snb = reinterpret_cast<int32_t*>(win + 2 * BUF);
     uint64_t* bars = reinterpret_cast<uint64_t*>(win + 2 * BUF + 256 * 4);   // BUF, 256*4 are 16-B multiples
     const int64_t g = (int64_t)blockIdx.x * WPB + wib;
     if (g >= RA.n_rows) return;
@@ -486,25 +492,37 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
     const int colc = valid ? col : 0;
     const int gc = A.c0 + colc;
     const int p0 = RA.p0[g];
+    const int S = RA.stride[g];
     const int64_t off = A.nb_off[p0];
     const int m = (int)(A.nb_off[p0 + 1] - off);
-    for (int e = lane; e < m; e += 32) snb[e] = A.nb_idx[off + e];
+    for (int e = lane; e < m; e += 32) {
+        const int pe = RA.perm[g * 256 + e];
+        snb[e] = (A.nb_idx[off + pe] << 8) | pe;
+    }
     __syncwarp();
     const double* Pp = A.P + off * PD;
-    // run [e0, e1): consecutive neighbour indices (one x-line of offsets)
+    // run [e0, e1): neighbour indices stepping by S (one line of offsets along the group's axis)
+    // (inside a run j steps by exactly S, so entry e uses window boxes (e - e0) .. (e - e0) + 7)
     auto run_end = [&](int e0) {
         int e1 = e0 + 1;
-        while (e1 < m && snb[e1] == snb[e1 - 1] + 1 && snb[e1] - snb[e0] + G <= kRowsMaxWin) ++e1;
+        while (e1 < m && (snb[e1] >> 8) == (snb[e1 - 1] >> 8) + S && e1 - e0 + G <= kRowsMaxWin) ++e1;
         return e1;
     };
     auto issue = [&](int e0, int e1, int b) {          // window + pair records of run [e0, e1) into buffer b
-        const int nbox = snb[e1 - 1] - snb[e0] + G;
+        const int nbox = e1 - e0 - 1 + G;
         if (elect_one()) {
             const uint32_t prec = (uint32_t)(e1 - e0) * PD * sizeof(double);
             mbar_expect_tx(bars + b, (uint32_t)nbox * BOX + prec);
             for (int q = 0; q < nbox; ++q)
-                tma_load_3d(win + b * BUF + q * BOX, &tmap, cg * ROW, k1s, snb[e0] + q, bars + b);
-            bulk_load(win + b * BUF + PREC, Pp + (int64_t)e0 * PD, prec, bars + b);
+                tma_load_3d(win + b * BUF + q * BOX, &tmap, cg * ROW, k1s, (snb[e0] >> 8) + q * S, bars + b);
+            const int pe0 = snb[e0] & 255, pe1 = snb[e1 - 1] & 255;
+            if (pe1 - pe0 == e1 - 1 - e0) {                  // records contiguous in the CSR (x lines)
+                bulk_load(win + b * BUF + PREC, Pp + (int64_t)pe0 * PD, prec, bars + b);
+            } else {
+                for (int e = e0; e < e1; ++e)
+                    bulk_load(win + b * BUF + PREC + (e - e0) * PD * sizeof(double), Pp + (int64_t)(snb[e] & 255) * PD,
+                              PD * sizeof(double), bars + b);
+            }
         }
     };
     const double c1dv = axis_node(A.vmax, A.dv, k1s) / A.dv;   // W = 0 on a fixed cloud
@@ -528,7 +546,6 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
         mbar_wait(bars + b, use[b] & 1u);
         ++use[b];
         const double* wb = reinterpret_cast<const double*>(win + b * BUF) + lane;
-        const int jf = snb[e0];
         const double* pr = reinterpret_cast<const double*>(win + b * BUF + PREC);
         for (int e = e0; e < e1; ++e) {
             const double* pv = pr + (e - e0) * PD;                 // broadcast LDS
@@ -538,7 +555,7 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
                 dy[k] = pv[k * 3];
                 y[k] = fma(dy[k], c1dv, fma(pv[k * 3 + 1], c2, pv[k * 3 + 2] * c3));
             }
-            const double* wj = wb + (snb[e] - jf) * (BOX / sizeof(double));
+            const double* wj = wb + (e - e0) * (BOX / sizeof(double));
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const double C = neg_part(fma((double)r, dy[0], y[0])) + neg_part(fma((double)r, dy[1], y[1])) +
@@ -553,7 +570,7 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
     }
     const double Sa[1] = {0.0};
 #pragma unroll
-    for (int k = 0; k < G; ++k) transport_epilogue<3, R, false>(A, p0 + k, w, k1s, colc, gc, valid, Qf[k], Sc, Sa);
+    for (int k = 0; k < G; ++k) transport_epilogue<3, R, false>(A, p0 + k * S, w, k1s, colc, gc, valid, Qf[k], Sc, Sa);
 }
 
 // ============================================================================
@@ -1077,10 +1094,12 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
 }
 
 
-// Lattice-row groups of the cached fixed-cloud geometry: runs of kRowsG interior particles with
-// consecutive indices (+x neighbours) in the cell-ordered list whose neighbour lists are the same
-// offsets (nb(p0 + k)[e] = nb(p0)[e] + k and x_j - x_i equal to 1e-12 dx for every e and k).
-// Everything else stays with the general kernel (order_rest keeps the cell order).
+// Lattice-row groups of the cached fixed-cloud geometry: kRowsG interior particles on one lattice
+// line -- along x (index step 1) first, then y (n), then z (n^2) for what is left -- whose
+// neighbour lists are the same offsets (nb(p0 + kS)[e] = nb(p0)[e] + kS and x_j - x_i equal to
+// 1e-12 dx for every e and k).  Each group stores p0's entries in run order (offsets sharing the
+// other two coordinates, ascending along the line).  The rest stays with the general kernel
+// (order_rest keeps the cell order).
 bgk_status build_rows(bgk_ctx* c, cudaStream_t s) {
     c->rows_built = false;
     c->n_rows = 0;
@@ -1103,33 +1122,61 @@ bgk_status build_rows(bgk_ctx* c, cudaStream_t s) {
         e = cudaMemcpy(nb.data(), c->g.nb_idx, sizeof(int32_t) * nb.size(), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) return BGK_E_CUDA;
     }
-    const double tol = 1e-12 * c->cfg.dx;
-    auto same_stencil = [&](int64_t p, int64_t q, int k) {   // q = p + k
+    const double tol = 1e-12 * c->cfg.dx, dx = c->cfg.dx;
+    auto same_stencil = [&](int64_t p, int64_t q, int64_t shift) {   // nb(q)[e] = nb(p)[e] + shift, same offsets
         const int64_t m = off[p + 1] - off[p];
         if (off[q + 1] - off[q] != m || m > 256) return false;
         for (int64_t e2 = 0; e2 < m; ++e2) {
             const int64_t j = nb[off[p] + e2], jq = nb[off[q] + e2];
-            if (jq != j + k) return false;
+            if (jq != j + shift) return false;
             for (int a = 0; a < d; ++a)
                 if (std::fabs((x[jq * d + a] - x[q * d + a]) - (x[j * d + a] - x[p * d + a])) > tol) return false;
         }
         return true;
     };
+    // lines along x, then y, then z (index steps 1, n, n^2 on the lattice: n points per axis)
+    const int64_t n_axis = (int64_t)std::llround(c->cfg.L / dx) + 1;
     std::vector<char> grouped(N, 0);
-    std::vector<int32_t> p0s;
-    for (int64_t t = 0; t + kRowsG <= c->N_int; ++t) {
-        const int p = order[t];
-        if (grouped[p]) continue;
-        bool ok = p + kRowsG <= N;
-        for (int k = 1; ok && k < kRowsG; ++k) {
-            const int64_t q = p + k;
-            ok = kind[q] == 0 && !grouped[q] && std::fabs(x[q * d] - x[p * d] - (double)k * c->cfg.dx) <= 1e-9 * c->cfg.dx;
-            for (int a = 1; ok && a < d; ++a) ok = x[q * d + a] == x[p * d + a];
-            ok = ok && same_stencil(p, q, k);
+    std::vector<int32_t> p0s, strides;
+    std::vector<int16_t> perms;
+    static const int axes = [] {
+        const char* ev = getenv("BGK_ROWS_AXES");   // tuning knob: lines along the first 1, 2 or 3 axes
+        return ev ? atoi(ev) : 3;
+    }();
+    for (int ax = 0; ax < d && ax < axes; ++ax) {
+        const int64_t S = ax == 0 ? 1 : (ax == 1 ? n_axis : n_axis * n_axis);
+        for (int64_t t = 0; t < c->N_int; ++t) {
+            const int p = order[t];
+            if (grouped[p]) continue;
+            bool ok = p + (kRowsG - 1) * S < N;
+            for (int k = 1; ok && k < kRowsG; ++k) {
+                const int64_t q = p + k * S;
+                ok = kind[q] == 0 && !grouped[q];
+                for (int a = 0; ok && a < d; ++a) {
+                    const double want = a == ax ? (double)k * dx : 0.0;
+                    ok = std::fabs(x[q * d + a] - x[(int64_t)p * d + a] - want) <= 1e-9 * dx;
+                }
+                ok = ok && same_stencil(p, q, k * S);
+            }
+            if (!ok) continue;
+            // runs: offsets sharing the other two coordinates, ascending along the line's axis
+            const int64_t m = off[p + 1] - off[p];
+            std::vector<std::pair<std::array<int64_t, 3>, int>> key(m);
+            for (int64_t e2 = 0; e2 < m; ++e2) {
+                const int64_t j = nb[off[p] + e2];
+                int64_t dl[3] = {0, 0, 0};
+                for (int a = 0; a < d; ++a) dl[a] = std::llround((x[j * d + a] - x[(int64_t)p * d + a]) / dx);
+                const int o1 = (ax + 1) % 3, o2 = (ax + 2) % 3;
+                key[e2] = {{dl[o2], dl[o1], dl[ax]}, (int)e2};
+            }
+            std::stable_sort(key.begin(), key.end());
+            for (int k = 0; k < kRowsG; ++k) grouped[p + k * S] = 1;
+            p0s.push_back(p);
+            strides.push_back((int32_t)S);
+            const size_t base = perms.size();
+            perms.resize(base + 256, 0);
+            for (int64_t e2 = 0; e2 < m; ++e2) perms[base + e2] = (int16_t)key[e2].second;
         }
-        if (!ok) continue;
-        for (int k = 0; k < kRowsG; ++k) grouped[p + k] = 1;
-        p0s.push_back(p);
     }
     std::vector<int32_t> rest;
     rest.reserve(c->N_int);
@@ -1138,6 +1185,10 @@ bgk_status build_rows(bgk_ctx* c, cudaStream_t s) {
     c->n_rows = (int64_t)p0s.size();
     c->n_rest = (int64_t)rest.size();
     if (!p0s.empty()) e = cudaMemcpy(c->rows_p0, p0s.data(), sizeof(int32_t) * p0s.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !p0s.empty())
+        e = cudaMemcpy(c->rows_stride, strides.data(), sizeof(int32_t) * strides.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !p0s.empty())
+        e = cudaMemcpy(c->rows_perm, perms.data(), sizeof(int16_t) * perms.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !rest.empty())
         e = cudaMemcpy(c->order_rest, rest.data(), sizeof(int32_t) * rest.size(), cudaMemcpyHostToDevice);
     // partial slots the general kernel never writes stay zero (the moment reduction sums them all)
@@ -1182,6 +1233,8 @@ void launch_transport_rows(bgk_ctx* c, const double* fin, double* fout, cudaStre
     a.ucap = 0;
     a.signed_n = false;
     ra.p0 = c->rows_p0;
+    ra.stride = c->rows_stride;
+    ra.perm = c->rows_perm;
     ra.n_rows = c->n_rows;
     const unsigned gx = (unsigned)((c->n_rows + WPB - 1) / WPB);
     k_transport_rows<WPB><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(c->tmap_rows[fin == c->f[0] ? 0 : 1],
