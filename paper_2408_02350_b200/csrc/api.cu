@@ -113,7 +113,10 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
         if (c->rows_on) c->nwpp = std::max(c->nchunk, c->rows_nchunk) * c->ncg;
     }
     c->bnd_chunk = 256;
-    c->bnd_nch = (int)((c->Ks + 511) / 512);   // k_bnd_interp: 256 threads x 2 nodes per block
+#ifndef BGK_BND_NPT
+#define BGK_BND_NPT 2
+#endif
+    c->bnd_nch = (int)((c->Ks + 256 * BGK_BND_NPT - 1) / (256 * BGK_BND_NPT));   // k_bnd_interp: 256 threads x NPT nodes
 }
 
 // particle-management scratch (only when cfg.manage): decision arrays over the capacity, the

@@ -284,7 +284,14 @@ constexpr int kBndChunk = 256;
 // 256 stored nodes).  Neighbouring boundary particles share most interior neighbours, so the
 // rows loaded for one particle of the group are L1 hits for the next.
 constexpr int kBndGroup = 8;
-constexpr int kBndNPT = 2;   // nodes per thread in k_bnd_interp
+#ifndef BGK_BND_NPT
+#define BGK_BND_NPT 2
+#endif
+#ifndef BGK_BND_UNROLL
+#define BGK_BND_UNROLL 4
+#endif
+constexpr int kBndNPT = BGK_BND_NPT;   // nodes per thread in k_bnd_interp
+constexpr int kBndUnroll = BGK_BND_UNROLL;   // interior neighbours in flight per thread
 
 template <int D>
 __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restrict__ bids, int64_t nb,
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restr
 #pragma unroll
             for (int c = 0; c < NV; ++c) acc[q][c] = 0.0;
         }
-#pragma unroll 4
+#pragma unroll kBndUnroll
         for (int e = 0; e < mi; ++e) {
             const int64_t j = __ldg(bidx + off + e);
             const double c = __ldg(bcw + off + e);
