@@ -167,6 +167,7 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->err = k.take<int64_t>(4);
     c->stab = k.take<unsigned long long>(1);
     c->scan_tmp = k.take<int64_t>(1024);
+    c->blk_tmp = k.take<int32_t>(1024);
     c->g.cell_of = k.take<int32_t>(N);
     c->g.cell_cnt = k.take<int32_t>(c->ncell);
     c->g.cell_start = k.take<int32_t>(c->ncell + 1);

@@ -124,6 +124,7 @@ struct bgk_ctx {
     int rows_nchunk;    // velocity chunks of kRowsR nodes along v_1
     int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)
     int64_t* scan_tmp;  // [1024]
+    int32_t* blk_tmp;   // [1024] per-block partial counts of the multi-block scans
     bgk::Geo g;
     // host-side error state
     char msg[256];

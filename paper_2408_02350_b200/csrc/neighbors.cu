@@ -8,10 +8,13 @@
 //   k_cell_assign  particle -> cell (edge >= h, 3^d sweep suffices), counts
 //   k_scan         exclusive scan of cell counts (single block)
 //   k_cell_fill    scatter particle ids into cells, k_cell_sort: ascending per cell
-//   k_compact      interior particles in cell order -> transport processing order
+//   k_compact_*    interior particles in cell order -> transport processing order (multi-block)
 //   k_nb_count     warp per particle: lanes test the 3^d cells' candidates, ballot+popc
 //   k_scan         exclusive scan of counts -> CSR offsets (int64)
 //   k_nb_fill      warp per particle: ballot compaction into shared memory, rank sort, store
+#include <algorithm>
+#include <climits>
+
 #include "bgk_internal.cuh"
 #include "cells.cuh"
 
@@ -92,11 +95,30 @@ __global__ void k_cell_fill(int64_t N, const int32_t* __restrict__ cell_of, cons
     cell_pts[pos] = (int32_t)i;
 }
 
+// ascending particle ids inside each cell: one warp per cell, rank sort of up to 64 ids held two
+// per lane (ids are distinct, so rank = number of smaller ids); larger cells fall back to an
+// insertion sort by one lane
 __global__ void k_cell_sort(int ncell, const int32_t* __restrict__ cell_start, int32_t* __restrict__ cell_pts) {
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (c >= ncell) return;
-    int b = cell_start[c], e = cell_start[c + 1];
-    for (int q = b + 1; q < e; ++q) {  // insertion sort, cells hold a few dozen points
+    const int b = cell_start[c], e = cell_start[c + 1], n = e - b;
+    if (n <= 64) {
+        const int v0 = lane < n ? cell_pts[b + lane] : INT_MAX;
+        const int v1 = lane + 32 < n ? cell_pts[b + lane + 32] : INT_MAX;
+        int r0 = 0, r1 = 0;
+        for (int k = 0; k < 32; ++k) {
+            const int u0 = __shfl_sync(0xffffffffu, v0, k), u1 = __shfl_sync(0xffffffffu, v1, k);
+            r0 += (u0 < v0) + (u1 < v0);
+            r1 += (u0 < v1) + (u1 < v1);
+        }
+        __syncwarp();
+        if (lane < n) cell_pts[b + r0] = v0;
+        if (lane + 32 < n) cell_pts[b + r1] = v1;
+        return;
+    }
+    if (lane != 0) return;
+    for (int q = b + 1; q < e; ++q) {
         int v = cell_pts[q], r = q - 1;
         while (r >= b && cell_pts[r] > v) {
             cell_pts[r + 1] = cell_pts[r];
@@ -106,41 +128,106 @@ __global__ void k_cell_sort(int ncell, const int32_t* __restrict__ cell_start, i
     }
 }
 
-// order = interior particles in cell order (stable compaction, one block)
-__global__ void __launch_bounds__(kScanThreads) k_compact(const int32_t* __restrict__ cell_pts,
-                                                           const int8_t* __restrict__ kind, int64_t n,
-                                                           int32_t* __restrict__ order) {
-    __shared__ int64_t wsum[32];
-    const int t = threadIdx.x;
-    const int64_t chunk = (n + kScanThreads - 1) / kScanThreads;
-    const int64_t b = t * chunk, e = min(n, b + chunk);
-    int64_t local = 0;
-    for (int64_t i = b; i < e; ++i) local += (kind[cell_pts[i]] == 0);
-    const int lane = t & 31, wid = t >> 5;
-    int64_t v = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int64_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-    }
-    if (lane == 31) wsum[wid] = v;
+// exclusive scan of n int32 counts into out[0..n] (int64) with many blocks: per-block sums, a
+// single-block scan of the sums, then each block scans its chunk from its offset
+__global__ void __launch_bounds__(256) k_bsum(const int32_t* __restrict__ in, int64_t n, int64_t chunk,
+                                              int32_t* __restrict__ bsum) {
+    __shared__ int wsum[8];
+    const int64_t b = blockIdx.x * chunk, e = min(n, b + chunk);
+    int acc = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += 256) acc += in[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
     __syncthreads();
-    if (wid == 0) {
-        int64_t w = wsum[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int64_t u = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += u;
-        }
-        wsum[lane] = w;
-    }
-    __syncthreads();
-    int64_t run = v - local + (wid > 0 ? wsum[wid - 1] : 0);
-    for (int64_t i = b; i < e; ++i) {
-        int p = cell_pts[i];
-        if (kind[p] == 0) order[run++] = p;
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < 8; ++w) t += wsum[w];
+        bsum[blockIdx.x] = t;
     }
 }
+
+__global__ void __launch_bounds__(256) k_bscan(const int32_t* __restrict__ in, int64_t n, int64_t chunk,
+                                               const int64_t* __restrict__ boff, int64_t nblk,
+                                               int64_t* __restrict__ out) {
+    __shared__ int64_t wsum[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t base = boff[blockIdx.x];
+    const int64_t b = blockIdx.x * chunk, e = min(n, b + chunk);
+    for (int64_t i0 = b; i0 < e; i0 += 256) {
+        const int64_t i = i0 + threadIdx.x;
+        const int64_t v = i < e ? in[i] : 0;
+        int64_t x = v;                                       // inclusive warp scan
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += u;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        int64_t before = 0, total = 0;
+        for (int w = 0; w < 8; ++w) {
+            before += w < wid ? wsum[w] : 0;
+            total += wsum[w];
+        }
+        if (i < e) out[i] = base + before + x - v;
+        base += total;
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = boff[nblk];
+}
+
+void scan_counts(bgk_ctx* c, const int32_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+    const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(1000, (n + 2047) / 2048));
+    const int64_t chunk = (n + nblk - 1) / nblk;
+    k_bsum<<<(unsigned)nblk, 256, 0, s>>>(in, n, chunk, c->blk_tmp);
+    k_scan<int64_t><<<1, kScanThreads, 0, s>>>(c->blk_tmp, c->scan_tmp, nblk);
+    k_bscan<<<(unsigned)nblk, 256, 0, s>>>(in, n, chunk, c->scan_tmp, nblk, out);
+}
+
+// order = interior particles in cell order, multi-block stable compaction: per-block counts, a scan
+// of the counts (k_scan), then each block writes its interior ids at its offset in order
+__global__ void __launch_bounds__(256) k_compact_count(const int32_t* __restrict__ cell_pts,
+                                                       const int8_t* __restrict__ kind, int64_t n, int64_t chunk,
+                                                       int32_t* __restrict__ bcnt) {
+    __shared__ int wsum[8];
+    const int64_t b = blockIdx.x * chunk, e = min(n, b + chunk);
+    int cnt = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += 256) cnt += kind[cell_pts[i]] == 0;
+    cnt = warp_sum(cnt);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < 8; ++w) t += wsum[w];
+        bcnt[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_compact_write(const int32_t* __restrict__ cell_pts,
+                                                       const int8_t* __restrict__ kind, int64_t n, int64_t chunk,
+                                                       const int64_t* __restrict__ boff, int32_t* __restrict__ order) {
+    __shared__ int wsum[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t base = boff[blockIdx.x];
+    const int64_t b = blockIdx.x * chunk, e = min(n, b + chunk);
+    for (int64_t i0 = b; i0 < e; i0 += 256) {               // 256 ids per round, in order
+        const int64_t i = i0 + threadIdx.x;
+        const int p = i < e ? cell_pts[i] : 0;
+        const bool keep = i < e && kind[p] == 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < 8; ++w) {
+            before += w < wid ? wsum[w] : 0;
+            total += wsum[w];
+        }
+        if (keep) order[base + before + __popc(bal & ((1u << lane) - 1u))] = p;
+        base += total;
+        __syncthreads();
+    }
+}
+
 
 template <int D, bool FILL>
 __global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, const int32_t* __restrict__ cell_of,
@@ -214,7 +301,7 @@ __global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, 
 
 }  // namespace
 
-int launches_neighbors() { return 8; }
+int launches_neighbors() { return 12; }
 
 void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
     const int64_t N = c->N;
@@ -230,8 +317,14 @@ void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
                                            c->nc[0], c->nc[1], 1, c->g.cell_of, c->g.cell_cnt, c->err);
     k_scan<int32_t><<<1, kScanThreads, 0, s>>>(c->g.cell_cnt, c->g.cell_start, c->ncell);
     k_cell_fill<<<nb, tpb, 0, s>>>(N, c->g.cell_of, c->g.cell_start, c->g.cell_fill, c->g.cell_pts);
-    k_cell_sort<<<(c->ncell + 127) / 128, 128, 0, s>>>(c->ncell, c->g.cell_start, c->g.cell_pts);
-    k_compact<<<1, kScanThreads, 0, s>>>(c->g.cell_pts, c->kind, N, c->g.order);
+    k_cell_sort<<<(c->ncell + 3) / 4, 128, 0, s>>>(c->ncell, c->g.cell_start, c->g.cell_pts);
+    {
+        const int64_t nblk = std::min<int64_t>(1000, (N + 2047) / 2048);
+        const int64_t chunk = (N + nblk - 1) / nblk;
+        k_compact_count<<<(unsigned)nblk, 256, 0, s>>>(c->g.cell_pts, c->kind, N, chunk, c->g.nb_cnt);
+        k_scan<int64_t><<<1, kScanThreads, 0, s>>>(c->g.nb_cnt, c->scan_tmp, nblk);
+        k_compact_write<<<(unsigned)nblk, 256, 0, s>>>(c->g.cell_pts, c->kind, N, chunk, c->scan_tmp, c->g.order);
+    }
     const int wpb = 8;
     const unsigned nbw = (unsigned)((N + wpb - 1) / wpb);
     const size_t smem = sizeof(int32_t) * wpb * c->max_nb;
@@ -239,7 +332,7 @@ void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
         k_neighbors<3, false><<<nbw, wpb * 32, 0, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
                                                       c->g.cell_pts, c->nc[0], c->nc[1], c->nc[2], c->max_nb,
                                                       c->g.nb_cnt, nullptr, nullptr, c->cap, c->err);
-        k_scan<int64_t><<<1, kScanThreads, 0, s>>>(c->g.nb_cnt, c->g.nb_off, N);
+        scan_counts(c, c->g.nb_cnt, c->g.nb_off, N, s);
         k_neighbors<3, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
                                                         c->g.cell_pts, c->nc[0], c->nc[1], c->nc[2], c->max_nb,
                                                         c->g.nb_cnt, c->g.nb_off, c->g.nb_idx, c->cap, c->err);
@@ -247,7 +340,7 @@ void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
         k_neighbors<2, false><<<nbw, wpb * 32, 0, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
                                                       c->g.cell_pts, c->nc[0], c->nc[1], 1, c->max_nb,
                                                       c->g.nb_cnt, nullptr, nullptr, c->cap, c->err);
-        k_scan<int64_t><<<1, kScanThreads, 0, s>>>(c->g.nb_cnt, c->g.nb_off, N);
+        scan_counts(c, c->g.nb_cnt, c->g.nb_off, N, s);
         k_neighbors<2, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
                                                         c->g.cell_pts, c->nc[0], c->nc[1], 1, c->max_nb,
                                                         c->g.nb_cnt, c->g.nb_off, c->g.nb_idx, c->cap, c->err);
