@@ -798,72 +798,72 @@ __global__ void __launch_bounds__(128) k_pair_union(const int32_t* __restrict__ 
     }
 }
 
-// 2D tail columns (N_v = 32: the 33rd column): thread per (interior particle, chunk of R nodes
-// along v_1), looping over its neighbours with the pair record held in registers; the same
-// arithmetic as k_transport (C/2 = sum_e min(y_e, 0), Q and sum C for g1 and g2, the factor 2 in
-// the epilogue).  Moment partials go to slot nchunk*ncg + chunk of the particle.
+// 2D tail columns (N_v = 32: the 33rd column): warp per (interior particle, chunk of R nodes along
+// v_1), lane r owning row k1s + r, looping over the neighbours (pair record and neighbour index
+// broadcast, one 16-B load of (g1, g2) per lane); the same arithmetic as k_transport (C/2 =
+// sum_e min(y_e, 0), Q and sum C for g1 and g2, the factor 2 in the epilogue).  Moment partials
+// go to slot nchunk*ncg + chunk of the particle.
 template <int R>
 __global__ void __launch_bounds__(128) k_transport_tail(const TArgs A, int tail0, int nchunk) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // warp per (interior particle, chunk): lane r owns node row k1s + r of each tail column
+    static_assert(R <= 32, "one row per lane");
+    const int lane = threadIdx.x & 31;
+    const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
     if (t >= A.n_int * nchunk) return;
     const int64_t pos = t / nchunk;
     const int chunk = (int)(t - pos * nchunk);
     const int p = A.order[pos];
     const int k1s = chunk * R;
+    const bool row_ok = lane < R && k1s + lane < A.n1;
+    const int k1 = row_ok ? k1s + lane : k1s;
     const int64_t off = A.nb_off[p];
     const int m = (int)(A.nb_off[p + 1] - off);
     const double W0 = A.W[(int64_t)p * 2], W1 = A.W[(int64_t)p * 2 + 1];
     const int64_t rowstride = (int64_t)A.ncs * 2;
+    const double v1 = axis_node(A.vmax, A.dv, k1);
+    const double c1 = v1 - W0;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, sE = 0.0, amax = 0.0;
     for (int col = tail0; col < A.ncol; ++col) {
         const double v2 = axis_node(A.vmax, A.dv, A.c0 + col);
         const double c2 = v2 - W1;
-        double Q0[R], Q1[R], Sc[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) Q0[r] = Q1[r] = Sc[r] = 0.0;
+        double Q0 = 0.0, Q1 = 0.0, Sc = 0.0;
+#pragma unroll 4
         for (int e = 0; e < m; ++e) {
             const int j = __ldg(A.nb_idx + off + e);
             const double2 pa = __ldg(reinterpret_cast<const double2*>(A.P + (off + e) * 4));
             const double2 pb = __ldg(reinterpret_cast<const double2*>(A.P + (off + e) * 4 + 2));
-            const double4 pv = make_double4(pa.x, pa.y, pb.x, pb.y);
-            const double yn0 = fma(pv.y, c2, pv.x * (axis_node(A.vmax, A.dv, k1s) - W0));
-            const double yt0 = fma(pv.w, c2, pv.z * (axis_node(A.vmax, A.dv, k1s) - W0));
-            const double dyn = A.dv * pv.x, dyt = A.dv * pv.z;
-            const double2* fj = reinterpret_cast<const double2*>(A.f + (int64_t)j * A.n1 * rowstride) + col;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                if (k1s + r >= A.n1) break;
-                const double C = neg_part(fma((double)r, dyn, yn0)) + neg_part(fma((double)r, dyt, yt0));
-                const double2 g = __ldg(fj + (int64_t)(k1s + r) * A.ncs);
-                Q0[r] = fma(C, g.x, Q0[r]);
-                Q1[r] = fma(C, g.y, Q1[r]);
-                Sc[r] += C;
-            }
+            const double C = neg_part(fma(pa.y, c2, pa.x * c1)) + neg_part(fma(pb.y, c2, pb.x * c1));
+            const double2 g = __ldg(reinterpret_cast<const double2*>(A.f + ((int64_t)j * A.n1 + k1) * rowstride) + col);
+            Q0 = fma(C, g.x, Q0);
+            Q1 = fma(C, g.y, Q1);
+            Sc += C;
         }
-        const double2* fi = reinterpret_cast<const double2*>(A.f + (int64_t)p * A.n1 * rowstride) + col;
-        double2* fo = reinterpret_cast<double2*>(A.ft + (int64_t)p * A.n1 * rowstride) + col;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            if (k1s + r >= A.n1) break;
-            const double v1 = axis_node(A.vmax, A.dv, k1s + r);
-            const double2 fv = __ldg(fi + (int64_t)(k1s + r) * A.ncs);
-            const double o0 = fv.x - 2.0 * A.dt * (Q0[r] - fv.x * Sc[r]);
-            const double o1 = fv.y - 2.0 * A.dt * (Q1[r] - fv.y * Sc[r]);
-            fo[(int64_t)(k1s + r) * A.ncs] = make_double2(o0, o1);
+        if (row_ok) {
+            const double2 fv = __ldg(reinterpret_cast<const double2*>(A.f + ((int64_t)p * A.n1 + k1) * rowstride) + col);
+            const double o0 = fv.x - 2.0 * A.dt * (Q0 - fv.x * Sc);
+            const double o1 = fv.y - 2.0 * A.dt * (Q1 - fv.y * Sc);
+            reinterpret_cast<double2*>(A.ft + ((int64_t)p * A.n1 + k1) * rowstride)[col] = make_double2(o0, o1);
             s0 += o0;
             s1 += v1 * o0;
             s2 += v2 * o0;
             sE += (v1 * v1 + v2 * v2) * o0 + o1;
-            amax = fmax(amax, -2.0 * Sc[r]);
+            amax = fmax(amax, -2.0 * Sc);
         }
     }
-    double* pp = A.partials + ((int64_t)p * A.nwpp + (int64_t)nchunk * A.ncg + chunk) * kPM;
-    pp[0] = s0;
-    pp[1] = s1;
-    pp[2] = s2;
-    pp[3] = sE;
-    pp[4] = 0.0;
-    atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    sE = warp_sum(sE);
+    amax = warp_max(amax);
+    if (lane == 0) {
+        double* pp = A.partials + ((int64_t)p * A.nwpp + (int64_t)nchunk * A.ncg + chunk) * kPM;
+        pp[0] = s0;
+        pp[1] = s1;
+        pp[2] = s2;
+        pp[3] = sE;
+        pp[4] = 0.0;
+        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+    }
 }
 
 template <int D, int R, int WPB, bool SG, int MINB = 1>
@@ -1081,8 +1081,8 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     else {
         if (c->ncg > 0) dispatch<2>(c->R, wpb, tm, a, s);
         if (c->tail_cols) {
-            const int64_t nt = c->N_int * c->nchunk;
-            const unsigned gx = (unsigned)((nt + 127) / 128);
+            const int64_t nt = c->N_int * c->nchunk;             // warps
+            const unsigned gx = (unsigned)((nt + 3) / 4);
             switch (c->R) {
                 case 17: k_transport_tail<17><<<gx, 128, 0, s>>>(a, c->ncg * 32, c->nchunk); break;
                 case 13: k_transport_tail<13><<<gx, 128, 0, s>>>(a, c->ncg * 32, c->nchunk); break;
