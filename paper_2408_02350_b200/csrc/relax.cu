@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
     constexpr int NV = (D == 2) ? 2 : 1;
     __shared__ double e[D][64];
     __shared__ double par[8];
+    extern __shared__ double colf[];            // [ncs] per stored column (dynamic)
     const int64_t bi = blockIdx.x;
     if (bi >= A.n) return;
     const int p = A.ids[bi];
@@ -144,12 +145,34 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
     }
     __syncthreads();
     const double a1 = par[0], a2 = par[1], pref = par[2], RT = par[3];
+    // per stored column: the v_2 (and v_3) factor of the separable Maxwellian, 0 on padding columns
+    for (int c = threadIdx.x; c < A.ncs; c += blockDim.x) {
+        double cf = 0.0;
+        if (c < A.ncol) {
+            const int gc = A.c0 + c;
+            if constexpr (D == 3) cf = e[1][gc / A.n1] * e[2][gc - (gc / A.n1) * A.n1];
+            else cf = e[1][gc];
+        }
+        colf[c] = cf;
+    }
+    __syncthreads();
     double2* fp2 = reinterpret_cast<double2*>(A.f + (int64_t)p * A.Ks * NV);
     // 16-byte accesses: in 3D two adjacent columns (ncs is even), in 2D the (g1, g2) pair of a node.
-    // Four independent loads in flight per thread keep enough bytes moving to stream at HBM rate.
-    const int n2 = (D == 3) ? A.Ks / 2 : A.Ks;
+    // Four independent loads in flight per thread; (row, column) of each advance incrementally
+    // (no integer division in the streaming loop).
+    const int P = (D == 3) ? A.ncs / 2 : A.ncs;              // 16-B elements per stored row
+    const int n2 = P * A.n1;
     constexpr int U = 4;
-    for (int u0 = threadIdx.x; u0 < n2; u0 += U * blockDim.x) {
+    const int stride = U * blockDim.x;
+    const int dk = stride / P, dc = stride - dk * P;
+    int kr[U], cq[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const int u = threadIdx.x + q * blockDim.x;
+        kr[q] = u / P;
+        cq[q] = u - kr[q] * P;
+    }
+    for (int u0 = threadIdx.x; u0 < n2; u0 += stride) {
         double2 g[U];
 #pragma unroll
         for (int q = 0; q < U; ++q) {
@@ -159,28 +182,25 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
 #pragma unroll
         for (int q = 0; q < U; ++q) {
             const int u = u0 + q * blockDim.x;
-            if (u >= n2) break;
-            if constexpr (D == 3) {
-                const int t = 2 * u;
-                const int k1 = t / A.ncs, col = t - k1 * A.ncs, gc = A.c0 + col;
-                const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-                const double base = pref * e[0][k1] * e[1][k2];
-                const double M0 = base * e[2][k3];
-                // the second column may be the next v_2 line (k3 = n1-1 -> 0) or the padding column
-                double M1 = 0.0;
-                if (col + 1 < A.ncol) {
-                    const int gc1 = gc + 1, k21 = gc1 / A.n1, k31 = gc1 - k21 * A.n1;
-                    M1 = pref * e[0][k1] * e[1][k21] * e[2][k31];
+            if (u < n2) {
+                const double rowf = pref * e[0][kr[q]];
+                if constexpr (D == 3) {
+                    const int col = 2 * cq[q];
+                    g[q].x = a1 * g[q].x + a2 * (rowf * colf[col]);
+                    g[q].y = col + 1 < A.ncol ? a1 * g[q].y + a2 * (rowf * colf[col + 1]) : 0.0;
+                } else {
+                    const double M = rowf * colf[cq[q]];
+                    g[q].x = a1 * g[q].x + a2 * M;
+                    g[q].y = a1 * g[q].y + a2 * (RT * M);
                 }
-                g[q].x = a1 * g[q].x + a2 * M0;
-                g[q].y = (col + 1 < A.ncol) ? a1 * g[q].y + a2 * M1 : 0.0;
-            } else {
-                const int k1 = u / A.ncs, col = u - k1 * A.ncs;
-                const double M = pref * e[0][k1] * e[1][A.c0 + col];
-                g[q].x = a1 * g[q].x + a2 * M;
-                g[q].y = a1 * g[q].y + a2 * (RT * M);
+                fp2[u] = g[q];
             }
-            fp2[u] = g[q];
+            cq[q] += dc;
+            kr[q] += dk;
+            if (cq[q] >= P) {
+                cq[q] -= P;
+                ++kr[q];
+            }
         }
     }
 }
@@ -511,8 +531,9 @@ void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
     a.dmol = c->cfg.dmol;
     a.L = c->cfg.L;
     a.clamp_eps = 1e-3 * c->cfg.dx;
-    if (c->d == 3) k_relax<3><<<(unsigned)c->N_int, 256, 0, s>>>(a);
-    else k_relax<2><<<(unsigned)c->N_int, 256, 0, s>>>(a);
+    const size_t smem = sizeof(double) * c->ncs;   // column factors of the separable Maxwellian
+    if (c->d == 3) k_relax<3><<<(unsigned)c->N_int, 256, smem, s>>>(a);
+    else k_relax<2><<<(unsigned)c->N_int, 256, smem, s>>>(a);
 }
 
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
