@@ -98,7 +98,7 @@ struct bgk_ctx {
     double* sums;       // [N][kPM] rank-local (then all-reduced) moment sums
     double* wallpart;   // [N_b][bnd_nch]
     double* wallnum;    // [N] rank-local (then all-reduced) incoming wall flux
-    double* Mw;         // [2d][RS] wall Maxwellians M(1, U_w, T_w) on the local columns
+    double* Mw;         // [2d][RS] wall Maxwellians M(1, U_w, T_w) on the outgoing nodes of each wall, -1 elsewhere
     double* wall_den;   // [2d] sum_{v.n>0} (v.n) M_w over the GLOBAL grid
     double* outbuf;     // [N][d+2] scratch for moments / copies
     int64_t* err;       // [4] code, particle, needed, spare

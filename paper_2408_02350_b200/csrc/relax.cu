@@ -259,11 +259,14 @@ __global__ void k_wall_M(double* __restrict__ Mw, int n1, int ncol, int ncs, int
                          double dv, double R, double Twall, double lid0, double lid1, double lid2) {
     constexpr int NV = (D == 2) ? 2 : 1;
     const int wid = blockIdx.y + 1;
+    const int axis = (wid - 1) / 2;
+    const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
     const double U[3] = {wid == 2 * D ? lid0 : 0.0, wid == 2 * D ? lid1 : 0.0, wid == 2 * D ? lid2 : 0.0};
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Ks; t += (int64_t)gridDim.x * blockDim.x) {
         double v[3];
-        double M[2] = {0.0, 0.0};
-        if (node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) maxwellian_at<D>(1.0, U, Twall, R, v, M);
+        double M[2] = {-1.0, -1.0};    // -1: not an outgoing node of this wall (k_bnd_fill skips it)
+        if (node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v) && sgn * v[axis] > 0.0)
+            maxwellian_at<D>(1.0, U, Twall, R, v, M);
 #pragma unroll
         for (int q = 0; q < NV; ++q) Mw[((int64_t)blockIdx.y * Ks + t) * NV + q] = M[q];
     }
@@ -407,10 +410,12 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_fill(const int32_t* __restric
     const double rho_w = -wallnum[b] / den[wid - 1];
     const double* Mrow = Mw + (int64_t)(wid - 1) * Kloc * NV;
     double* frow = f + (int64_t)b * Kloc * NV;
+    // the wall table holds M(1, U_w, T_w) on the wall's outgoing nodes and -1 elsewhere (k_wall_M)
+    (void)axis;
+    (void)sgn;
     for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
-        double v[3];
-        if (!node_vel_s<D>(t, ncs, ncol, c0, n1, vmax, dv, v)) continue;
-        if (!(sgn * v[axis] > 0.0)) continue;
+        const double m0 = Mrow[t * NV];
+        if (m0 < 0.0) continue;
 #pragma unroll
         for (int q = 0; q < NV; ++q) frow[t * NV + q] = rho_w * Mrow[t * NV + q];
     }
