@@ -68,7 +68,7 @@ typedef struct bgk_config {
     int32_t dims;        /* 2 = Chu-reduced 2D model (values g1, g2), 3 = full 3D model */
     int32_t Nv;          /* velocity cells per axis, 2..63: Nv+1 nodes per axis; odd Nv
                           * (no zero node) as in the paper's Figs. 6-7 (Nv = 15) */
-    double vmax;         /* velocity bound; > 0 */
+    double vmax;         /* velocity bound; <= 0: |U_lid| + 4 sqrt(R T_wall) (Z4) */
     double L;            /* cavity edge [m] */
     double h;            /* neighbour radius [m], h = 3.1 dx */
     double h2;           /* h*h exactly as the caller computed it; neighbour test d2 <= h2 */
@@ -108,15 +108,19 @@ typedef struct bgk_config {
 bgk_status bgk_workspace_size(const bgk_config* cfg, int64_t N, size_t* bytes);
 
 /* Create a context and fill the initial state.
- *   x      : host or device, N*dims fp64 positions (row-major [N][dims]), inside [0, L]^dims.
- *   kind   : host or device, N int8 (0 interior, 1..2*dims wall id).
+ *   x      : host or device, N*dims fp64 positions (row-major [N][dims]), inside [0, L]^dims;
+ *            or NULL (with kind NULL) for the regular cavity lattice of n = L/dx + 1 points per
+ *            axis (N must be n^dims): index ix + n iy (+ n^2 iz), coordinates i dx (the last one
+ *            exactly L), face points are boundary particles of the lowest wall id they lie on.
+ *   kind   : host or device, N int8 (0 interior, 1..2*dims wall id), or NULL with x.
  *   macro0 : host or device, N*(dims+2) fp64 initial (rho, U[dims], T) per particle, or NULL for
  *            the uniform state (rho, U, T) = (1, 0, T_wall).  f^0 = M(rho^0, U^0, T^0) at every
  *            particle; the transport velocity W^0 = U^0 (ALE) or 0 (fixed cloud).
  *   workspace, ws_bytes : caller-owned device memory of at least bgk_workspace_size bytes,
  *            16-byte aligned; it must outlive the context.
- * Errors: BGK_E_INVALID_ARG (dims not 2/3, Nv < 2 or > 63, vmax <= 0, N < 1, bad column
- * range, workspace too small), BGK_E_OUT_OF_DOMAIN.  Synchronises the stream. */
+ * Errors: BGK_E_INVALID_ARG (dims not 2/3, Nv < 2 or > 63, vmax NaN, N < 1, bad column
+ * range, workspace too small, x == NULL with N not a lattice size), BGK_E_OUT_OF_DOMAIN.
+ * Synchronises the stream. */
 bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* kind,
                           const double* macro0, int64_t N, void* workspace, size_t ws_bytes,
                           bgk_stream stream, bgk_ctx** out);

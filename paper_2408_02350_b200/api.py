@@ -66,7 +66,7 @@ class Bgk:
         self.nval = 2 if cfg.dims == 2 else 1
         self.device = torch.device(device if device is not None else "cuda")
         self.c = make_config(cfg, col_range, max_neighbors, dt)
-        N = int(len(cloud["x"]))
+        N = int(len(cloud["x"])) if cloud.get("x") is not None else cfg.n_particles
         self._N = N
         n1 = cfg.Nv + 1
         ncol_g = n1 ** (cfg.dims - 1)
@@ -77,8 +77,9 @@ class Bgk:
         nbytes = C.c_size_t(0)
         self._check(self.L.bgk_workspace_size(C.byref(self.c), N, C.byref(nbytes)), ctx=False)
         self.ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
-        x = np.ascontiguousarray(cloud["x"], dtype=np.float64)
-        kind = np.ascontiguousarray(cloud["kind"], dtype=np.int8)
+        lattice = cloud.get("x") is None                     # the library builds the regular lattice
+        x = None if lattice else np.ascontiguousarray(cloud["x"], dtype=np.float64)
+        kind = None if lattice else np.ascontiguousarray(cloud["kind"], dtype=np.int8)
         macro0 = None
         if "rho" in cloud:
             macro0 = np.ascontiguousarray(np.column_stack([cloud["rho"], cloud["U"], cloud["T"]]), dtype=np.float64)

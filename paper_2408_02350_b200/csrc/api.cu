@@ -30,11 +30,34 @@ struct Carver {
     }
 };
 
+// x == NULL at bgk_init_cloud: the regular cavity lattice, n = L/dx + 1 points
+// per axis, index = ix + n iy (+ n^2 iz), coordinates i dx with the last one exactly L; points on
+// a face are boundary particles of the lowest wall id they lie on (1: x=0, 2: x=L, 3: y=0, ...).
+bool make_lattice(int d, double L, double dx, int64_t N, std::vector<double>& x, std::vector<int8_t>& kind) {
+    const int64_t n = (int64_t)std::llround(L / dx) + 1;
+    int64_t nn = 1;
+    for (int a = 0; a < d; ++a) nn *= n;
+    if (n < 3 || nn != N) return false;
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t r = i;
+        int8_t k = 0;
+        for (int a = 0; a < d; ++a) {
+            const int64_t ia = r % n;
+            r /= n;
+            x[i * d + a] = ia == n - 1 ? L : (double)ia * dx;
+            const int8_t wid = ia == 0 ? (int8_t)(2 * a + 1) : (ia == n - 1 ? (int8_t)(2 * a + 2) : 0);
+            if (wid && (k == 0 || wid < k)) k = wid;
+        }
+        kind[i] = k;
+    }
+    return true;
+}
+
 bool valid_cfg(const bgk_config* c, int64_t N) {
     if (!c || N < 1) return false;
     if (c->dims != 2 && c->dims != 3) return false;
     if (c->Nv < 2 || c->Nv + 1 > 64) return false;   // odd Nv allowed: the paper's Figs. 6-7 use Nv = 15
-    if (!(c->vmax > 0.0) || !(c->L > 0.0) || !(c->h > 0.0) || !(c->h2 > 0.0) || !(c->dt >= 0.0)) return false;
+    if (std::isnan(c->vmax) || !(c->L > 0.0) || !(c->h > 0.0) || !(c->h2 > 0.0) || !(c->dt >= 0.0)) return false;
     if (!(c->R > 0.0) || !(c->kb > 0.0) || !(c->dmol > 0.0) || !(c->T_wall > 0.0) || !(c->alpha_w > 0.0)) return false;
     if (N > (int64_t)INT32_MAX || c->max_particles > (int64_t)INT32_MAX) return false;
     if (c->manage != 0 && c->manage != 1) return false;
@@ -46,6 +69,11 @@ bool valid_cfg(const bgk_config* c, int64_t N) {
 // geometry + mapping that only depends on the configuration and N
 void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->cfg = *cfg;
+    if (!(c->cfg.vmax > 0.0)) {   // v_max = |U_wall| + 4 sqrt(R T_wall)
+        const double* u = cfg->U_lid;
+        c->cfg.vmax = std::sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]) + 4.0 * std::sqrt(cfg->R * cfg->T_wall);
+    }
+    cfg = &c->cfg;
     c->d = cfg->dims;
     c->nv = c->d == 2 ? 2 : 1;
     c->n1 = cfg->Nv + 1;
@@ -314,7 +342,7 @@ bgk_status bgk_workspace_size(const bgk_config* cfg, int64_t N, size_t* bytes) {
 
 bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* kind, const double* macro0,
                           int64_t N, void* workspace, size_t ws_bytes, bgk_stream stream, bgk_ctx** out) {
-    if (!out || !x || !kind || !workspace) return BGK_E_INVALID_ARG;
+    if (!out || !workspace || (!x) != (!kind)) return BGK_E_INVALID_ARG;
     *out = nullptr;
     size_t need = 0;
     if (bgk_workspace_size(cfg, N, &need) != BGK_OK || ws_bytes < need) return BGK_E_INVALID_ARG;
@@ -330,9 +358,15 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
     // kinds and positions on the host to build the interior / boundary lists
     std::vector<int8_t> hk(N);
     std::vector<double> hx(N * c->d);
-    cudaError_t e = cudaMemcpy(hk.data(), kind, N, cudaMemcpyDefault);
-    if (e == cudaSuccess) e = cudaMemcpy(hx.data(), x, sizeof(double) * N * c->d, cudaMemcpyDefault);
-    if (e != cudaSuccess) { bgk_status st = cuda_fail(c, e); delete c; return st; }
+    cudaError_t e = cudaSuccess;
+    if (x) {
+        e = cudaMemcpy(hk.data(), kind, N, cudaMemcpyDefault);
+        if (e == cudaSuccess) e = cudaMemcpy(hx.data(), x, sizeof(double) * N * c->d, cudaMemcpyDefault);
+        if (e != cudaSuccess) { bgk_status st = cuda_fail(c, e); delete c; return st; }
+    } else if (!make_lattice(c->d, cfg->L, cfg->dx, N, hx, hk)) {
+        delete c;
+        return BGK_E_INVALID_ARG;
+    }
     for (int64_t i = 0; i < N; ++i)
         if (hk[i] < 0 || hk[i] > 2 * c->d) { delete c; return BGK_E_INVALID_ARG; }
     {
@@ -345,7 +379,7 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
     cudaMemsetAsync(c->f[0], 0, sizeof(double) * N * c->RS, s);
     cudaMemsetAsync(c->f[1], 0, sizeof(double) * N * c->RS, s);
     cudaMemsetAsync(c->stab, 0, sizeof(unsigned long long), s);
-    cudaMemcpyAsync(c->x, x, sizeof(double) * N * c->d, cudaMemcpyDefault, s);
+    cudaMemcpyAsync(c->x, hx.data(), sizeof(double) * N * c->d, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(c->kind, hk.data(), N, cudaMemcpyHostToDevice, s);
     const double* m0 = nullptr;
     if (macro0) {

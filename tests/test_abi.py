@@ -51,7 +51,7 @@ def test_invalid_configs_rejected(lib):
     import bgk_inputs as bi
     from paper_2408_02350_b200.api import make_config
     nb = C.c_size_t(0)
-    for bad in (dict(Nv=1), dict(Nv=64), dict(Nv=0), dict(dims=4), dict(vmax=-1.0)):
+    for bad in (dict(Nv=1), dict(Nv=64), dict(Nv=0), dict(dims=4), dict(vmax=float("nan"))):
         cfg = bi.C1.replace(**{k: v for k, v in bad.items()})
         c = make_config(cfg)
         assert lib.bgk_workspace_size(C.byref(c), 441, C.byref(nb)) == 1

@@ -434,3 +434,19 @@ def test_lattice_rows_c5_sampled(torch_cuda):
     rows = fbuf[torch.tensor(sample, device=fbuf.device)].reshape(len(sample), -1).cpu().numpy()
     for q, i in enumerate(sample):
         assert rel(rows[q], ref[i]["f"]) <= TOL, (i, rel(rows[q], ref[i]["f"]))
+
+
+def test_library_lattice_and_default_vmax(torch_cuda):
+    """bgk_init_cloud with x = kind = NULL builds the regular cavity lattice itself (same points,
+    order and wall ids as bgk_inputs.lattice), and vmax <= 0 defaults to |U_lid| + 4 sqrt(R T0)."""
+    from paper_2408_02350_b200 import Bgk
+    cfg = bi.C1
+    cloud = bi.make_cloud(cfg)
+    lib_cloud = {"rho": cloud["rho"], "U": cloud["U"], "T": cloud["T"]}
+    g = Bgk(cfg.replace(vmax=-1.0), lib_cloud, device="cuda:0")
+    assert np.array_equal(g.positions(), cloud["x"])
+    assert np.array_equal(g.kinds(), cloud["kind"])
+    g.step(2)
+    h, _ = gpu(cfg, cloud)
+    h.step(2)
+    assert np.array_equal(g.get_f(), h.get_f())
