@@ -216,6 +216,16 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->gUlen = k.take<int32_t>(4 * ng);
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
+    {
+        const char* e = getenv("BGK_BND_G");        // boundary interpolation groups: 4 (default), 8, 0 = per particle
+        c->bnd_g = e ? atoi(e) : 4;
+        if (c->bnd_g != 4 && c->bnd_g != 8) c->bnd_g = 0;
+        c->bu_cap = c->bnd_g ? std::min(c->bnd_g * c->max_nb, 512) : 1;   // union rows per group (CAPACITY beyond)
+        const size_t ng = c->bnd_g ? (size_t)N / c->bnd_g + 1 : 1;
+        c->bu_j = k.take<int32_t>(ng * c->bu_cap);
+        c->bu_w = k.take<double>(ng * c->bu_cap * std::max(c->bnd_g, 1));
+        c->bu_n = k.take<int32_t>(ng);
+    }
     c->rows_p0 = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
     c->rows_stride = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
     c->rows_perm = k.take<int16_t>(c->rows_on ? ((size_t)N / kRowsG + 1) * 256 : 1);
@@ -308,6 +318,7 @@ bgk_status ensure_geometry(bgk_ctx* c, cudaStream_t s) {
             if (changed) launch_build_neighbors(c, s);
         }
         launch_wls(c, s);
+        launch_bnd_union(c, s);
         launch_group_union(c, s);
         c->geometry_valid = true;
         c->rows_built = false;

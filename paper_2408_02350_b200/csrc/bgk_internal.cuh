@@ -108,6 +108,13 @@ struct bgk_ctx {
     int ucap;
     bgk::Manage mg;     // particle-management scratch (cfg.manage)
     double* stage;      // [Ncap][nv*Kloc] canonical input staging buffer (cfg.staging)
+    // grouped boundary interpolation (relax.cu, BGK_BND_G): union of bnd_g consecutive boundary
+    // particles' interior neighbours and the dense weight matrix, rebuilt with the geometry
+    int bnd_g;          // 0: per-particle kernel; 4 or 8
+    int bu_cap;
+    int32_t* bu_j;      // [groups][bu_cap]
+    double* bu_w;       // [groups][bu_cap][bnd_g]
+    int32_t* bu_n;      // [groups]
     cudaEvent_t ev_staged, ev_consumed;
     bool stage_pending;
     int64_t mg_report[6];   // host copy of the last pass's report
@@ -178,6 +185,7 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
 void launch_moment_reduce(bgk_ctx* c, cudaStream_t s);
 void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s);
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s);
+void launch_bnd_union(bgk_ctx* c, cudaStream_t s);
 void launch_boundary_fill(bgk_ctx* c, double* fnew, cudaStream_t s);
 void launch_wall_tables(bgk_ctx* c, cudaStream_t s);
 void launch_init_f(bgk_ctx* c, const double* macro0, cudaStream_t s);

@@ -386,6 +386,200 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restr
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Boundary interpolation by groups of G consecutive particles of the face-sorted boundary list
+// (BGK_BND_G = 4, the default / 8; 0 = the per-particle kernel above).  C5: 2.83 ms at G = 4
+// against 3.20 ms per particle and 3.27 ms at G = 8 (the FMAs grow with G, the row loads shrink).  k_bnd_union (per geometry build) merges
+// their compacted (neighbour, weight) lists into one union with a dense G-column weight matrix;
+// k_bnd_interp_u loads each union row's chunk ONCE for the group and applies it to every member
+// (weight 0 if not its neighbour): fewer row loads for more FMAs.
+// ---------------------------------------------------------------------------------------------
+template <int G>
+__global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ bids, int64_t nb,
+                                                   const int64_t* __restrict__ nb_off,
+                                                   const int32_t* __restrict__ bidx, const double* __restrict__ bcw,
+                                                   const int32_t* __restrict__ bcnt, int cap,
+                                                   int32_t* __restrict__ bu_j, double* __restrict__ bu_w,
+                                                   int32_t* __restrict__ bu_n, int64_t* err) {
+    extern __shared__ int32_t keys[];                       // [2 n2]: sorted (j << 3 | q), then union slots
+    __shared__ int s_len[G + 1];
+    __shared__ int s_n;
+    const int64_t g = blockIdx.x;
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int q = 0; q < G; ++q) {
+            s_len[q] = tot;
+            const int64_t bi = g * G + q;
+            if (bi < nb) tot += bcnt[bids[bi]];
+        }
+        s_len[G] = tot;
+    }
+    __syncthreads();
+    const int tot = s_len[G];
+    int n2 = 1;
+    while (n2 < tot) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) keys[i] = INT_MAX;
+    __syncthreads();
+    for (int q = 0; q < G; ++q) {
+        const int64_t bi = g * G + q;
+        if (bi >= nb) break;
+        const int b = bids[bi];
+        const int64_t off = nb_off[b];
+        for (int i = threadIdx.x; i < bcnt[b]; i += blockDim.x) keys[s_len[q] + i] = (bidx[off + i] << 3) | q;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const int a = keys[i], b = keys[ixj];
+                    if ((a > b) == ((i & k) == 0)) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    int32_t* upos = keys + n2;
+    if (threadIdx.x == 0) {
+        int u = -1, prev = -1;
+        for (int i = 0; i < tot; ++i) {
+            const int j = keys[i] >> 3;
+            if (j != prev) {
+                ++u;
+                prev = j;
+                if (u < cap) bu_j[g * cap + u] = j;
+            }
+            upos[i] = u;
+        }
+        s_n = u + 1;
+        if (u + 1 > cap) latch_error(err, BGK_E_CAPACITY, bids[g * G]);
+        bu_n[g] = u + 1 > cap ? 0 : u + 1;
+    }
+    __syncthreads();
+    if (s_n > cap) return;
+    double* W = bu_w + g * cap * G;
+    for (int i = threadIdx.x; i < s_n * G; i += blockDim.x) W[i] = 0.0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+        const int j = keys[i] >> 3, q = keys[i] & 7;
+        const int b = bids[g * G + q];
+        const int64_t off = nb_off[b];
+        int lo = 0, hi = bcnt[b] - 1;                       // compacted lists are ascending in j
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (bidx[off + mid] < j) lo = mid + 1;
+            else hi = mid;
+        }
+        W[upos[i] * G + q] = bcw[off + lo];
+    }
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(kBndChunk) k_bnd_interp_u(const int32_t* __restrict__ bids, int64_t nb,
+                                                            const int8_t* __restrict__ kind,
+                                                            const int32_t* __restrict__ bu_j,
+                                                            const double* __restrict__ bu_w,
+                                                            const int32_t* __restrict__ bu_n, int cap,
+                                                            double* __restrict__ f, double* __restrict__ wallpart,
+                                                            int nch, int n1, int ncol, int ncs, int c0, int64_t Kloc,
+                                                            double vmax, double dv) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    constexpr int NPT = 2;
+    extern __shared__ double sW[];                          // [U][G] weights, then [U] rows
+    __shared__ double sh[32];
+    const int64_t g = blockIdx.x;
+    const int U = bu_n[g];
+    int32_t* sJ = reinterpret_cast<int32_t*>(sW + (size_t)cap * G);
+    for (int i = threadIdx.x; i < U * G; i += blockDim.x) sW[i] = bu_w[g * cap * G + i];
+    for (int i = threadIdx.x; i < U; i += blockDim.x) sJ[i] = bu_j[g * cap + i];
+    int b[G], axis[G];
+    bool live[G];
+    double sgn[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        const int64_t bi = g * G + q;
+        live[q] = bi < nb;
+        b[q] = live[q] ? bids[bi] : 0;
+        const int wid = live[q] ? kind[b[q]] : 1;
+        axis[q] = (wid - 1) / 2;
+        sgn[q] = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
+    }
+    int64_t t[NPT];
+    double v[NPT][3];
+    bool need[NPT], inc[G][NPT];
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+        t[n] = (int64_t)blockIdx.y * kBndChunk * NPT + n * kBndChunk + threadIdx.x;
+        v[n][0] = v[n][1] = v[n][2] = 0.0;
+        const bool in_range = t[n] < Kloc && node_vel_s<D>(t[n], ncs, ncol, c0, n1, vmax, dv, v[n]);
+        need[n] = false;
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            inc[q][n] = live[q] && in_range && sgn[q] * v[n][axis[q]] <= 0.0;
+            need[n] = need[n] || inc[q][n];
+        }
+    }
+    __syncthreads();
+    double acc[G][NPT][NV];
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int n = 0; n < NPT; ++n)
+#pragma unroll
+            for (int c = 0; c < NV; ++c) acc[q][n][c] = 0.0;
+    constexpr int UB = 4;                                   // rows in flight per thread
+    for (int u0 = 0; u0 < U; u0 += UB) {
+        double fv[UB][NPT][NV];
+#pragma unroll
+        for (int uu = 0; uu < UB; ++uu) {
+            const int u = u0 + uu;
+            const int64_t j = u < U ? sJ[u] : 0;
+#pragma unroll
+            for (int n = 0; n < NPT; ++n) {
+                const bool ld = need[n] && u < U;
+                if constexpr (NV == 1) {
+                    fv[uu][n][0] = ld ? __ldg(f + j * Kloc + t[n]) : 0.0;
+                } else {
+                    const double2 gv = ld ? __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t[n])
+                                          : make_double2(0.0, 0.0);
+                    fv[uu][n][0] = gv.x;
+                    fv[uu][n][1] = gv.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int uu = 0; uu < UB; ++uu) {
+            if (u0 + uu >= U) break;
+            const double* wu = sW + (u0 + uu) * G;
+#pragma unroll
+            for (int q = 0; q < G; ++q) {
+                const double w = wu[q];
+#pragma unroll
+                for (int n = 0; n < NPT; ++n)
+#pragma unroll
+                    for (int c = 0; c < NV; ++c) acc[q][n][c] = fma(w, fv[uu][n][c], acc[q][n][c]);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        double flux = 0.0;
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) {
+            if (!inc[q][n]) continue;
+            if constexpr (NV == 1) f[(int64_t)b[q] * Kloc + t[n]] = acc[q][n][0];
+            else reinterpret_cast<double2*>(f)[(int64_t)b[q] * Kloc + t[n]] = make_double2(acc[q][n][0], acc[q][n][1]);
+            const double vn = sgn[q] * v[n][axis[q]];
+            if (vn < 0.0) flux += vn * acc[q][n][0];
+        }
+        const double tot = block_sum<kBndChunk>(flux, sh);
+        if (threadIdx.x == 0 && live[q]) wallpart[(g * G + q) * nch + blockIdx.y] = tot;
+    }
+}
+
 __global__ void k_wall_reduce(const int32_t* __restrict__ bids, int64_t nb, const double* __restrict__ wallpart,
                               int nch, double* __restrict__ wallnum) {
     const int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -541,8 +735,44 @@ void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
     else k_relax<2><<<(unsigned)c->N_int, 256, smem, s>>>(a);
 }
 
+template <int G>
+void bnd_union_g(bgk_ctx* c, cudaStream_t s) {
+    const unsigned ng = (unsigned)((c->N_b + G - 1) / G);
+    int n2 = 1;
+    while (n2 < G * c->max_nb) n2 <<= 1;
+    k_bnd_union<G><<<ng, 256, sizeof(int32_t) * 2 * n2, s>>>(c->boundary, c->N_b, c->g.nb_off, c->g.bidx, c->g.bcw,
+                                                           c->g.bcnt, c->bu_cap, c->bu_j, c->bu_w, c->bu_n, c->err);
+}
+
+void launch_bnd_union(bgk_ctx* c, cudaStream_t s) {
+    if (!c->N_b || !c->bnd_g) return;
+    if (c->bnd_g == 4) bnd_union_g<4>(c, s);
+    else bnd_union_g<8>(c, s);
+}
+
+template <int D, int G>
+void bnd_interp_g(bgk_ctx* c, double* fnew, cudaStream_t s) {
+    const size_t smem = (size_t)c->bu_cap * (G * sizeof(double) + sizeof(int32_t));
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_bnd_interp_u<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        configured = true;
+    }
+    dim3 gg((unsigned)((c->N_b + G - 1) / G), (unsigned)c->bnd_nch);
+    k_bnd_interp_u<D, G><<<gg, kBndChunk, smem, s>>>(c->boundary, c->N_b, c->kind, c->bu_j, c->bu_w, c->bu_n,
+                                                     c->bu_cap, fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs,
+                                                     c->c0, c->Ks, c->cfg.vmax, c->dv);
+}
+
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
+    if (c->bnd_g) {
+        if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_g<3, 4>(c, fnew, s) : bnd_interp_g<3, 8>(c, fnew, s));
+        else (c->bnd_g == 4 ? bnd_interp_g<2, 4>(c, fnew, s) : bnd_interp_g<2, 8>(c, fnew, s));
+        k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart,
+                                                                        c->bnd_nch, c->wallnum);
+        return;
+    }
     dim3 g((unsigned)((c->N_b + kBndGroup - 1) / kBndGroup), (unsigned)c->bnd_nch);
     if (c->d == 3)
         k_bnd_interp<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.bidx, c->g.bcw,
