@@ -130,7 +130,9 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
  * (no FMA), ascending j.  Also refreshes the context's internal lists.
  * If offsets/idx are non-NULL (device), writes the CSR copy there: offsets[N+1] int64,
  * idx[offsets[N]] int32; cap = capacity of idx.  *needed (host, may be NULL) receives offsets[N].
- * Errors: BGK_E_CAPACITY if offsets[N] > cap or any particle exceeds max_neighbors.
+ * Errors: BGK_E_CAPACITY if offsets[N] > cap or any particle exceeds max_neighbors (such a
+ * particle's internal list is left empty, so no later kernel reads past the per-particle
+ * capacity; bgk_last_error reports the smallest such particle).
  * Synchronises the stream. */
 bgk_status bgk_build_neighbors(bgk_ctx* ctx, int64_t* offsets, int32_t* idx, int64_t cap,
                                int64_t* needed, bgk_stream stream);

@@ -282,8 +282,8 @@ __global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, 
         }
     }
     if (!FILL) {
-        if (lane == 0) {
-            nb_cnt[i] = m;
+        if (lane == 0) {            // an overflowing list is left empty: no later kernel reads
+            nb_cnt[i] = m > max_nb ? 0 : m;   // past the per-particle capacity (error latched)
             if (m > max_nb) latch_error(err, BGK_E_CAPACITY, i);
         }
         return;

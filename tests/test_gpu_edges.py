@@ -67,11 +67,18 @@ def test_neighbor_capacity_reported(torch_cuda):
     truncated list."""
     from paper_2408_02350_b200 import BgkError
     cfg = bi.C1
+    cloud = bi.make_cloud(cfg)
     with pytest.raises(BgkError) as ei:
-        g = gpu(cfg, bi.make_cloud(cfg), max_neighbors=8)
+        g = gpu(cfg, cloud, max_neighbors=8)
         g.step(1)
         g.sync()
     assert ei.value.status == 2
+    off, _ = oracle.neighbors(cloud["x"], cfg.h2)
+    assert ei.value.particle == int(np.nonzero(np.diff(off) > 8)[0][0])
+    # the context stays usable: a fresh one with the default capacity steps normally
+    g = gpu(cfg, cloud)
+    g.step(1)
+    g.sync()
 
 
 def test_coarse_grid_degenerate_state_matches_oracle(torch_cuda):
