@@ -265,7 +265,9 @@ bgk_status bgk_use_staged_f(bgk_ctx* ctx, bgk_stream stream);
  *     interpolated the same way;
  *  3. the surviving particles keep their relative order, inserted ones follow.
  * Deficient interpolation stencils keep the pair / skip the proposal; inserts stop at the
- * capacity.  report (host, may be NULL) receives int64[6] = {merges, merges kept (deficient),
+ * capacity.  One pass creates at most 4096 new particles (merged + inserted): pairs past that
+ * are kept (counted with the deficient ones) and proposals past it are counted as capacity
+ * skips; the next pass takes them up (the oracle has no such limit).  report (host, may be NULL) receives int64[6] = {merges, merges kept (deficient),
  * inserts, inserts skipped (deficient), inserts skipped (capacity), N after the pass}.
  * Runs on the caller's stream and synchronises it; invalidates cached geometry; the next
  * bgk_step rebuilds it.  Particle indices change when anything was merged or inserted:
