@@ -882,8 +882,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int R, int G, int NS>
-__global__ void __launch_bounds__(G * 32, 8 / G) k_transport_cta(const __grid_constant__ CUtensorMap tmap,
+template <int R, int G, int NS, int MINB>
+__global__ void __launch_bounds__(G * 32, MINB) k_transport_cta(const __grid_constant__ CUtensorMap tmap,
                                                                  const TArgs A) {
     constexpr int PD = 10;
     constexpr uint32_t F_BYTES = R * 32 * sizeof(double);
@@ -1156,27 +1156,30 @@ void dispatch_pair(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s)
     }
 }
 
-template <int R, int G>
+template <int R, int G, int MINB>
 void launch_cta_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int NS0 = (G == 8 ? 200 : 100) * 1024 / (R * 32 * 8);   // one (G = 8) or two (G = 4) blocks per SM
+    constexpr int NS0 = (200 / MINB) * 1024 / (R * 32 * 8);         // MINB blocks per SM
     constexpr int NS = NS0 > 32 ? 32 : NS0;                            // producer lookahead stays inside two batches
     constexpr size_t smem = (size_t)NS * R * 32 * 8 + 2 * NS * 8 + (size_t)G * 8 * (10 * 8 + 8);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_transport_cta<R, G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_transport_cta<R, G, NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         configured = true;
     }
     const unsigned gx = (unsigned)((a.n_int + G - 1) / G);
-    k_transport_cta<R, G, NS><<<dim3(gx, (unsigned)a.nw_grid), G * 32, smem, s>>>(tm, a);
+    k_transport_cta<R, G, NS, MINB><<<dim3(gx, (unsigned)a.nw_grid), G * 32, smem, s>>>(tm, a);
 }
 
+// R = 25 / 21: one block of 8 (two of 4) warps per SM; R = 13: two blocks of 8 (four of 4) -- 16 warps
 void dispatch_cta(int G, int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     if (G == 8) {
-        if (R == 25) return launch_cta_one<25, 8>(tm, a, s);
-        return launch_cta_one<21, 8>(tm, a, s);
+        if (R == 25) return launch_cta_one<25, 8, 1>(tm, a, s);
+        if (R == 21) return launch_cta_one<21, 8, 1>(tm, a, s);
+        return launch_cta_one<13, 8, 2>(tm, a, s);
     }
-    if (R == 25) return launch_cta_one<25, 4>(tm, a, s);
-    return launch_cta_one<21, 4>(tm, a, s);
+    if (R == 25) return launch_cta_one<25, 4, 2>(tm, a, s);
+    if (R == 21) return launch_cta_one<21, 4, 2>(tm, a, s);
+    return launch_cta_one<13, 4, 4>(tm, a, s);
 }
 
 constexpr int kRChoices3[] = {25, 21, 17, 15, 13, 11, 9, 7, 5, 3, 1};
@@ -1216,7 +1219,7 @@ int transport_particles_per_warp(int d, int wls_order) {
 int transport_cta_group(int d, int wls_order, int np, int R) {
     const char* e = getenv("BGK_TRANSPORT_CTA");
     const int g = e ? atoi(e) : 0;
-    if (d != 3 || wls_order != 1 || np != 1 || (R != 25 && R != 21)) return 0;
+    if (d != 3 || wls_order != 1 || np != 1 || (R != 25 && R != 21 && R != 13)) return 0;
     return (g == 4 || g == 8) ? g : 0;
 }
 
