@@ -1238,12 +1238,16 @@ void launch_group_union(bgk_ctx* c, cudaStream_t s) {
         const int G = c->cta_g;
         const int64_t ng = (c->N_int + G - 1) / G;
         const size_t smem = (size_t)G * (2 * c->max_nb + 1) * sizeof(int32_t);
-        if (G == 8) {
+        static size_t configured[2] = {0, 0};          // largest shared-memory size set per instantiation
+        if (smem > configured[G == 8]) {
             cudaFuncSetAttribute(k_cta_union<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(k_cta_union<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            configured[G == 8] = smem;
+        }
+        if (G == 8) {
             k_cta_union<8><<<(unsigned)ng, 256, smem, s>>>(cta_order(c), c->N_int, c->g.nb_off, c->g.nb_idx, c->max_nb,
                                                            c->ucap, c->gU, c->gUlen);
         } else {
-            cudaFuncSetAttribute(k_cta_union<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             k_cta_union<4><<<(unsigned)ng, 128, smem, s>>>(cta_order(c), c->N_int, c->g.nb_off, c->g.nb_idx, c->max_nb,
                                                            c->ucap, c->gU, c->gUlen);
         }
