@@ -193,8 +193,9 @@ typedef enum {
     BGK_BUF_MOMENT_SUMS = 0, /* [N][5] fp64 rank-local sums (sum f, sum v f, sum |v|^2 f (+g2)) */
     BGK_BUF_WALL_FLUX = 1,   /* [N] fp64 rank-local sum_{v.n<0} (v.n) f_b (boundary rows) */
     BGK_BUF_F = 2            /* the current distribution, internal layout f[N][Nv+1][ncs][nval] fp64 where
-                                ncs = local column count rounded up to even in 3D (equal in 2D); the
-                                padding column is zero */
+                                ncs = local column count rounded up to a multiple of 16 in 3D (128-B
+                                rows; BGK_NCS_ALIGN = 2, 4, 8 overrides), equal in 2D; read ncs off
+                                the buffer size (bytes / (8 N (Nv+1) nval)); padding columns are zero */
 } bgk_buffer_id;
 
 /* Device pointer and byte size of an internal buffer (inside the caller's workspace). */

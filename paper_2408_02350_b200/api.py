@@ -199,8 +199,8 @@ class Bgk:
     @property
     def ncs(self) -> int:
         """Stored column stride of the internal layout f[N][n1][ncs][nval] (include/bgk.h BGK_BUF_F):
-        the local column count rounded up to even in 3D (16-byte TMA row strides)."""
-        return self.ncol + (self.ncol & 1) if self.dims == 3 else self.ncol
+        the local column count padded in 3D (128-byte rows), read off the buffer's size."""
+        return self.buffer(_lib.BUF_F).numel() // (self.N * self.n1 * self.nval)
 
     def f_internal(self) -> torch.Tensor:
         """The current distribution buffer as a [N, n1, ncol, nval] view (padding stripped)."""

@@ -89,7 +89,17 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->N = N;
     c->Ncap = std::max<int64_t>(N, cfg->max_particles);
     c->Kloc = (int64_t)c->n1 * c->ncol;
-    c->ncs = c->d == 3 ? c->ncol + (c->ncol & 1) : c->ncol;
+    // 3D row stride padded to a multiple of 16 doubles (128 B): every 256-B box row of a column group
+    // then starts on a cache line and covers exactly 8 L2 sectors (C5 transport: 75.7 ms at 16-B
+    // rows, 73.4 at 32 B, 72.8 at 64 B, 71.4 at 128 B; profiles/r01_tuning.md); BGK_NCS_ALIGN overrides
+    {
+        static const int al = [] {
+            const char* e = getenv("BGK_NCS_ALIGN");
+            const int v = e ? atoi(e) : 16;
+            return (v == 2 || v == 4 || v == 8 || v == 16) ? v : 16;
+        }();
+        c->ncs = c->d == 3 ? (c->ncol + al - 1) / al * al : c->ncol;
+    }
     c->Ks = (int64_t)c->n1 * c->ncs;
     c->RS = c->Ks * c->nv;
     c->max_nb = cfg->max_neighbors > 0 ? cfg->max_neighbors : (c->d == 2 ? 96 : 256);
@@ -130,11 +140,6 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
         c->nchunk = (c->n1 + c->R - 1) / c->R;
         c->nwpp = c->nchunk * c->ncg + (c->tail_cols ? c->nchunk : 0);
         c->nslots = c->nwpp * 32;
-    }
-    c->cta_g = transport_cta_group(c->d, c->wls_order, c->np, c->R);
-    if (c->cta_g) {
-        if (c->Ncap >= (1 << 23)) c->cta_g = 0;          // union entries pack j << 8
-        else c->ucap = c->cta_g * c->max_nb;
     }
     // fixed-cloud lattice rows (SURVEY §8(d) "the one lever"): partial slots sized for both mappings
     {
@@ -216,8 +221,8 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->g.bcw = k.take<double>(c->cap);
     c->g.bcnt = k.take<int32_t>(N);
     c->g.order = k.take<int32_t>(N);
-    const int64_t ng = c->np == 2 ? (N + 1) / 2 : (c->cta_g ? (N + c->cta_g - 1) / c->cta_g : 1);
-    c->gU = k.take<int32_t>(c->np == 2 ? (size_t)ng * c->ucap * 2 : (c->cta_g ? (size_t)ng * c->ucap : 2));   // int2 / int32
+    const int64_t ng = c->np == 2 ? (N + 1) / 2 : 1;
+    c->gU = k.take<int32_t>(c->np == 2 ? (size_t)ng * c->ucap * 2 : 2);   // int2 entries
     c->gUlen = k.take<int32_t>(4 * ng);
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
@@ -657,7 +662,7 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
     if (c->cfg.ale) k += launches_neighbors() + launches_wls() - (c->N_b ? 0 : 1) - (c->N_int ? 0 : 1);
     if (c->cfg.ale && c->cfg.manage) k += 2;   // k_mg_detect + k_mg_decide (plus 3 more and a neighbour
                                                // rebuild in the rare steps where the cloud changes)
-    if (c->cfg.ale && (c->np == 2 || c->cta_g)) k += 1;      // k_pair_union / k_cta_union
+    if (c->cfg.ale && c->np == 2) k += 1;      // k_pair_union
     if (c->N_int) k += 3;        // transport, moment reduce, relax
     if (c->N_b) k += 3;          // boundary interp, wall reduce, fill
     *n = k;

@@ -130,7 +130,6 @@ struct bgk_ctx {
     int32_t* order_rest;// [Ncap] the rest, in cell order
     int rows_nchunk;    // velocity chunks of kRowsR nodes along v_1
     int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)
-    int cta_g;          // > 0: CTA-shared neighbour boxes, cta_g warps (particles) per block (BGK_TRANSPORT_CTA)
     int64_t* scan_tmp;  // [1024]
     int32_t* blk_tmp;   // [1024] per-block partial counts of the multi-block scans
     bgk::Geo g;
@@ -197,7 +196,6 @@ void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStre
 void launch_check_domain(bgk_ctx* c, cudaStream_t s);
 int transport_rows_per_thread(int d, int n1, int np);
 int transport_particles_per_warp(int d, int wls_order);
-int transport_cta_group(int d, int wls_order, int np, int R);
 bool make_tensor_maps(bgk_ctx* c);
 // fixed-cloud lattice rows: host-side group detection on the cached geometry, and the kernel
 bgk_status build_rows(bgk_ctx* c, cudaStream_t s);

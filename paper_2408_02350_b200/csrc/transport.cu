@@ -798,208 +798,6 @@ __global__ void __launch_bounds__(128) k_pair_union(const int32_t* __restrict__ 
     }
 }
 
-// ============================================================================
-// CTA-shared neighbour boxes (3D first order, BGK_TRANSPORT_CTA = G in {4, 8}; experimental).
-// A block of G warps owns G consecutive particles of the cell-ordered interior list and one
-// (chunk, column group).  The block walks the UNION of their neighbour lists (ascending j,
-// k_cta_union: entry = j << 8 | member mask): each union box is fetched ONCE by TMA into a
-// block-wide ring of NS stages and every member warp applies it with its own pair record, so the
-// L2 -> SM bytes drop by the union / sum-of-lists ratio while each warp keeps the one-particle
-// register footprint.  full[s]: TMA landed (count 1 + tx); empty[s]: every warp of the block has
-// passed the entry (count G; non-members arrive after the full wait, which keeps each warp's
-// arrivals in phase order).  Warp 0's elected lane is the producer: it refills non-blockingly up
-// to NS entries ahead and blocks on empty only for the entry it needs next.
-template <int G>
-__global__ void __launch_bounds__(G * 32) k_cta_union(const int32_t* __restrict__ order, int64_t n_int,
-                                                      const int64_t* __restrict__ nb_off,
-                                                      const int32_t* __restrict__ nb_idx, int max_nb, int ucap,
-                                                      int32_t* __restrict__ gU, int32_t* __restrict__ gUlen) {
-    extern __shared__ int32_t usm[];
-    int32_t* L = usm;                                   // [G][max_nb] the lists
-    int32_t* pre = L + G * max_nb;                      // [G][max_nb + 1] exclusive prefix of "first owner" flags
-    __shared__ int mc[G];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t grp = blockIdx.x;
-    const int64_t t = grp * G + w;
-    int m = 0;
-    if (t < n_int) {
-        const int p = order[t];
-        const int64_t off = nb_off[p];
-        m = (int)(nb_off[p + 1] - off);
-        for (int e = lane; e < m; e += 32) L[w * max_nb + e] = nb_idx[off + e];
-    }
-    if (lane == 0) mc[w] = m;
-    __syncthreads();
-    auto lower = [&](int w2, int v) {                   // first position in list w2 with L >= v
-        const int32_t* l = L + w2 * max_nb;
-        int lo = 0, hi = mc[w2];
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (l[mid] < v) lo = mid + 1;
-            else hi = mid;
-        }
-        return lo;
-    };
-    const unsigned below = (1u << lane) - 1u;
-    int base = 0;
-    for (int b = 0; b < m; b += 32) {                   // owner = first list holding v
-        const int e = b + lane;
-        bool own = e < m;
-        if (own) {
-            const int v = L[w * max_nb + e];
-            for (int w2 = 0; w2 < w && own; ++w2) {
-                const int q = lower(w2, v);
-                own = !(q < mc[w2] && L[w2 * max_nb + q] == v);
-            }
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, own);
-        if (e < m) pre[w * (max_nb + 1) + e] = base + __popc(bal & below);
-        base += __popc(bal);
-    }
-    if (lane == 0) pre[w * (max_nb + 1) + m] = base;
-    __syncthreads();
-    for (int e = lane; e < m; e += 32) {
-        if (pre[w * (max_nb + 1) + e + 1] == pre[w * (max_nb + 1) + e]) continue;   // not the owner
-        const int v = L[w * max_nb + e];
-        int rank = pre[w * (max_nb + 1) + e];
-        unsigned mask = 1u << w;
-        for (int w2 = 0; w2 < G; ++w2) {
-            if (w2 == w) continue;
-            const int q = lower(w2, v);
-            rank += pre[w2 * (max_nb + 1) + q];
-            if (q < mc[w2] && L[w2 * max_nb + q] == v) mask |= 1u << w2;
-        }
-        gU[grp * ucap + rank] = (v << 8) | (int)mask;
-    }
-    if (threadIdx.x == 0) {
-        int u = 0;
-        for (int w2 = 0; w2 < G; ++w2) u += pre[w2 * (max_nb + 1) + mc[w2]];
-        gUlen[grp] = u;
-    }
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-template <int R, int G, int NS, int MINB>
-__global__ void __launch_bounds__(G * 32, MINB) k_transport_cta(const __grid_constant__ CUtensorMap tmap,
-                                                                 const TArgs A) {
-    constexpr int PD = 10;
-    constexpr uint32_t F_BYTES = R * 32 * sizeof(double);
-    static_assert(F_BYTES % 128 == 0, "stage alignment");
-    constexpr int RD = 8;                                 // pair-record ring per warp (members ahead)
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NS * F_BYTES);
-    uint64_t* empty = full + NS;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    double* rring = reinterpret_cast<double*>(empty + NS) + wib * RD * PD;
-    uint64_t* rbar = reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(empty + NS) + G * RD * PD) + wib * RD;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, G);
-        }
-        for (int s = 0; s < G * RD; ++s) mbar_init(reinterpret_cast<uint64_t*>(reinterpret_cast<double*>(empty + NS) + G * RD * PD) + s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __shared__ int passed[NS];                            // warps that have passed slot s, over all rounds
-    for (int s = threadIdx.x; s < NS; s += blockDim.x) passed[s] = 0;
-    __syncthreads();
-    const int w = blockIdx.y;
-    const int64_t grp = blockIdx.x;
-    const int64_t pos = grp * G + wib;
-    const bool active = pos < A.n_int;                    // warp-uniform; idle warps still pass every entry
-    const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
-    const int p = active ? A.order[pos] : 0;
-    const int col = cg * 32 + lane;
-    const bool valid = col < A.ncol;
-    const int k1s = chunk * R;
-    const int colc = valid ? col : 0;
-    const int gc = A.c0 + colc;
-    const int U = A.gUlen[grp];
-    const int32_t* ul = A.gU + grp * A.ucap;
-    int uA = lane < U ? __ldg(ul + lane) : 0;
-    int uB = 32 + lane < U ? __ldg(ul + 32 + lane) : 0;
-    int ubase = 0;                                        // union index of uA's lane 0
-    const int64_t off = active ? A.nb_off[p] : 0;
-    const int m = active ? (int)(A.nb_off[p + 1] - off) : 0;
-    const double* Pp = A.P + off * PD;
-    auto rec_issue = [&](int q) {                         // elected lane: record q -> slot q % RD
-        mbar_expect_tx(rbar + q % RD, PD * sizeof(double));
-        bulk_load(rring + (q % RD) * PD, Pp + (int64_t)q * PD, PD * sizeof(double), rbar + q % RD);
-    };
-    if (elect_one())
-        for (int q = 0; q < RD && q < m; ++q) rec_issue(q);
-
-    double Wp[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) Wp[a] = active ? A.W[(int64_t)p * 3 + a] : 0.0;
-    double c0v[3];
-    c0v[0] = axis_node(A.vmax, A.dv, k1s) - Wp[0];
-    {
-        const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-        c0v[1] = axis_node(A.vmax, A.dv, k2) - Wp[1];
-        c0v[2] = axis_node(A.vmax, A.dv, k3) - Wp[2];
-    }
-    const double c1dv = c0v[0] / A.dv;
-    double Qf[R][1], Sc[R], Sa[1];
-#pragma unroll
-    for (int r = 0; r < R; ++r) Qf[r][0] = Sc[r] = 0.0;
-    int e = 0;                                            // the warp's own list position
-    auto issue = [&](int t, int j) {                      // elected lane: union entry t -> slot t % NS
-        mbar_expect_tx(full + t % NS, F_BYTES);
-        tma_load_3d(smem_raw + (size_t)(t % NS) * F_BYTES, &tmap, cg * 32, k1s, j, full + t % NS);
-    };
-    if (wib == 0)
-        for (int t = 0; t < NS && t < U; ++t) {
-            const int ent0 = __shfl_sync(0xffffffffu, t < 32 ? uA : uB, t & 31);
-            if (elect_one()) issue(t, ent0 >> 8);
-            __syncwarp();
-        }
-    for (int u = 0; u < U; ++u) {
-        if (u - ubase == 32) {                            // warp-uniform batch rotation
-            uA = uB;
-            ubase += 32;
-            uB = ubase + 32 + lane < U ? __ldg(ul + ubase + 32 + lane) : 0;
-        }
-        const int ent = __shfl_sync(0xffffffffu, uA, (u - ubase) & 31);
-        const int s = u % NS;
-        mbar_wait(full + s, (uint32_t)(u / NS) & 1u);
-        if ((ent >> wib) & 1) {
-            double y[3], dy[3], Lc, dL;
-            {
-                mbar_wait(rbar + e % RD, (uint32_t)(e / RD) & 1u);
-                const double* rs = rring + (e % RD) * PD;
-                double rec[PD];
-#pragma unroll
-                for (int q = 0; q < PD; ++q) rec[q] = rs[q];
-                pair_coeffs<3>(rec, c0v, c1dv, A.dv, y, dy, Lc, dL);
-            }
-            __syncwarp();
-            if (e + RD < m && elect_one()) rec_issue(e + RD);
-            ++e;
-            const double* st = reinterpret_cast<const double*>(smem_raw + (size_t)s * F_BYTES) + lane;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                double C = neg_part(fma((double)r, dy[0], y[0])) + neg_part(fma((double)r, dy[1], y[1]));
-                C += neg_part(fma((double)r, dy[2], y[2]));
-                Qf[r][0] = fma(C, st[r * 32], Qf[r][0]);
-                Sc[r] += C;
-            }
-        }
-        // the LAST warp to pass entry u refills its slot with entry u + NS at once (no producer lag)
-        __syncwarp();
-        int last = 0;
-        if (lane == 0) last = atomicAdd(&passed[s], 1) == (u / NS + 1) * G - 1;
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last && u + NS < U && elect_one()) issue(u + NS, __ldg(ul + u + NS) >> 8);
-        __syncwarp();
-    }
-    if (active) transport_epilogue<3, R, false>(A, p, w, k1s, colc, gc, valid, Qf, Sc, Sa);
-}
-
 // 2D tail columns (N_v = 32: the 33rd column): warp per (interior particle, chunk of R nodes along
 // v_1), lane r owning row k1s + r, looping over the neighbours (pair record and neighbour index
 // broadcast, one 16-B load of (g1, g2) per lane); the same arithmetic as k_transport (C/2 =
@@ -1156,32 +954,6 @@ void dispatch_pair(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s)
     }
 }
 
-template <int R, int G, int MINB>
-void launch_cta_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int NS0 = (200 / MINB) * 1024 / (R * 32 * 8);         // MINB blocks per SM
-    constexpr int NS = NS0 > 32 ? 32 : NS0;                            // producer lookahead stays inside two batches
-    constexpr size_t smem = (size_t)NS * R * 32 * 8 + 2 * NS * 8 + (size_t)G * 8 * (10 * 8 + 8);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_transport_cta<R, G, NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
-    }
-    const unsigned gx = (unsigned)((a.n_int + G - 1) / G);
-    k_transport_cta<R, G, NS, MINB><<<dim3(gx, (unsigned)a.nw_grid), G * 32, smem, s>>>(tm, a);
-}
-
-// R = 25 / 21: one block of 8 (two of 4) warps per SM; R = 13: two blocks of 8 (four of 4) -- 16 warps
-void dispatch_cta(int G, int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    if (G == 8) {
-        if (R == 25) return launch_cta_one<25, 8, 1>(tm, a, s);
-        if (R == 21) return launch_cta_one<21, 8, 1>(tm, a, s);
-        return launch_cta_one<13, 8, 2>(tm, a, s);
-    }
-    if (R == 25) return launch_cta_one<25, 4, 2>(tm, a, s);
-    if (R == 21) return launch_cta_one<21, 4, 2>(tm, a, s);
-    return launch_cta_one<13, 4, 4>(tm, a, s);
-}
-
 constexpr int kRChoices3[] = {25, 21, 17, 15, 13, 11, 9, 7, 5, 3, 1};
 constexpr int kRChoices2[] = {17, 13, 11, 9, 7, 5, 3, 1};
 
@@ -1216,43 +988,7 @@ int transport_particles_per_warp(int d, int wls_order) {
     return np == 2 ? 2 : 1;
 }
 
-int transport_cta_group(int d, int wls_order, int np, int R) {
-    const char* e = getenv("BGK_TRANSPORT_CTA");
-    const int g = e ? atoi(e) : 0;
-    if (d != 3 || wls_order != 1 || np != 1 || (R != 25 && R != 21 && R != 13)) return 0;
-    return (g == 4 || g == 8) ? g : 0;
-}
-
-// CTA groups: G consecutive interior particles by index (BGK_CTA_ORDER=1, default: on a lattice-indexed
-// cloud these are x-neighbours, whose members keep step along the union) or in cell order (0)
-static const int32_t* cta_order(const bgk_ctx* c) {
-    static const int by_index = [] {
-        const char* e = getenv("BGK_CTA_ORDER");
-        return e ? atoi(e) : 1;
-    }();
-    return by_index ? c->interior : c->g.order;
-}
-
 void launch_group_union(bgk_ctx* c, cudaStream_t s) {
-    if (c->cta_g && c->N_int > 0) {
-        const int G = c->cta_g;
-        const int64_t ng = (c->N_int + G - 1) / G;
-        const size_t smem = (size_t)G * (2 * c->max_nb + 1) * sizeof(int32_t);
-        static size_t configured[2] = {0, 0};          // largest shared-memory size set per instantiation
-        if (smem > configured[G == 8]) {
-            cudaFuncSetAttribute(k_cta_union<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            cudaFuncSetAttribute(k_cta_union<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            configured[G == 8] = smem;
-        }
-        if (G == 8) {
-            k_cta_union<8><<<(unsigned)ng, 256, smem, s>>>(cta_order(c), c->N_int, c->g.nb_off, c->g.nb_idx, c->max_nb,
-                                                           c->ucap, c->gU, c->gUlen);
-        } else {
-            k_cta_union<4><<<(unsigned)ng, 128, smem, s>>>(cta_order(c), c->N_int, c->g.nb_off, c->g.nb_idx, c->max_nb,
-                                                           c->ucap, c->gU, c->gUlen);
-        }
-        return;
-    }
     if (c->np != 2 || c->N_int == 0) return;
     const int64_t ng = (c->N_int + 1) / 2;
     k_pair_union<<<(unsigned)((ng + 3) / 4), 128, 0, s>>>(c->g.order, c->N_int, c->g.nb_off, c->g.nb_idx, c->ucap,
@@ -1337,10 +1073,6 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
         a.n_int = c->n_rest;
     }
     if (c->np == 2) return dispatch_pair(c->R, tm, a, s);
-    if (c->cta_g && !c->rows_built) {
-        a.order = cta_order(c);
-        return dispatch_cta(c->cta_g, c->R, tm, a, s);
-    }
     static const int wpb = [] {
         const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (2, 4, 8); default kDefaultWarps
         return e ? atoi(e) : kDefaultWarps;

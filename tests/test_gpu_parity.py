@@ -352,25 +352,6 @@ def test_pair_warp_transport_ten_steps(torch_cuda, cfg, monkeypatch):
     check_state(g, oracle_run(cfg, 10), cfg)
 
 
-# ------------------------------------ CTA-shared neighbour boxes (opt-in)
-@pytest.mark.parametrize("G", ["8", "4"])
-@pytest.mark.parametrize("cfg,R", [(bi.C4, "21"), (bi.CavityConfig("C4j", 3, 15, 8, jitter=0.3, dt=5e-12), "25"),
-                                   (bi.CavityConfig("C5s", 3, 8, 24, jitter=0.2, dt=5e-12), "")])
-def test_cta_shared_transport(torch_cuda, cfg, R, G, monkeypatch):
-    """BGK_TRANSPORT_CTA=G: a block of G warps walks the union of G particles' lists (k_cta_union)
-    and shares each TMA box.  Jittered clouds give unequal, partially overlapping lists; 13^3 and
-    6^3 interior particles leave a partial last block.  R is forced where N_v is small (rows past
-    N_v are TMA zero-fill)."""
-    monkeypatch.setenv("BGK_TRANSPORT_CTA", G)
-    if R:
-        monkeypatch.setenv("BGK_TRANSPORT_R", R)
-    steps = 3 if cfg.Nv == 24 else 10
-    g, _ = gpu(cfg)
-    g.step(steps)
-    g.sync()
-    check_state(g, oracle_run(cfg, steps), cfg)
-
-
 # -------------------------------------------------- degenerate cloud shapes
 @pytest.mark.parametrize("cfg", [bi.CavityConfig("open2d", 2, 17, 10, jitter=0.2, dt=4e-12),
                                  bi.CavityConfig("open3d", 3, 9, 6, jitter=0.2, dt=4e-12)])

@@ -39,6 +39,6 @@ except Exception as ex:
     print('warning:', ex, file=sys.stderr)
 out = {p: acc[i] / a.steps for i, p in enumerate(_lib.PHASES)}
 out["total"] = sum(out.values())
-out["knobs"] = {k: v for k, v in os.environ.items() if k.startswith("BGK_TRANSPORT_")}
+out["knobs"] = {k: v for k, v in os.environ.items() if k.startswith("BGK_")}
 out["config"] = cfg.name
 print(json.dumps(out))
