@@ -67,9 +67,9 @@ struct Manage {
 struct bgk_ctx {
     bgk_config cfg;
     int d, nv, n1, ncol_g, c0, c1, ncol;
-    int ncs;                           // stored column stride: ncol rounded up to even in 3D (16-B TMA strides)
-    int64_t N, N_int, N_b, Kloc, Ks, RS;
-    int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
+    int ncs;                           // stored column stride: ncol rounded up to a multiple of 16 in 3D (128-B rows)
+    int64_t N, N_int, N_b, Kloc, Ks, RS;   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
+    int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)
     int ncg;                           // 32-column groups per chunk (transport)
     int tail_cols;                     // 2D: columns past the last full group, done by k_transport_tail
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
