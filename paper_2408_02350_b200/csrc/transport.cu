@@ -1073,10 +1073,12 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
         a.n_int = c->n_rest;
     }
     if (c->np == 2) return dispatch_pair(c->R, tm, a, s);
-    static const int wpb = [] {
-        const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (2, 4, 8); default kDefaultWarps
-        return e ? atoi(e) : kDefaultWarps;
+    static const int wpb_env = [] {
+        const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (2, 4, 8); default below
+        return e ? atoi(e) : 0;
     }();
+    // 3D, R = 25: blocks of 2 warps (70.2 vs 70.9 ms on C5 with 128-B rows; profiles/r01_tuning.md)
+    const int wpb = wpb_env ? wpb_env : (c->d == 3 && c->R == 25 ? 2 : kDefaultWarps);
     if (c->d == 3) dispatch<3>(c->R, wpb, tm, a, s);
     else {
         if (c->ncg > 0) dispatch<2>(c->R, wpb, tm, a, s);
