@@ -98,7 +98,12 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
             const int v = e ? atoi(e) : 16;
             return (v == 2 || v == 4 || v == 8 || v == 16) ? v : 16;
         }();
-        c->ncs = c->d == 3 ? (c->ncol + al - 1) / al * al : c->ncol;
+        static const int al2 = [] {   // 2D: (g1, g2) = 16 B per column; padding to 128-B rows (8) measured
+            const char* e = getenv("BGK_NCS2_ALIGN");   // no gain on C2/C3 (profiles/r01_tuning.md): default 1
+            const int v = e ? atoi(e) : 1;
+            return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 1;
+        }();
+        c->ncs = c->d == 3 ? (c->ncol + al - 1) / al * al : (c->ncol + al2 - 1) / al2 * al2;
     }
     c->Ks = (int64_t)c->n1 * c->ncs;
     c->RS = c->Ks * c->nv;
