@@ -100,10 +100,39 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU oracle baseline
-def oracle_sample_rate(cfg, cloud, seconds: float = 15.0, threads: int = 0, max_particles: int = 4096):
+class _AllRows:
+    """f^0 rows of a whole cloud (built once by the oracle's or_init_f) as the row cache the sampled
+    driver reads: the input state exists before the timed region, as on the GPU."""
+
+    def __init__(self, F0):
+        self.F0 = F0
+
+    def __contains__(self, j):
+        return True
+
+    def __getitem__(self, j):
+        return self.F0[j]
+
+
+def cpu_info():
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model}
+
+
+def oracle_sample_rate(cfg, cloud, seconds: float = 10.0, threads: int = 0, max_particles: int = 65536,
+                       rows=None):
     """Time the oracle (as it stands) on interior particles of the workload: each task is the
-    oracle's whole first step at one particle (neighbours, WLS, transport over all K nodes,
-    moments, Maxwellian, relaxation).  Returns (updates/s, cores, sample description)."""
+    oracle's whole first step at one particle -- brute-force neighbour list, WLS + frames, transport
+    over all K nodes, moments, tau, Maxwellian, relaxation, ALE move (oracle.sampled_first_step).
+    The input state f^0 is built before the timed region (``rows``).  Returns (updates/s, threads,
+    sample description)."""
     import concurrent.futures as cf
 
     import oracle
@@ -112,35 +141,87 @@ def oracle_sample_rate(cfg, cloud, seconds: float = 15.0, threads: int = 0, max_
     inter = np.nonzero(kind == 0)[0]
     rng = np.random.default_rng(2408)
     order = rng.permutation(inter)[:max_particles]
-    threads = threads or min(os.cpu_count() or 1, 32)
+    threads = threads or (os.cpu_count() or 1)
+    if rows is None:
+        c = oracle.make_cfg(cfg)
+        rows = _AllRows(oracle.init_f(c, cloud["rho"], cloud["U"], cloud["T"]))
     K = cfg.n_nodes
     done = 0
     t0 = time.perf_counter()
-    with cf.ThreadPoolExecutor(threads) as ex:   # ctypes releases the GIL inside the C oracle
-        it = iter(order)
-        futs = set()
-        while True:
-            while len(futs) < 2 * threads:
-                try:
-                    i = int(next(it))
-                except StopIteration:
-                    break
-                futs.add(ex.submit(oracle.sampled_first_step, cfg, cloud, [i]))
-            if not futs:
-                break
-            fin, futs = cf.wait(futs, return_when=cf.FIRST_COMPLETED)
-            done += len(fin)
+    if threads == 1:
+        for i in order:
+            oracle.sampled_first_step(cfg, cloud, [int(i)], f0=rows)
+            done += 1
             if time.perf_counter() - t0 > seconds:
-                for f in futs:
-                    f.cancel()
-                cf.wait(futs)
-                done += sum(1 for f in futs if f.done() and not f.cancelled())
                 break
+    else:
+        with cf.ThreadPoolExecutor(threads) as ex:   # ctypes releases the GIL inside the C oracle
+            it = iter(order)
+            futs = set()
+            while True:
+                while len(futs) < 2 * threads:
+                    try:
+                        i = int(next(it))
+                    except StopIteration:
+                        break
+                    futs.add(ex.submit(oracle.sampled_first_step, cfg, cloud, [i], None, rows))
+                if not futs:
+                    break
+                fin, futs = cf.wait(futs, return_when=cf.FIRST_COMPLETED)
+                done += len(fin)
+                if time.perf_counter() - t0 > seconds:
+                    cf.wait(futs)                    # in-flight particles finish inside the timed region
+                    done += len(futs)
+                    break
     dt = time.perf_counter() - t0
     rate = done * K / dt
-    desc = (f"oracle full first step at {done} random interior particles of {cfg.name} "
-            f"(all {K} nodes each), {threads} threads, {dt:.1f} s")
+    desc = (f"oracle whole first step (neighbours, WLS, transport, moments, relaxation, move) at {done} random "
+            f"interior particles of {cfg.name} (all {K} nodes each; f^0 built before timing), {threads} "
+            f"thread(s), {dt:.1f} s")
     return rate, threads, desc
+
+
+def oracle_whole_steps(cfg, steps: int, threads: int):
+    """Seconds per whole-cloud oracle step (or_step: geometry, transport, moments, relaxation, move,
+    boundary) at `threads` OpenMP threads; the initial state is built before timing."""
+    import oracle
+    oracle.build()
+    prev = oracle.omp_threads()
+    oracle.set_threads(threads)
+    try:
+        st = oracle.State(oracle.make_cfg(cfg), bi.make_cloud(cfg))
+        t0 = time.perf_counter()
+        st.step(steps)
+        dt = (time.perf_counter() - t0) / steps
+    finally:
+        oracle.set_threads(prev)
+    return dt
+
+
+def cpu_baseline(cfg, cloud, seconds: float, full: bool = False):
+    """The paper's CPU (1 thread) and OMP (all cores) columns (Tables 1-2) for this
+    host: the bench workload sampled per particle at 1 thread and at all cores, and whole oracle steps
+    of the two small configs (C1 2D, C4 3D) at 1 thread and all cores (C4 at 1 thread takes ~2 min:
+    only with ``full``)."""
+    import oracle
+    info = cpu_info()
+    ncores = info["nproc"]
+    c = oracle.make_cfg(cfg)
+    rows = _AllRows(oracle.init_f(c, cloud["rho"], cloud["U"], cloud["T"]))
+    par, par_threads, par_desc = oracle_sample_rate(cfg, cloud, seconds, ncores, rows=rows)
+    seq, _, seq_desc = oracle_sample_rate(cfg, cloud, seconds, 1, rows=rows)
+    del rows
+    whole = {}
+    for wc, steps in ((bi.C1, 3), (bi.C4, 1)):
+        upd = wc.n_particles * wc.n_nodes
+        tp = oracle_whole_steps(wc, steps, ncores)
+        whole[wc.name] = {"par_s_per_step": tp, "par_updates_per_s": upd / tp, "par_threads": ncores}
+        if full or wc.dims == 2:
+            t1 = oracle_whole_steps(wc, steps, 1)
+            whole[wc.name].update({"seq_s_per_step": t1, "seq_updates_per_s": upd / t1})
+    return {"value": par, "unit": UNIT, "cores": par_threads, "kind": "oracle", "sample": par_desc,
+            "sequential": {"value": seq, "unit": UNIT, "cores": 1, "sample": seq_desc},
+            "whole_steps": whole, **info}
 
 
 # ---------------------------------------------------------------- our arm
@@ -270,7 +351,8 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         Kl = g.Kloc
-        host_f = torch.empty((N, nval, Kl), dtype=torch.float64, pin_memory=True)
+        N_e = g.N                        # the cloud as it is now (management may have changed it)
+        host_f = torch.empty((N_e, nval, Kl), dtype=torch.float64, pin_memory=True)
         g.get_f(host_f)
         rho = torch.empty(N, dtype=torch.float64, pin_memory=True)
         U = torch.empty((N, cfg.dims), dtype=torch.float64, pin_memory=True)
@@ -293,6 +375,14 @@ def run_ours(args):
             else:
                 g.step(1)
                 rr, uu, tt = g.moments()
+            if g.N != N_e and n + 1 < n_e2e:
+                # particle management changed the cloud: the staged rows are stale (bgk_use_staged_f
+                # would refuse them) -- size the host buffer for the new N and stage again
+                copy_stream.synchronize()
+                N_e = g.N
+                host_f = torch.empty((N_e, nval, Kl), dtype=torch.float64, pin_memory=True)
+                g.get_f(host_f)
+                g.stage_f(host_f, copy_stream)
         copy_stream.synchronize()
         barrier()
         dt_e2e = time.perf_counter() - t0
@@ -302,7 +392,7 @@ def run_ours(args):
         dt_e2e = float(tt_.item())
         e2e = {"value": N * K * n_e2e / dt_e2e, "unit": UNIT,
                "h2d_bytes_per_step": int(host_f.numel() * 8 * world),
-               "d2h_bytes_per_step": int(N * (cfg.dims + 2) * 8),
+               "d2h_bytes_per_step": int(N_e * (cfg.dims + 2) * 8),
                "steps": n_e2e,
                "path": "bgk_stage_f(pinned host, copy stream, one step ahead) + bgk_use_staged_f + bgk_step "
                        "+ bgk_moments(host)"}
@@ -350,8 +440,7 @@ def run_ours(args):
                             "lattice_row_groups": info[2], "general_kernel_particles": info[3]}
         g2.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, desc = oracle_sample_rate(cfg, cloud, seconds=args.cpu_seconds)
-        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        out["cpu_baseline"] = cpu_baseline(cfg, cloud, args.cpu_seconds, args.cpu_full)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -366,13 +455,15 @@ def run_reference(args):
         return
     cfg = bi.CONFIGS[args.config] if args.config in bi.CONFIGS else getattr(bi, args.config)
     cloud = bi.make_cloud(cfg)
+    import oracle
     per = max(5.0, min(30.0, 150.0 / max(1, args.steps + args.warmup)))
+    rows = _AllRows(oracle.init_f(oracle.make_cfg(cfg), cloud["rho"], cloud["U"], cloud["T"]))
     for _ in range(args.warmup):
-        oracle_sample_rate(cfg, cloud, seconds=per / 3)
+        oracle_sample_rate(cfg, cloud, seconds=per / 3, rows=rows)
     rates, cores, desc = [], 1, ""
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        r, cores, desc = oracle_sample_rate(cfg, cloud, seconds=per)
+        r, cores, desc = oracle_sample_rate(cfg, cloud, seconds=per, rows=rows)
         rates.append(r)
     wall = time.perf_counter() - t0
     value = float(np.mean(rates))
@@ -393,13 +484,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C5_3d_40cube_Nv24")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the fixed-cloud secondary number")
     ap.add_argument("--manage", type=int, default=1, choices=[0, 1],
                     help="particle management pass in every ALE step (the paper's Particle Organization)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true", help="also time a whole C4 oracle step at 1 thread (~2 min)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

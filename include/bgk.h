@@ -250,8 +250,12 @@ const char* bgk_version(void);
  * without synchronising.  bgk_use_staged_f makes `stream` wait for that copy and converts the
  * staged state into the current f (the state the next bgk_step advances).  A user loop
  *   stage(f_0); for n: { use_staged(); stage(f_{n+1}); step(); read results; }
- * moves step n+1's input while step n computes.  Errors: BGK_E_INVALID_ARG (no staging buffer,
- * nothing staged), BGK_E_CUDA. */
+ * moves step n+1's input while step n computes.  Size contract: bgk_stage_f copies
+ * N*nval*K_local doubles for the N current when it is called (the caller's buffer must hold that
+ * many) and records N and the cloud generation; bgk_use_staged_f refuses (BGK_E_INVALID_ARG,
+ * nothing converted, the staged input dropped) if particle management changed N or renumbered the
+ * rows in between -- stage again for the new cloud.  Errors: BGK_E_INVALID_ARG (no staging buffer,
+ * nothing staged, stale staged input), BGK_E_CUDA. */
 bgk_status bgk_stage_f(bgk_ctx* ctx, const double* f, bgk_stream copy_stream);
 bgk_status bgk_use_staged_f(bgk_ctx* ctx, bgk_stream stream);
 

@@ -440,7 +440,56 @@ def set_threads(n: int) -> None:
     lib().or_set_threads(int(n))
 
 
-def sampled_first_step(cfg, cloud, sample, k_range=None):
+def wls_particle(c: OrCfg, x, i: int, nb):
+    """S, a, frames, rot of ONE interior particle i with neighbour list nb, through or_wls_all (the
+    whole-cloud routine) on a one-particle CSR: every other particle is marked non-interior and has an
+    empty list, so the C loop skips it.  Same arithmetic as the whole-cloud step, one C call."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    N, d = x.shape
+    nb = np.ascontiguousarray(nb, dtype=np.int32)
+    m = len(nb)
+    kind = np.ones(N, dtype=np.int8)
+    kind[i] = 0
+    off = np.zeros(N + 1, dtype=np.int64)
+    off[i + 1:] = m
+    S1 = np.empty((N, d, d))          # or_wls_all writes row i only
+    a = np.zeros((max(m, 1), d))
+    fr = np.zeros((max(m, 1), d, d))
+    rot = np.zeros((max(m, 1), d))
+    bad = C.c_int64(-1)
+    st = lib().or_wls_all(d, _p(x), N, _p(kind), _p(off), _p(nb), c.h2, c.alpha_w, c.wls_order,
+                          _p(S1), _p(a), _p(fr), _p(rot), C.byref(bad))
+    if st != OR_OK:
+        raise OracleError(st, i)
+    return S1[i].copy(), a[:m], fr[:m], rot[:m]
+
+
+def initial_rows(cfg, cloud, particles) -> dict:
+    """f^0 rows (the Maxwellian of the seeded initial fields) of the given particles."""
+    c = make_cfg(cfg)
+    return {int(j): maxwellian_row(c, cloud["rho"][j], cloud["U"][j], cloud["T"][j]) for j in particles}
+
+
+def sample_support(cfg, cloud, sample):
+    """Every particle whose f^0 row the first step at `sample` reads: the sample, its neighbours and,
+    for boundary particles, their interior neighbours' neighbours."""
+    x, kind = cloud["x"], cloud["kind"]
+    need = set()
+    for i in sample:
+        i = int(i)
+        nb = neighbors_of(x, cfg.h2, i)
+        need.add(i)
+        if kind[i] == 0:
+            need.update(int(j) for j in nb)
+        else:
+            for j in nb:
+                if kind[int(j)] == 0:
+                    need.add(int(j))
+                    need.update(int(q) for q in neighbors_of(x, cfg.h2, int(j)))
+    return need
+
+
+def sampled_first_step(cfg, cloud, sample, k_range=None, f0=None):
     """First step n=0 -> 1 at the sampled particles of a full-size cloud.
 
     Builds only what the sample needs, from the oracle's own primitives: f^0
@@ -451,12 +500,14 @@ def sampled_first_step(cfg, cloud, sample, k_range=None):
     with f the full row of f^1 and (rho, U, T) the recovered state for
     interior particles.  ``k_range`` limits transport to a node range (rows are
     then only valid there; relaxation needs all nodes, so it is skipped).
+    ``f0`` (optional dict j -> row, e.g. from ``initial_rows``) supplies the input rows, so a timed
+    caller can build the input state outside its timed region; missing rows are built on demand.
     """
     c = make_cfg(cfg)
     x, kind = cloud["x"], cloud["kind"]
     d = c.dims
     K = num_nodes(c)
-    f0 = {}
+    f0 = {} if f0 is None else f0
 
     def row0(j):
         if j not in f0:
@@ -465,9 +516,7 @@ def sampled_first_step(cfg, cloud, sample, k_range=None):
 
     def interior_f1(i):
         nb = neighbors_of(x, c.h2, i)
-        S, a = wls_one(x, i, nb, c.h2, c.alpha_w, c.wls_order)
-        frs = np.stack([frame(x[j] - x[i]) for j in nb])
-        rot = np.stack([rotate(a[q], frs[q]) for q in range(len(nb))])
+        S, a, frs, rot = wls_particle(c, x, i, nb)
         W = cloud["U"][i] if c.ale else np.zeros(d)
         kb, ke = (0, K) if k_range is None else k_range
         ft = transport_one(c, W, rot, frs, [row0(int(j)) for j in nb], row0(i), kb, ke)

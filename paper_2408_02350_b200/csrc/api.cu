@@ -124,8 +124,7 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->vmin = -cfg->vmax;
     c->wls_order = cfg->wls_order == 2 ? 2 : 1;
     c->PD = (c->d == 2 ? 4 : 10) + (c->wls_order == 2 ? 2 : 0);
-    c->np = transport_particles_per_warp(c->d, c->wls_order);
-    c->R = transport_rows_per_thread(c->d, c->n1, c->np);
+    c->R = transport_rows_per_thread(c->d, c->n1);
     c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
     c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
     // 2D, 33 columns (N_v = 32): a 32-lane group for ONE column would idle 31 lanes -- the few
@@ -137,19 +136,10 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     if (c->tail_cols) c->ncg = c->ncol / 32;
     c->nwpp = c->nchunk * c->ncg + (c->tail_cols ? c->nchunk : 0);
     c->nslots = c->nwpp * 32;
-    // particle-pair warps: union of two lists, <= 2 max_nb int2 entries per pair, CSR positions < 2^16
-    c->ucap = 2 * c->max_nb;
-    if (c->np == 2 && c->max_nb >= 65536) {
-        c->np = 1;
-        c->R = transport_rows_per_thread(c->d, c->n1, 1);
-        c->nchunk = (c->n1 + c->R - 1) / c->R;
-        c->nwpp = c->nchunk * c->ncg + (c->tail_cols ? c->nchunk : 0);
-        c->nslots = c->nwpp * 32;
-    }
     // fixed-cloud lattice rows (SURVEY §8(d) "the one lever"): partial slots sized for both mappings
     {
         const char* e = getenv("BGK_TRANSPORT_ROWS");
-        c->rows_on = !cfg->ale && c->d == 3 && c->wls_order == 1 && c->np == 1 && c->ncol == c->ncol_g &&
+        c->rows_on = !cfg->ale && c->d == 3 && c->wls_order == 1 && c->ncol == c->ncol_g &&
                      c->Ncap < (1 << 23) && c->max_nb <= 256 &&
                      !(e && atoi(e) == 0);
         c->rows_nchunk = (c->n1 + kRowsR - 1) / kRowsR;
@@ -226,9 +216,6 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->g.bcw = k.take<double>(c->cap);
     c->g.bcnt = k.take<int32_t>(N);
     c->g.order = k.take<int32_t>(N);
-    const int64_t ng = c->np == 2 ? (N + 1) / 2 : 1;
-    c->gU = k.take<int32_t>(c->np == 2 ? (size_t)ng * c->ucap * 2 : 2);   // int2 entries
-    c->gUlen = k.take<int32_t>(4 * ng);
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     {
@@ -276,15 +263,17 @@ const char* code_msg(int code) {
 bgk_status sync_check(bgk_ctx* c, cudaStream_t s) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(c, e);
-    int64_t h[2];
-    e = cudaMemcpy(h, c->err, sizeof(h), cudaMemcpyDeviceToHost);
+    unsigned long long h = 0;
+    e = cudaMemcpy(&h, c->err, sizeof(h), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(c, e);
-    if (h[0] != 0) {
-        std::snprintf(c->msg, sizeof(c->msg), "%s", code_msg((int)h[0]));
-        c->bad = h[1] == INT64_MAX ? -1 : h[1];
-        const int64_t reset[2] = {0, INT64_MAX};
-        cudaMemcpy(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice);
-        return (bgk_status)h[0];
+    if (h != 0) {                       // latch_error's packed word: code << 56 | particle
+        const int code = (int)(h >> 56);
+        const unsigned long long part = h & kErrNoParticle;
+        std::snprintf(c->msg, sizeof(c->msg), "%s", code_msg(code));
+        c->bad = part == kErrNoParticle ? -1 : (int64_t)part;
+        const unsigned long long reset = 0;
+        cudaMemcpy(c->err, &reset, sizeof(reset), cudaMemcpyHostToDevice);
+        return (bgk_status)code;
     }
     return BGK_OK;
 }
@@ -334,7 +323,6 @@ bgk_status ensure_geometry(bgk_ctx* c, cudaStream_t s) {
         }
         launch_wls(c, s);
         launch_bnd_union(c, s);
-        launch_group_union(c, s);
         c->geometry_valid = true;
         c->rows_built = false;
         if (c->rows_on) {                         // fixed cloud: detect the lattice rows once
@@ -399,12 +387,17 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
         bgk_status st = install_lists(c, hk.data(), hx.data(), s);
         if (st != BGK_OK) { delete c; return st; }
     }
-    const int64_t reset[4] = {0, INT64_MAX, 0, 0};
+    const int64_t reset[4] = {0, 0, 0, 0};
     cudaMemcpyAsync(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice, s);
-    // padding columns stay zero forever (TMA boxes of the last column group read them)
-    cudaMemsetAsync(c->f[0], 0, sizeof(double) * N * c->RS, s);
-    cudaMemsetAsync(c->f[1], 0, sizeof(double) * N * c->RS, s);
+    // padding columns stay zero forever (TMA boxes of the last column group read them): both
+    // buffers are cleared over the whole capacity, so rows that management appends past the
+    // initial N start with zero padding too (the kernels only ever write valid columns)
+    cudaMemsetAsync(c->f[0], 0, sizeof(double) * c->Ncap * c->RS, s);
+    cudaMemsetAsync(c->f[1], 0, sizeof(double) * c->Ncap * c->RS, s);
     cudaMemsetAsync(c->stab, 0, sizeof(unsigned long long), s);
+    // rank-local sums exchanged by the caller (all-reduce): defined for every slot, boundary rows too
+    cudaMemsetAsync(c->sums, 0, sizeof(double) * c->Ncap * kPM, s);
+    cudaMemsetAsync(c->wallnum, 0, sizeof(double) * c->Ncap, s);
     cudaMemcpyAsync(c->x, hx.data(), sizeof(double) * N * c->d, cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(c->kind, hk.data(), N, cudaMemcpyHostToDevice, s);
     const double* m0 = nullptr;
@@ -467,9 +460,10 @@ bgk_status bgk_get_wls(bgk_ctx* c, double* Sout, double* rot, double* frames, do
     if (!c) return BGK_E_INVALID_ARG;
     cudaStream_t s = S(stream);
     const int d = c->d;
+    bgk_status st = sync_check(c, s);        // in-flight geometry work finishes before nnz is read
+    if (st != BGK_OK) return st;
     int64_t nnz = 0;
     cudaMemcpy(&nnz, c->g.nb_off + c->N, sizeof(int64_t), cudaMemcpyDeviceToHost);
-    bgk_status st;
     if (Sout && (st = copy_out(c, Sout, c->g.S, sizeof(double) * c->N * d * d, s)) != BGK_OK) return st;
     if (cw && nnz && (st = copy_out(c, cw, c->g.cw, sizeof(double) * nnz, s)) != BGK_OK) return st;
     if (rot || frames) {
@@ -667,7 +661,6 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
     if (c->cfg.ale) k += launches_neighbors() + launches_wls() - (c->N_b ? 0 : 1) - (c->N_int ? 0 : 1);
     if (c->cfg.ale && c->cfg.manage) k += 2;   // k_mg_detect + k_mg_decide (plus 3 more and a neighbour
                                                // rebuild in the rare steps where the cloud changes)
-    if (c->cfg.ale && c->np == 2) k += 1;      // k_pair_union
     if (c->N_int) k += 3;        // transport, moment reduce, relax
     if (c->N_b) k += 3;          // boundary interp, wall reduce, fill
     *n = k;
@@ -703,11 +696,22 @@ bgk_status bgk_stage_f(bgk_ctx* c, const double* f, bgk_stream copy_stream) {
     if (e == cudaSuccess) e = cudaEventRecord(c->ev_staged, cs);
     if (e != cudaSuccess) return cuda_fail(c, e);
     c->stage_pending = true;
+    c->stage_N = c->N;                 // the staged rows belong to this cloud (size and numbering)
+    c->stage_gen = c->cloud_gen;
     return BGK_OK;
 }
 
 bgk_status bgk_use_staged_f(bgk_ctx* c, bgk_stream stream) {
     if (!c || !c->cfg.staging || !c->stage_pending) return BGK_E_INVALID_ARG;
+    if (c->stage_N != c->N || c->stage_gen != c->cloud_gen) {
+        // particle management changed N or renumbered the rows after bgk_stage_f: the staged
+        // rows no longer match the cloud (the copy itself completed within the old size)
+        std::snprintf(c->msg, sizeof(c->msg), "staged f was copied for %lld particles before the cloud changed "
+                      "(now %lld); stage it again", (long long)c->stage_N, (long long)c->N);
+        c->bad = -1;
+        c->stage_pending = false;
+        return BGK_E_INVALID_ARG;
+    }
     cudaStream_t s = S(stream);
     cudaError_t e = cudaStreamWaitEvent(s, c->ev_staged, 0);
     if (e != cudaSuccess) return cuda_fail(c, e);
@@ -742,7 +746,7 @@ bgk_status bgk_count(bgk_ctx* c, int64_t* N, int64_t* n_interior, int64_t* n_bou
 
 bgk_status bgk_transport_info(bgk_ctx* c, int64_t* info) {
     if (!c || !info) return BGK_E_INVALID_ARG;
-    info[0] = c->np;
+    info[0] = 1;                      // particles per transport warp
     info[1] = c->R;
     info[2] = c->rows_built ? c->n_rows : 0;
     info[3] = c->rows_built ? c->n_rest : c->N_int;

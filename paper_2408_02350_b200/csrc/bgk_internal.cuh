@@ -101,11 +101,8 @@ struct bgk_ctx {
     double* Mw;         // [2d][RS] wall Maxwellians M(1, U_w, T_w) on the outgoing nodes of each wall, -1 elsewhere
     double* wall_den;   // [2d] sum_{v.n>0} (v.n) M_w over the GLOBAL grid
     double* outbuf;     // [N][d+2] scratch for moments / copies
-    int64_t* err;       // [4] code, particle, needed, spare
+    int64_t* err;       // [4] packed (code << 56 | particle) word (latch_error), spare
     unsigned long long* stab;  // [1] max_{i,k} sum_j |C_ijk| as ordered bits
-    int32_t* gU;        // [groups][ucap] packed union (j << 4 | member mask) of each particle group's lists
-    int32_t* gUlen;     // [groups]
-    int ucap;
     bgk::Manage mg;     // particle-management scratch (cfg.manage)
     double* stage;      // [Ncap][nv*Kloc] canonical input staging buffer (cfg.staging)
     // grouped boundary interpolation (relax.cu, BGK_BND_G): union of bnd_g consecutive boundary
@@ -117,6 +114,9 @@ struct bgk_ctx {
     int32_t* bu_n;      // [groups]
     cudaEvent_t ev_staged, ev_consumed;
     bool stage_pending;
+    int64_t stage_N;        // N when the staged copy was enqueued
+    uint64_t stage_gen;     //   and the cloud generation (bgk_use_staged_f refuses a changed cloud)
+    uint64_t cloud_gen;     // incremented whenever particle management changes N or the row numbering
     int64_t mg_report[6];   // host copy of the last pass's report
     // fixed-cloud lattice rows (transport_rows.cu): groups of kRowsG consecutive particles along x
     // with identical neighbour offsets share the pair coefficients and every neighbour box
@@ -129,7 +129,6 @@ struct bgk_ctx {
     int16_t* rows_perm;     // [Ncap / kRowsG][256] p0's neighbour entries in run order
     int32_t* order_rest;// [Ncap] the rest, in cell order
     int rows_nchunk;    // velocity chunks of kRowsR nodes along v_1
-    int np;             // particles per transport warp (1: per-warp neighbour ring; 2, 4: shared union)
     int64_t* scan_tmp;  // [1024]
     int32_t* blk_tmp;   // [1024] per-block partial counts of the multi-block scans
     bgk::Geo g;
@@ -158,10 +157,21 @@ __device__ __forceinline__ double dist2_rn(const double* xi, const double* xj) {
     return s;
 }
 
+// The device error word err[0]: error code in the top byte, offending particle in the low 56 bits
+// (kErrNoParticle: none).  The first code latched wins; later errors of the same code lower the
+// particle to the smallest index (deterministic), so code and particle always belong together.
+constexpr unsigned long long kErrNoParticle = 0x00FFFFFFFFFFFFFFull;
+
 __device__ __forceinline__ void latch_error(int64_t* err, int code, int64_t particle) {
     unsigned long long* e = reinterpret_cast<unsigned long long*>(err);
-    atomicCAS(e, 0ull, (unsigned long long)code);
-    atomicMin(reinterpret_cast<long long*>(err + 1), (long long)particle);
+    const unsigned long long pk = particle >= 0 ? (unsigned long long)particle & kErrNoParticle : kErrNoParticle;
+    const unsigned long long want = ((unsigned long long)code << 56) | pk;
+    unsigned long long old = atomicCAS(e, 0ull, want);
+    while (old != 0ull && (old >> 56) == (unsigned long long)code && (old & kErrNoParticle) > pk) {
+        const unsigned long long prev = atomicCAS(e, old, want);
+        if (prev == old) break;
+        old = prev;
+    }
 }
 
 template <typename T>
@@ -175,6 +185,17 @@ __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+}
+
+// Kernel attributes (cudaFuncSetAttribute: the dynamic shared-memory opt-in) are per device: a
+// launcher keeps one flag per device and sets the attribute the first time it runs on each.
+constexpr int kMaxDevices = 64;
+inline bool first_use_on_device(bool (&done)[kMaxDevices]) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return true;
+    if (done[dev]) return false;
+    done[dev] = true;
+    return true;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -194,8 +215,7 @@ void launch_moments_finalize(bgk_ctx* c, double* out, cudaStream_t s);
 void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_check_domain(bgk_ctx* c, cudaStream_t s);
-int transport_rows_per_thread(int d, int n1, int np);
-int transport_particles_per_warp(int d, int wls_order);
+int transport_rows_per_thread(int d, int n1);
 bool make_tensor_maps(bgk_ctx* c);
 // fixed-cloud lattice rows: host-side group detection on the cached geometry, and the kernel
 bgk_status build_rows(bgk_ctx* c, cudaStream_t s);
@@ -206,7 +226,6 @@ __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int
     return k1 * ncs + (t - k1 * ncol);
 }
 int launches_neighbors();
-void launch_group_union(bgk_ctx* c, cudaStream_t s);
 int launches_wls();
 // particle management: one pass (synchronises the stream); *changed = N or indices changed
 bgk_status manage_pass(bgk_ctx* c, cudaStream_t s, bool* changed);

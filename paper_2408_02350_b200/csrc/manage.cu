@@ -486,6 +486,7 @@ bgk_status run_pass(bgk_ctx* c, cudaStream_t s, bool* changed) {
     cudaMemcpyAsync(c->kind, m.kind, (size_t)n_out, cudaMemcpyDeviceToDevice, s);
     c->fcur = 1 - c->fcur;
     c->N = n_out;
+    ++c->cloud_gen;                     // rows renumbered: a pending staged input is stale
     std::vector<int8_t> hk(n_out);
     std::vector<double> hx(n_out * D);
     e = cudaMemcpyAsync(hk.data(), c->kind, (size_t)n_out, cudaMemcpyDeviceToHost, s);

@@ -753,10 +753,9 @@ void launch_bnd_union(bgk_ctx* c, cudaStream_t s) {
 template <int D, int G>
 void bnd_interp_g(bgk_ctx* c, double* fnew, cudaStream_t s) {
     const size_t smem = (size_t)c->bu_cap * (G * sizeof(double) + sizeof(int32_t));
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[kMaxDevices] = {};
+    if (first_use_on_device(configured)) {
         cudaFuncSetAttribute(k_bnd_interp_u<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        configured = true;
     }
     dim3 gg((unsigned)((c->N_b + G - 1) / G), (unsigned)c->bnd_nch);
     k_bnd_interp_u<D, G><<<gg, kBndChunk, smem, s>>>(c->boundary, c->N_b, c->kind, c->bu_j, c->bu_w, c->bu_n,

@@ -42,7 +42,6 @@ namespace bgk {
 namespace {
 
 constexpr int kDefaultWarps = 4;   // warps per block; tuned on B200 (profiles/r01_tuning.md)
-constexpr int kDefaultNP = 1;      // particles per warp of the 3D first-order transport (BGK_TRANSPORT_NP)
 
 struct TArgs {
     const double* __restrict__ f;
@@ -54,9 +53,6 @@ struct TArgs {
     const double* __restrict__ P;
     double* __restrict__ partials;
     unsigned long long* stab;
-    const int32_t* __restrict__ gU;    // multi-particle warps: packed union list per particle group
-    const int32_t* __restrict__ gUlen; //                       its length
-    int ucap;                          //                       capacity per group
     bool signed_n;                     // second-order WLS: pair record carries s_n = -sign(abar)
     int64_t n_int;
     int n1, ncol, ncs, c0, ncg, nwpp;   // nwpp: partial slots per particle (stride)
@@ -303,9 +299,6 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
         const int s = (int)((g0 + (uint32_t)e) % NST);
         unsigned char* st = ring + s * St::BYTES;
         mbar_expect_tx(bars + s, St::F_BYTES + St::P_BYTES);
-#ifdef BGK_EXP_SAMEBOX
-        jn = p;   // timing experiment: always the particle's own (L2-hot) box
-#endif
         tma_load_3d(st, &tmap, cg * ROW, k1s, jn, bars + s);
         bulk_load(st + St::F_BYTES, Pp + (int64_t)e * PD, St::P_BYTES, bars + s);
     };
@@ -413,15 +406,9 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
         }
         const int jn = __shfl_sync(0xffffffffu, nbA, t & 31);
         __syncwarp();   // every lane has consumed the stage before it is refilled
-#ifndef BGK_EXP_NOPIPE   // timing experiment: no refills, no waits (stale data; compute ceiling)
         if (t < m && elect_one()) issue(t, jn);
-#endif
         if (more) {
-#ifndef BGK_EXP_NOPIPE
             if (!nready) mbar_wait(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u);
-#else
-            (void)nready;
-#endif
             asm volatile("" ::: "memory");                 // order the stage reads after the test
             coeffs(e + 1, y, dy, Lc, dL, sn);
         }
@@ -573,231 +560,6 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
     for (int k = 0; k < G; ++k) transport_epilogue<3, R, false>(A, p0 + k * S, w, k1s, colc, gc, valid, Qf[k], Sc, Sa);
 }
 
-// ============================================================================
-// Particle-pair warps (3D, first-order WLS).  A warp owns TWO consecutive particles A, B of the
-// cell-ordered interior list, one chunk of R nodes along v_1 and 32 velocity columns, and walks
-// the UNION of their neighbour lists (k_pair_union, rebuilt with the geometry), sorted into three
-// segments: members of both lists, of A only, of B only (ascending j inside each; the order in
-// which a particle's neighbours are summed is free up to rounding, Z22).  Each member's box
-// f[j][k1s .. k1s+R)[cols] is fetched ONCE by TMA and applied to every particle that has j --
-// on C5 the union of two neighbouring particles has 0.67x their combined members, so the
-// L2 -> SM traffic per (i, j, k) triple (the bound of the one-particle kernel: ~6.6 kB/clk,
-// the chip's L2 throughput cap) drops by a third.  The segment is known from the member's
-// position, so the inner loops carry no per-member mask test; members of both lists run one
-// fused row loop (one LDS of f_jk for two particles).  Warps stay independent.
-// Measured on C5 (profiles/r01_tuning.md): 96 ms against 74 ms for the one-particle kernel --
-// R = 13 (register budget of four accumulator rows) doubles the per-neighbour setup and the
-// L2 traffic was not the binding limit; kept as an opt-in (BGK_TRANSPORT_NP=2), parity-tested.
-// Union entries: int2 {j, eA | eB << 16} (CSR positions of j in A's and B's lists); counts
-// gUlen[4 g + {0, 1, 2}] = (both, A only, B only).
-// ============================================================================
-template <int R>
-struct PStage {
-    static constexpr int PD = 10;
-    static constexpr uint32_t F_BYTES = R * 32 * sizeof(double);
-    static constexpr uint32_t P_BYTES = PD * sizeof(double);
-    static constexpr uint32_t BYTES = (F_BYTES + 2 * P_BYTES + 127) / 128 * 128;
-};
-
-// y_e = P_e . c at the chunk's first node and dy_e = dv P_e[0] (pair record slot 3e), 3D
-__device__ __forceinline__ void pair_y(const double* ps, double c1dv, double c2, double c3, double (&y)[3],
-                                       double (&dy)[3]) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        dy[k] = ps[k * 3];
-        y[k] = fma(ps[k * 3], c1dv, fma(ps[k * 3 + 1], c2, ps[k * 3 + 2] * c3));
-    }
-}
-
-template <int R, int NST, int WPB, int MINB>
-__global__ void __launch_bounds__(WPB * 32, MINB) k_transport_pair(const __grid_constant__ CUtensorMap tmap,
-                                                                   const TArgs A) {
-    using St = PStage<R>;
-    constexpr int PD = St::PD;
-    constexpr int ROW = 32;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned char* ring = smem_raw + (size_t)wib * NST * St::BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)WPB * NST * St::BYTES) + wib * NST;
-    if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncwarp();
-    const int w = blockIdx.y;
-    const int64_t grp = (int64_t)blockIdx.x * WPB + wib;
-    if (2 * grp >= A.n_int) return;                       // warp-uniform
-    const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
-    const int col = cg * 32 + lane;
-    const bool valid = col < A.ncol;
-    const int k1s = chunk * R;
-    const int colc = valid ? col : 0;
-    const int gc = A.c0 + colc;
-    const int k2 = gc / A.n1, k3 = gc - k2 * A.n1;
-    const int pA = A.order[2 * grp];
-    const int pB = 2 * grp + 1 < A.n_int ? A.order[2 * grp + 1] : -1;
-    const double* PA = A.P + A.nb_off[pA] * PD;
-    const double* PB = A.P + (pB >= 0 ? A.nb_off[pB] : 0) * PD;
-    double c1A, c2A, c3A, c1B, c2B, c3B;                  // c = v(k1s, col) - W (c1 in units of dv)
-    {
-        const double v1 = axis_node(A.vmax, A.dv, k1s), v2 = axis_node(A.vmax, A.dv, k2),
-                     v3 = axis_node(A.vmax, A.dv, k3);
-        const double* Wa = A.W + (int64_t)pA * 3;
-        const double* Wb = A.W + (int64_t)(pB >= 0 ? pB : pA) * 3;
-        c1A = (v1 - Wa[0]) / A.dv;
-        c2A = v2 - Wa[1];
-        c3A = v3 - Wa[2];
-        c1B = (v1 - Wb[0]) / A.dv;
-        c2B = v2 - Wb[1];
-        c3B = v3 - Wb[2];
-    }
-    const int nboth = A.gUlen[4 * grp], nA = A.gUlen[4 * grp + 1], nBo = A.gUlen[4 * grp + 2];
-    const int segA = nboth, segB = nboth + nA, ulen = segB + nBo;
-    const int2* ul = reinterpret_cast<const int2*>(A.gU) + grp * A.ucap;
-    int2 nbA = lane < ulen ? ul[lane] : make_int2(0, 0);   // union entries, 32 per register batch
-    int2 nbB = 32 + lane < ulen ? ul[32 + lane] : make_int2(0, 0);
-
-    auto issue = [&](int t, int j, int ee) {               // one elected lane: stage of member t
-        const int s = t % NST;
-        unsigned char* st = ring + s * St::BYTES;
-        const bool hasA = t < segB, hasB = t < segA || t >= segB;
-        mbar_expect_tx(bars + s, St::F_BYTES + (uint32_t)(hasA + hasB) * St::P_BYTES);
-        tma_load_3d(st, &tmap, cg * ROW, k1s, j, bars + s);
-        if (hasA) bulk_load(st + St::F_BYTES, PA + (int64_t)(ee & 0xffff) * PD, St::P_BYTES, bars + s);
-        if (hasB) bulk_load(st + St::F_BYTES + St::P_BYTES, PB + (int64_t)(ee >> 16) * PD, St::P_BYTES, bars + s);
-    };
-#pragma unroll
-    for (int s = 0; s < NST; ++s) {
-        const int j = __shfl_sync(0xffffffffu, nbA.x, s), ee = __shfl_sync(0xffffffffu, nbA.y, s);
-        if (s < ulen && elect_one()) issue(s, j, ee);
-    }
-
-    double QA[R], SA[R], QB[R], SB[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) QA[r] = SA[r] = QB[r] = SB[r] = 0.0;
-    for (int e = 0; e < ulen; ++e) {
-        const unsigned char* stb = ring + (e % NST) * St::BYTES;
-        mbar_wait(bars + e % NST, (uint32_t)(e / NST) & 1u);
-        const double* st = reinterpret_cast<const double*>(stb) + lane;
-        const double* psA = reinterpret_cast<const double*>(stb + St::F_BYTES);
-        const double* psB = reinterpret_cast<const double*>(stb + St::F_BYTES + St::P_BYTES);
-        double yA[3], dyA[3], yB[3], dyB[3];
-        if (e < segA) {                                    // member of both lists: one fused row loop
-            pair_y(psA, c1A, c2A, c3A, yA, dyA);
-            pair_y(psB, c1B, c2B, c3B, yB, dyB);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double fj = st[r * ROW];
-                const double CA = neg_part(fma((double)r, dyA[0], yA[0])) + neg_part(fma((double)r, dyA[1], yA[1])) +
-                                  neg_part(fma((double)r, dyA[2], yA[2]));
-                const double CB = neg_part(fma((double)r, dyB[0], yB[0])) + neg_part(fma((double)r, dyB[1], yB[1])) +
-                                  neg_part(fma((double)r, dyB[2], yB[2]));
-                QA[r] = fma(CA, fj, QA[r]);
-                SA[r] += CA;
-                QB[r] = fma(CB, fj, QB[r]);
-                SB[r] += CB;
-            }
-        } else if (e < segB) {                             // A only
-            pair_y(psA, c1A, c2A, c3A, yA, dyA);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double CA = neg_part(fma((double)r, dyA[0], yA[0])) + neg_part(fma((double)r, dyA[1], yA[1])) +
-                                  neg_part(fma((double)r, dyA[2], yA[2]));
-                QA[r] = fma(CA, st[r * ROW], QA[r]);
-                SA[r] += CA;
-            }
-        } else {                                           // B only
-            pair_y(psB, c1B, c2B, c3B, yB, dyB);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double CB = neg_part(fma((double)r, dyB[0], yB[0])) + neg_part(fma((double)r, dyB[1], yB[1])) +
-                                  neg_part(fma((double)r, dyB[2], yB[2]));
-                QB[r] = fma(CB, st[r * ROW], QB[r]);
-                SB[r] += CB;
-            }
-        }
-        // refill the consumed stage with member e + NST
-        const int t = e + NST;
-        if ((t & 31) == 0) {                               // warp-uniform batch rotation
-            nbA = nbB;
-            nbB = t + 32 + lane < ulen ? ul[t + 32 + lane] : make_int2(0, 0);
-        }
-        const int j = __shfl_sync(0xffffffffu, nbA.x, t & 31), ee = __shfl_sync(0xffffffffu, nbA.y, t & 31);
-        __syncwarp();                                      // every lane has consumed the stage
-        if (t < ulen && elect_one()) issue(t, j, ee);
-    }
-    const double Sa[1] = {0.0};
-    double (&QAv)[R][1] = *reinterpret_cast<double (*)[R][1]>(&QA);
-    double (&QBv)[R][1] = *reinterpret_cast<double (*)[R][1]>(&QB);
-    transport_epilogue<3, R, false>(A, pA, w, k1s, colc, gc, valid, QAv, SA, Sa);
-    if (pB >= 0) transport_epilogue<3, R, false>(A, pB, w, k1s, colc, gc, valid, QBv, SB, Sa);
-}
-
-// Union of the neighbour lists of each particle pair (A, B) = order[2g], order[2g+1], in three
-// segments (both / A only / B only, ascending j in each) with the CSR positions of j in A's and
-// B's lists.  One warp per pair: membership by binary search in the other (ascending) list,
-// positions by ballot prefix counts.
-__global__ void __launch_bounds__(128) k_pair_union(const int32_t* __restrict__ order, int64_t n_int,
-                                                    const int64_t* __restrict__ nb_off,
-                                                    const int32_t* __restrict__ nb_idx, int ucap,
-                                                    int2* __restrict__ gU, int32_t* __restrict__ gUlen) {
-    const int lane = threadIdx.x & 31;
-    const int64_t grp = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (2 * grp >= n_int) return;
-    const int pA = order[2 * grp];
-    const int pB = 2 * grp + 1 < n_int ? order[2 * grp + 1] : -1;
-    const int32_t* LA = nb_idx + nb_off[pA];
-    const int mA = (int)(nb_off[pA + 1] - nb_off[pA]);
-    const int32_t* LB = pB >= 0 ? nb_idx + nb_off[pB] : nullptr;
-    const int mB = pB >= 0 ? (int)(nb_off[pB + 1] - nb_off[pB]) : 0;
-    auto find = [](const int32_t* L, int m, int v) {       // position of v in ascending L, or -1
-        int lo = 0, hi = m;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (L[mid] < v) lo = mid + 1;
-            else hi = mid;
-        }
-        return lo < m && L[lo] == v ? lo : -1;
-    };
-    int nboth = 0;
-    for (int b = 0; b < mA; b += 32) {                     // pass 1: size of the intersection
-        const int i = b + lane;
-        const bool hit = i < mA && find(LB, mB, LA[i]) >= 0;
-        nboth += __popc(__ballot_sync(0xffffffffu, hit));
-    }
-    int2* out = gU + grp * ucap;
-    const unsigned below = (1u << lane) - 1u;
-    int wb = 0, wa = nboth;
-    for (int b = 0; b < mA; b += 32) {                     // pass 2: both + A only
-        const int i = b + lane;
-        const int jb = i < mA ? find(LB, mB, LA[i]) : -1;
-        const unsigned hb = __ballot_sync(0xffffffffu, i < mA && jb >= 0);
-        const unsigned ha = __ballot_sync(0xffffffffu, i < mA && jb < 0);
-        if (i < mA) {
-            if (jb >= 0) out[wb + __popc(hb & below)] = make_int2(LA[i], i | (jb << 16));
-            else out[wa + __popc(ha & below)] = make_int2(LA[i], i);
-        }
-        wb += __popc(hb);
-        wa += __popc(ha);
-    }
-    int wo = mA;                                           // B only after both + A only
-    for (int b = 0; b < mB; b += 32) {
-        const int i = b + lane;
-        const bool only = i < mB && find(LA, mA, LB[i]) < 0;
-        const unsigned ho = __ballot_sync(0xffffffffu, only);
-        if (only) out[wo + __popc(ho & below)] = make_int2(LB[i], i << 16);
-        wo += __popc(ho);
-    }
-    if (lane == 0) {
-        gUlen[4 * grp] = nboth;
-        gUlen[4 * grp + 1] = mA - nboth;
-        gUlen[4 * grp + 2] = wo - mA;
-        gUlen[4 * grp + 3] = 0;
-    }
-}
-
 // 2D tail columns (N_v = 32: the 33rd column): warp per (interior particle, chunk of R nodes along
 // v_1), lane r owning row k1s + r, looping over the neighbours (pair record and neighbour index
 // broadcast, one 16-B load of (g1, g2) per lane); the same arithmetic as k_transport (C/2 =
@@ -880,11 +642,10 @@ template <int D, int R, int WPB, bool SG = false, int MINB = 1>
 void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     constexpr int NST = stages_for<D, R, WPB, SG, MINB>();
     constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG>::BYTES + WPB * NST * 8;
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[kMaxDevices] = {};
+    if (first_use_on_device(configured)) {
         cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        configured = true;
     }
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
     k_transport<D, R, NST, WPB, SG, MINB><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(tm, a);
@@ -893,11 +654,8 @@ void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
 template <int D, int R>
 void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     if (a.signed_n) return launch_one<D, R, kDefaultWarps, true>(tm, a, s);   // second-order WLS
-    if constexpr (D == 3 && (R == 25 || R == 13)) {
-        if (wpb == 8) return launch_one<D, R, 8>(tm, a, s);
+    if constexpr (D == 3 && R == 25) {
         if (wpb == 2) return launch_one<D, R, 2>(tm, a, s);
-        if (wpb == 43) return launch_one<D, R, 4, false, 3>(tm, a, s);   // 12 resident warps per SM
-        if (wpb == 44) return launch_one<D, R, 4, false, 4>(tm, a, s);   // 16 resident warps per SM
     }
     launch_one<D, R, kDefaultWarps>(tm, a, s);
 }
@@ -921,36 +679,6 @@ void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_
         case 5: launch_wpb<D, 5>(wpb, tm, a, s); break;
         case 3: launch_wpb<D, 3>(wpb, tm, a, s); break;
         default: launch_wpb<D, 1>(wpb, tm, a, s); break;
-    }
-}
-
-template <int R, int MINB = (R <= 13 ? 3 : 2)>        // 12 (8) resident warps per SM
-void launch_pair_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int WPB = kDefaultWarps;
-    constexpr int B = PStage<R>::BYTES;
-    constexpr int NST0 = (220 * 1024) / (MINB * WPB * B);
-    constexpr int NST = NST0 > 8 ? 8 : (NST0 < 2 ? 2 : NST0);
-    constexpr size_t smem = (size_t)WPB * NST * B + WPB * NST * 8;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_transport_pair<R, NST, WPB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        configured = true;
-    }
-    const int64_t ng = (a.n_int + 1) / 2;
-    const unsigned gx = (unsigned)((ng + WPB - 1) / WPB);
-    k_transport_pair<R, NST, WPB, MINB><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(tm, a);
-}
-
-constexpr int kPairR[] = {17, 13, 9, 5};   // rows per lane instantiated for particle-pair warps (R = 25: 255
-                                          // registers, rows serialise, 133 ms on C5)
-
-void dispatch_pair(int R, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    switch (R) {
-        case 17: return launch_pair_one<17>(tm, a, s);
-        case 13: return launch_pair_one<13>(tm, a, s);
-        case 9: return launch_pair_one<9>(tm, a, s);
-        default: return launch_pair_one<5>(tm, a, s);
     }
 }
 
@@ -980,28 +708,11 @@ bool listed(const int (&choices)[K], int R) {
 
 }  // namespace
 
-// particles per transport warp (3D first-order only): BGK_TRANSPORT_NP (1 or 2), default kDefaultNP
-int transport_particles_per_warp(int d, int wls_order) {
-    if (d != 3 || wls_order != 1) return 1;
-    int np = kDefaultNP;
-    if (const char* e = getenv("BGK_TRANSPORT_NP")) np = atoi(e);
-    return np == 2 ? 2 : 1;
-}
-
-void launch_group_union(bgk_ctx* c, cudaStream_t s) {
-    if (c->np != 2 || c->N_int == 0) return;
-    const int64_t ng = (c->N_int + 1) / 2;
-    k_pair_union<<<(unsigned)((ng + 3) / 4), 128, 0, s>>>(c->g.order, c->N_int, c->g.nb_off, c->g.nb_idx, c->ucap,
-                                                          reinterpret_cast<int2*>(c->gU), c->gUlen);
-}
-
 // rows per lane: BGK_TRANSPORT_R if instantiated for the mapping, else the instantiated R with
-// the fewest padded rows (pair warps: R is bounded by the register budget, 4 accumulators per
-// row; 2D keeps three accumulators per row, so it stops at 13)
-int transport_rows_per_thread(int d, int n1, int np) {
+// the fewest padded rows (2D keeps three accumulators per row, so it stops at 17)
+int transport_rows_per_thread(int d, int n1) {
     const char* e = getenv("BGK_TRANSPORT_R");
     const int want = e ? atoi(e) : 0;
-    if (np == 2) return listed(kPairR, want) ? want : fewest_padded(kPairR, n1);
     if (d == 3) return listed(kRChoices3, want) ? want : fewest_padded(kRChoices3, n1);
     return listed(kRChoices2, want) ? want : fewest_padded(kRChoices2, n1);
 }
@@ -1061,9 +772,6 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.vmax = c->cfg.vmax;
     a.dv = c->dv;
     a.dt = c->cfg.dt;
-    a.gU = c->gU;
-    a.gUlen = c->gUlen;
-    a.ucap = c->ucap;
     a.signed_n = c->wls_order == 2;
     const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
     if (c->rows_built && c->n_rows > 0) {          // fixed-cloud lattice rows + the general kernel on the rest
@@ -1072,7 +780,6 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
         a.order = c->order_rest;
         a.n_int = c->n_rest;
     }
-    if (c->np == 2) return dispatch_pair(c->R, tm, a, s);
     static const int wpb_env = [] {
         const char* e = getenv("BGK_TRANSPORT_WPB");   // tuning knob (2, 4, 8); default below
         return e ? atoi(e) : 0;
@@ -1203,10 +910,9 @@ bgk_status build_rows(bgk_ctx* c, cudaStream_t s) {
 void launch_transport_rows(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
     constexpr int WPB = 2;                     // 8 warps per SM at R = 3 (24 KB of windows per warp)
     constexpr size_t smem = WPB * kRowsWarpSmem;
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[kMaxDevices] = {};
+    if (first_use_on_device(configured)) {
         cudaFuncSetAttribute(k_transport_rows<WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        configured = true;
     }
     RowsArgs ra;
     TArgs& a = ra.t;
@@ -1230,9 +936,6 @@ void launch_transport_rows(bgk_ctx* c, const double* fin, double* fout, cudaStre
     a.vmax = c->cfg.vmax;
     a.dv = c->dv;
     a.dt = c->cfg.dt;
-    a.gU = nullptr;
-    a.gUlen = nullptr;
-    a.ucap = 0;
     a.signed_n = false;
     ra.p0 = c->rows_p0;
     ra.stride = c->rows_stride;

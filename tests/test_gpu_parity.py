@@ -338,20 +338,6 @@ def test_c5_ten_steps_invariants(torch_cuda):
     assert np.all(x >= 0) and np.all(x <= cfg.L)
 
 
-# ------------------------------------- particle-pair transport warps (opt-in)
-@pytest.mark.parametrize("cfg", [bi.C4, bi.CavityConfig("C4j", 3, 15, 8, jitter=0.3, dt=5e-12)])
-def test_pair_warp_transport_ten_steps(torch_cuda, cfg, monkeypatch):
-    """BGK_TRANSPORT_NP=2: one warp applies each union member's box to two particles (k_pair_union
-    segments both / A only / B only).  Same oracle bar as the one-particle kernel; the jittered
-    cloud has unequal, partially overlapping lists and an odd interior count (13^3: the last
-    warp holds one particle)."""
-    monkeypatch.setenv("BGK_TRANSPORT_NP", "2")
-    g, _ = gpu(cfg)
-    g.step(10)
-    g.sync()
-    check_state(g, oracle_run(cfg, 10), cfg)
-
-
 # -------------------------------------------------- degenerate cloud shapes
 @pytest.mark.parametrize("cfg", [bi.CavityConfig("open2d", 2, 17, 10, jitter=0.2, dt=4e-12),
                                  bi.CavityConfig("open3d", 3, 9, 6, jitter=0.2, dt=4e-12)])

@@ -223,6 +223,34 @@ def test_frames_orthonormal_right_handed(oracle_lib):
     np.testing.assert_allclose(F[2], [0, -1, 0], atol=1e-15)
 
 
+def test_frames_generic_angle_are_spherical_unit_vectors(oracle_lib):
+    """All three 3D frame rows at generic angles, pinned by their geometric meaning rather
+    than the trigonometric formula: n = e_r is the pair direction, b = e_phi is the horizontal unit
+    vector z x n / |z x n| (this fixes the rotation of (t, b) about n that orthonormality and
+    right-handedness leave free), and t = e_theta = b x n (so t_z = -sin(theta) <= 0, t lies in the
+    vertical plane through n and z)."""
+    rng = np.random.default_rng(17)
+    z = np.array([0.0, 0.0, 1.0])
+    for _ in range(500):
+        dj = rng.normal(size=3) * rng.uniform(0.1, 3.0)
+        F = oracle_lib.frame(dj)
+        n = dj / np.linalg.norm(dj)
+        b = np.cross(z, n)
+        b /= np.linalg.norm(b)
+        t = np.cross(b, n)
+        np.testing.assert_allclose(F[0], n, atol=2e-15)
+        np.testing.assert_allclose(F[2], b, atol=2e-15)
+        np.testing.assert_allclose(F[1], t, atol=2e-15)
+        assert F[2][2] == 0.0 and F[1][2] <= 0.0
+        # t is coplanar with z and n (zero triple product), and points away from the north pole
+        assert abs(np.dot(np.cross(z, n), F[1])) <= 2e-15
+        assert np.dot(F[1], z - n[2] * n) <= 1e-15
+    # azimuth quadrants: b follows phi = atan2(dy, dx) through all four quadrants
+    for dx_, dy_, bx, by in ((1, 1, -1, 1), (-1, 1, -1, -1), (-1, -1, 1, -1), (1, -1, 1, 1)):
+        F = oracle_lib.frame([dx_, dy_, 0.5])
+        np.testing.assert_allclose(F[2][:2], np.array([bx, by]) / np.sqrt(2), atol=1e-15)
+
+
 @pytest.mark.parametrize("k", range(4))
 def test_rotation_positive_abar_and_completeness(oracle_lib, k):
     cfg, x, kind = _clouds()[k]
