@@ -224,6 +224,70 @@ def cpu_baseline(cfg, cloud, seconds: float, full: bool = False):
             "whole_steps": whole, **info}
 
 
+def lean_count(dims: int) -> float:
+    """fp64 instructions per (particle, neighbour, node) triple -- 10 in 3D, 8 in
+    2D-Chu (two projections, two neg-parts, C, two accumulates shared by g1 and g2, sum C)."""
+    return 10.0 if dims == 3 else 8.0
+
+
+def measure_2d(cfg, dev, steps: int, warmup: int, peaks: dict):
+    """A 2D workload as a secondary bench line (the configs where the HBM
+    roofline is the binding one): whole ALE steps with particle management (CUDA events, the graph
+    path of bgk_step), per-phase times, achieved HBM GB/s at 32 B per value and two values (g1, g2)
+    per node, and the transport's fp64 roofline at the 2D lean count."""
+    import torch
+
+    from paper_2408_02350_b200 import Bgk
+    from paper_2408_02350_b200 import _lib
+    cfg = cfg.replace(manage=1)
+    cloud = bi.make_cloud(cfg)
+    g = Bgk(cfg, cloud, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        g.step(1)
+    g.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(steps):
+        g.step(1)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    g.sync()
+    phases = _lib.PHASES
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(phases) + 1)]
+    acc = np.zeros(len(phases))
+    nph = 10
+    for _ in range(nph):
+        ev[0].record(stream)
+        for q in range(len(phases)):
+            g.run_phase(q)
+            ev[q + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        acc += [ev[q].elapsed_time(ev[q + 1]) for q in range(len(phases))]
+    ph = {p: float(v / nph) for p, v in zip(phases, acc)}
+    g.sync()
+    N, K = g.N, cfg.n_nodes
+    off, _ = g.neighbors()
+    sum_m = int(np.diff(off)[cloud["kind"] == 0].sum())
+    hbm_gbs = 32.0 * 2 * N * K / (ms / 1e3) / 1e9
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    peak_instr = N_SM * FP64_LANES_PER_SM * sm_max * 1e6
+    algo = lean_count(2) * sum_m * K
+    info = g.transport_info()
+    g.close()
+    return {"workload": cfg.name, "ms_per_step": ms, "value": N * K / (ms / 1e3), "unit": UNIT, "steps": steps,
+            "particles": N, "velocity_nodes": K, "interior_pairs": sum_m, "particle_management": True,
+            "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / float(peaks.get("hbm_gbs", 6650.0)),
+            "hbm_bytes_per_step": 32.0 * 2 * N * K, "phases_ms": ph,
+            "transport_roofline": {"bound": "alu", "achieved": algo / (ph["transport"] / 1e3) / 1e12,
+                                   "peak": peak_instr / 1e12, "unit": "T fp64-instr/s",
+                                   "frac": algo / (ph["transport"] / 1e3) / peak_instr,
+                                   "per_unit": f"{lean_count(2):g} fp64 instr per triple x {sum_m} pairs x {K} nodes"},
+            "transport_mapping": {"particles_per_warp": info[0], "nodes_per_lane": info[1]}}
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -323,20 +387,24 @@ def run_ours(args):
     sum_m = int(np.diff(off)[inter].sum())
     k_loc = g.Kloc
     t_tr = phase_ms["transport"] / 1e3
-    instr_per_triple = 10.0          # SURVEY.md §8(d) lean count: 3 projections + 5 add/abs + 2 accumulates
+    # SURVEY.md §8(d) lean count: 3D 10 (3 projections + 5 add/abs + 2 accumulates), 2D-Chu 8
+    instr_per_triple = lean_count(cfg.dims)
     algo_instr = instr_per_triple * sum_m * k_loc
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     peak_instr = N_SM * FP64_LANES_PER_SM * sm_max * 1e6
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "transport_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(cfg.name)
+            tj = json.load(open(tp))
+            traffic = tj.get(cfg.name)
+            traffic_src = tj.get("_note")
         except Exception:
             traffic = None
     roofline = {"bound": "alu", "kernel": "k_transport (fp64 pipe)",
                 "achieved": algo_instr / t_tr / 1e12, "peak": peak_instr / 1e12,
                 "unit": "T fp64-instr/s", "frac": algo_instr / t_tr / peak_instr, "traffic": traffic,
+                "traffic_src": traffic_src,
                 "per_unit": f"{instr_per_triple:g} fp64 instr per (particle, neighbour, node) triple; "
                             f"{sum_m} interior pairs x {k_loc} local nodes",
                 "peak_src": f"{N_SM} SM x {FP64_LANES_PER_SM} FP64 lanes x {sm_max:.0f} MHz (sm_max of "
@@ -439,6 +507,8 @@ def run_ours(args):
                             "value": N * K / (ms2 / 1e3), "unit": UNIT, "steps": n2,
                             "lattice_row_groups": info[2], "general_kernel_particles": info[3]}
         g2.close()
+    if world == 1 and cfg.dims == 3 and not args.no_secondary:
+        out["secondary_2d"] = [measure_2d(c2, dev, 50, 5, peaks) for c2 in (bi.C2, bi.C3)]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, cloud, args.cpu_seconds, args.cpu_full)
     if rank == 0:

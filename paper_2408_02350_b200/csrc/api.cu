@@ -91,19 +91,16 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->Kloc = (int64_t)c->n1 * c->ncol;
     // 3D row stride padded to a multiple of 16 doubles (128 B): every 256-B box row of a column group
     // then starts on a cache line and covers exactly 8 L2 sectors (C5 transport: 75.7 ms at 16-B
-    // rows, 73.4 at 32 B, 72.8 at 64 B, 71.4 at 128 B; profiles/r01_tuning.md); BGK_NCS_ALIGN overrides
+    // rows, 73.4 at 32 B, 72.8 at 64 B, 71.4 at 128 B; profiles/r01_tuning.md); BGK_NCS_ALIGN overrides.
+    // 2D rows stay unpadded: the particle-set kernel copies a chunk of consecutive local nodes
+    // (k1 * ncol + col) of a neighbour's row with one bulk copy, which needs ncs == ncol.
     {
         static const int al = [] {
             const char* e = getenv("BGK_NCS_ALIGN");
             const int v = e ? atoi(e) : 16;
             return (v == 2 || v == 4 || v == 8 || v == 16) ? v : 16;
         }();
-        static const int al2 = [] {   // 2D: (g1, g2) = 16 B per column; padding to 128-B rows (8) measured
-            const char* e = getenv("BGK_NCS2_ALIGN");   // no gain on C2/C3 (profiles/r01_tuning.md): default 1
-            const int v = e ? atoi(e) : 1;
-            return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 1;
-        }();
-        c->ncs = c->d == 3 ? (c->ncol + al - 1) / al * al : (c->ncol + al2 - 1) / al2 * al2;
+        c->ncs = c->d == 3 ? (c->ncol + al - 1) / al * al : c->ncol;
     }
     c->Ks = (int64_t)c->n1 * c->ncs;
     c->RS = c->Ks * c->nv;
@@ -125,16 +122,18 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->wls_order = cfg->wls_order == 2 ? 2 : 1;
     c->PD = (c->d == 2 ? 4 : 10) + (c->wls_order == 2 ? 2 : 0);
     c->R = transport_rows_per_thread(c->d, c->n1);
-    c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
-    c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
-    // 2D, 33 columns (N_v = 32): a 32-lane group for ONE column would idle 31 lanes -- the few
-    // columns past the last full group go to a thread-per-(particle, chunk) tail kernel instead
-    c->tail_cols = (c->d == 2 && c->ncol > 32 && c->ncol % 32 != 0 && c->ncol % 32 <= 4 &&
-                    (c->R == 17 || c->R == 13 || c->R == 11 || c->R == 9) && c->wls_order == 1)
-                       ? c->ncol % 32
-                       : 0;
-    if (c->tail_cols) c->ncg = c->ncol / 32;
-    c->nwpp = c->nchunk * c->ncg + (c->tail_cols ? c->nchunk : 0);
+    if (c->d == 3) {
+        c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
+        c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
+        c->nwpp = c->nchunk * c->ncg;
+    } else {
+        // 2D: a warp = (set of set_P particles, chunk of 32*set_QC consecutive local nodes)
+        set_mapping_2d(c->wls_order, &c->set_P, &c->set_QC);
+        c->nchunk = (int)((c->Kloc + 32 * c->set_QC - 1) / (32 * c->set_QC));
+        c->ncg = 1;
+        c->nwpp = c->nchunk;
+        c->su_cap = c->set_P * c->max_nb;
+    }
     c->nslots = c->nwpp * 32;
     // fixed-cloud lattice rows (SURVEY §8(d) "the one lever"): partial slots sized for both mappings
     {
@@ -198,6 +197,7 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->wall_den = k.take<double>(2 * d);
     c->outbuf = k.take<double>(N * (d + 2));
     c->err = k.take<int64_t>(4);
+    c->gflag = k.take<int64_t>(2);
     c->stab = k.take<unsigned long long>(1);
     c->scan_tmp = k.take<int64_t>(1024);
     c->blk_tmp = k.take<int32_t>(1024);
@@ -216,6 +216,13 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->g.bcw = k.take<double>(c->cap);
     c->g.bcnt = k.take<int32_t>(N);
     c->g.order = k.take<int32_t>(N);
+    {   // 2D particle sets: unions and their pair records (every (member, neighbour) pair once)
+        const bool on = c->d == 2;
+        const size_t ns = on ? (size_t)(N + c->set_P - 1) / c->set_P : 1;
+        c->su_n = k.take<int32_t>(ns);
+        c->su_desc = k.take<int32_t>(on ? ns * c->su_cap : 1);
+        c->su_rec = k.take<double>(on ? ns * c->su_cap * kRecD2SG : 1);
+    }
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     {
@@ -280,6 +287,13 @@ bgk_status sync_check(bgk_ctx* c, cudaStream_t s) {
 
 cudaStream_t S(bgk_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// settle graph steps that a particle-management change skipped (graph.cu) before the state is used
+#define BGK_RECONCILE(c, s)                                         \
+    do {                                                            \
+        const bgk_status rc_ = bgk::graph_reconcile((c), (s));      \
+        if (rc_ != BGK_OK) return rc_;                              \
+    } while (0)
+
 }  // namespace
 
 // interior / boundary lists from host kinds and positions (boundary particles sorted by
@@ -323,6 +337,7 @@ bgk_status ensure_geometry(bgk_ctx* c, cudaStream_t s) {
         }
         launch_wls(c, s);
         launch_bnd_union(c, s);
+        if (c->d == 2) launch_set_union(c, s);   // after the WLS: the records carry its pair data
         c->geometry_valid = true;
         c->rows_built = false;
         if (c->rows_on) {                         // fixed cloud: detect the lattice rows once
@@ -389,6 +404,8 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
     }
     const int64_t reset[4] = {0, 0, 0, 0};
     cudaMemcpyAsync(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(c->gflag, reset, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    c->graph_ok = true;
     // padding columns stay zero forever (TMA boxes of the last column group read them): both
     // buffers are cleared over the whole capacity, so rows that management appends past the
     // initial N start with zero padding too (the kernels only ever write valid columns)
@@ -424,6 +441,7 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
 bgk_status bgk_build_neighbors(bgk_ctx* c, int64_t* offsets, int32_t* idx, int64_t cap, int64_t* needed,
                                bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     launch_build_neighbors(c, s);
     c->geometry_valid = false;
@@ -448,6 +466,7 @@ bgk_status bgk_build_neighbors(bgk_ctx* c, int64_t* offsets, int32_t* idx, int64
 
 bgk_status bgk_wls_coeffs(bgk_ctx* c, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     launch_wls(c, s);
     bgk_status st = check_launch(c);
@@ -458,6 +477,7 @@ bgk_status bgk_wls_coeffs(bgk_ctx* c, bgk_stream stream) {
 
 bgk_status bgk_get_wls(bgk_ctx* c, double* Sout, double* rot, double* frames, double* cw, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     const int d = c->d;
     bgk_status st = sync_check(c, s);        // in-flight geometry work finishes before nnz is read
@@ -490,6 +510,7 @@ bgk_status bgk_get_wls(bgk_ctx* c, double* Sout, double* rot, double* frames, do
 
 bgk_status bgk_run_phase(bgk_ctx* c, bgk_phase phase, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     double* fn = c->f[1 - c->fcur];
     switch (phase) {
@@ -532,6 +553,7 @@ bgk_status bgk_step(bgk_ctx* c, int n_steps, bgk_stream stream) {
     if (!c || n_steps < 0) return BGK_E_INVALID_ARG;
     if (c->ncol != c->ncol_g) return BGK_E_INVALID_ARG;   // sharded runs use the split phases
     for (int n = 0; n < n_steps; ++n) {
+        if (graph_step(c, S(stream))) continue;         // the whole step as one graph launch (graph.cu)
         bgk_status st;
         if ((st = bgk_step_transport(c, stream)) != BGK_OK) return st;
         if ((st = bgk_step_relax(c, stream)) != BGK_OK) return st;
@@ -542,6 +564,7 @@ bgk_status bgk_step(bgk_ctx* c, int n_steps, bgk_stream stream) {
 
 bgk_status bgk_buffer(bgk_ctx* c, bgk_buffer_id id, void** ptr, size_t* bytes) {
     if (!c || !ptr || !bytes) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, c->gstream);
     switch (id) {
         case BGK_BUF_MOMENT_SUMS: *ptr = c->sums; *bytes = sizeof(double) * c->N * kPM; return BGK_OK;
         case BGK_BUF_WALL_FLUX: *ptr = c->wallnum; *bytes = sizeof(double) * c->N; return BGK_OK;
@@ -552,12 +575,14 @@ bgk_status bgk_buffer(bgk_ctx* c, bgk_buffer_id id, void** ptr, size_t* bytes) {
 
 bgk_status bgk_moments_partial(bgk_ctx* c, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     launch_row_moments(c, c->f[c->fcur], S(stream));
     return check_launch(c);
 }
 
 bgk_status bgk_moments_finalize(bgk_ctx* c, double* rho, double* U, double* T, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     launch_moments_finalize(c, c->outbuf, s);
     bgk_status st = check_launch(c);
@@ -588,6 +613,7 @@ bgk_status bgk_moments(bgk_ctx* c, double* rho, double* U, double* T, bgk_stream
 
 bgk_status bgk_get_macro(bgk_ctx* c, double* macro, bgk_stream stream) {
     if (!c || !macro) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     bgk_status st = copy_out(c, macro, c->macro, sizeof(double) * c->N * (c->d + 2), s);
     if (st != BGK_OK) return st;
@@ -596,6 +622,7 @@ bgk_status bgk_get_macro(bgk_ctx* c, double* macro, bgk_stream stream) {
 
 bgk_status bgk_get_f(bgk_ctx* c, double* f, bgk_stream stream) {
     if (!c || !f) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     double* scratch = c->f[1 - c->fcur];
     launch_to_canonical(c, c->f[c->fcur], scratch, s);
@@ -607,6 +634,7 @@ bgk_status bgk_get_f(bgk_ctx* c, double* f, bgk_stream stream) {
 
 bgk_status bgk_set_f(bgk_ctx* c, const double* f, bgk_stream stream) {
     if (!c || !f) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     double* scratch = c->f[1 - c->fcur];
     bgk_status st = copy_out(c, scratch, f, sizeof(double) * c->N * c->nv * c->Kloc, s);
@@ -618,6 +646,7 @@ bgk_status bgk_set_f(bgk_ctx* c, const double* f, bgk_stream stream) {
 
 bgk_status bgk_get_positions(bgk_ctx* c, double* x, bgk_stream stream) {
     if (!c || !x) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     bgk_status st = copy_out(c, x, c->x, sizeof(double) * c->N * c->d, s);
     if (st != BGK_OK) return st;
@@ -626,6 +655,7 @@ bgk_status bgk_get_positions(bgk_ctx* c, double* x, bgk_stream stream) {
 
 bgk_status bgk_get_neighbors(bgk_ctx* c, int64_t* offsets, int32_t* idx, int64_t* nnz, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     bgk_status st = sync_check(c, s);
     if (st != BGK_OK) return st;
@@ -639,6 +669,7 @@ bgk_status bgk_get_neighbors(bgk_ctx* c, int64_t* offsets, int32_t* idx, int64_t
 
 bgk_status bgk_stable_dt(bgk_ctx* c, double* dt_out, bgk_stream stream) {
     if (!c || !dt_out) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     bgk_status st0 = ensure_geometry(c, s);
     if (st0 != BGK_OK) return st0;
@@ -669,6 +700,7 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
 
 bgk_status bgk_sync(bgk_ctx* c, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     return sync_check(c, S(stream));
 }
 
@@ -679,6 +711,7 @@ const char* bgk_last_error(bgk_ctx* c, int64_t* particle) {
 }
 
 bgk_status bgk_destroy(bgk_ctx* c) {
+    if (c) graph_release(c);
     if (c && c->cfg.staging) {
         cudaEventDestroy(c->ev_staged);
         cudaEventDestroy(c->ev_consumed);
@@ -689,6 +722,7 @@ bgk_status bgk_destroy(bgk_ctx* c) {
 
 bgk_status bgk_stage_f(bgk_ctx* c, const double* f, bgk_stream copy_stream) {
     if (!c || !f || !c->cfg.staging) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, c->gstream);
     cudaStream_t cs = S(copy_stream);
     cudaError_t e = cudaStreamWaitEvent(cs, c->ev_consumed, 0);   // the previous staged input is converted
     if (e == cudaSuccess)
@@ -703,6 +737,7 @@ bgk_status bgk_stage_f(bgk_ctx* c, const double* f, bgk_stream copy_stream) {
 
 bgk_status bgk_use_staged_f(bgk_ctx* c, bgk_stream stream) {
     if (!c || !c->cfg.staging || !c->stage_pending) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     if (c->stage_N != c->N || c->stage_gen != c->cloud_gen) {
         // particle management changed N or renumbered the rows after bgk_stage_f: the staged
         // rows no longer match the cloud (the copy itself completed within the old size)
@@ -724,6 +759,7 @@ bgk_status bgk_use_staged_f(bgk_ctx* c, bgk_stream stream) {
 
 bgk_status bgk_manage(bgk_ctx* c, int64_t* report, bgk_stream stream) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     if (!c->cfg.manage) return BGK_E_INVALID_ARG;   // no scratch carved
     cudaStream_t s = S(stream);
     launch_build_neighbors(c, s);
@@ -737,6 +773,7 @@ bgk_status bgk_manage(bgk_ctx* c, int64_t* report, bgk_stream stream) {
 
 bgk_status bgk_count(bgk_ctx* c, int64_t* N, int64_t* n_interior, int64_t* n_boundary, int64_t* capacity) {
     if (!c) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, c->gstream);
     if (N) *N = c->N;
     if (n_interior) *n_interior = c->N_int;
     if (n_boundary) *n_boundary = c->N_b;
@@ -746,8 +783,8 @@ bgk_status bgk_count(bgk_ctx* c, int64_t* N, int64_t* n_interior, int64_t* n_bou
 
 bgk_status bgk_transport_info(bgk_ctx* c, int64_t* info) {
     if (!c || !info) return BGK_E_INVALID_ARG;
-    info[0] = 1;                      // particles per transport warp
-    info[1] = c->R;
+    info[0] = c->d == 2 ? c->set_P : 1;       // particles per transport warp
+    info[1] = c->d == 2 ? c->set_QC : c->R;   // 3D: rows per lane; 2D: nodes per lane
     info[2] = c->rows_built ? c->n_rows : 0;
     info[3] = c->rows_built ? c->n_rest : c->N_int;
     return BGK_OK;
@@ -755,12 +792,14 @@ bgk_status bgk_transport_info(bgk_ctx* c, int64_t* info) {
 
 bgk_status bgk_manage_report(bgk_ctx* c, int64_t* report) {
     if (!c || !report) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, c->gstream);
     std::memcpy(report, c->mg_report, sizeof(c->mg_report));
     return BGK_OK;
 }
 
 bgk_status bgk_get_kind(bgk_ctx* c, int8_t* kind, bgk_stream stream) {
     if (!c || !kind) return BGK_E_INVALID_ARG;
+    BGK_RECONCILE(c, S(stream));
     cudaStream_t s = S(stream);
     bgk_status st = copy_out(c, kind, c->kind, (size_t)c->N, s);
     if (st != BGK_OK) return st;

@@ -16,6 +16,10 @@
 namespace bgk {
 
 constexpr int kPM = 5;          // moment partials per particle: s0, s_v (d), s_E  (2D: s0, s1, s2, sE, 0)
+// 2D set pair record (doubles): p_n (2), p_t (2), b_n, b_t with b_e = -p_e.W (first order); the
+// second-order WLS adds sigma = -s_n and a pad, with p_n, b_n pre-multiplied by sigma
+constexpr int kRecD2 = 6;
+constexpr int kRecD2SG = 8;
 constexpr int kMaxCellsPerAxis = 4096;
 
 struct Geo {                    // per-step geometry arrays (device)
@@ -70,8 +74,16 @@ struct bgk_ctx {
     int ncs;                           // stored column stride: ncol rounded up to a multiple of 16 in 3D (128-B rows)
     int64_t N, N_int, N_b, Kloc, Ks, RS;   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
     int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)
-    int ncg;                           // 32-column groups per chunk (transport)
-    int tail_cols;                     // 2D: columns past the last full group, done by k_transport_tail
+    int ncg;                           // 3D: 32-column groups per chunk (transport)
+    // 2D particle sets (k_transport2s): set_P consecutive interior particles of the
+    // cell order walk the union of their neighbour lists together; a warp owns one set and one chunk
+    // of 32*set_QC consecutive local nodes, each lane set_QC nodes (lane + 32 q)
+    int set_P, set_QC;
+    int64_t nset;                      // sets of the current interior list: ceil(N_int / set_P)
+    int su_cap;                        // union entries per set (set_P * max_nb)
+    int32_t* su_n;                     // [sets] union size
+    int32_t* su_desc;                  // [sets][su_cap] (j << 8) | member mask, ascending j
+    double* su_rec;                    // [sets][su_cap][kRecD2 | kRecD2SG] pair records in (j, member) order
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
     CUtensorMap tmap_rows[2];          //   the same with the lattice-row kernel's box {32, kRowsR, 1}
     int max_nb;
@@ -82,7 +94,7 @@ struct bgk_ctx {
     double dv, vmin;
     int PD;                     // doubles of pair data per CSR entry
     int wls_order;              // 1 or 2 (second order adds the signed tail to the pair record)
-    int R, nchunk, nslots, nwpp; // transport mapping
+    int R, nchunk, nslots, nwpp; // transport mapping (2D: nchunk = node chunks of 32*set_QC)
     int bnd_chunk, bnd_nch;     // boundary node chunking
     bool geometry_valid;
     int fcur;
@@ -129,6 +141,18 @@ struct bgk_ctx {
     int16_t* rows_perm;     // [Ncap / kRowsG][256] p0's neighbour entries in run order
     int32_t* order_rest;// [Ncap] the rest, in cell order
     int rows_nchunk;    // velocity chunks of kRowsR nodes along v_1
+    // whole-step CUDA graphs (graph.cu): one executable per buffer parity, rebuilt when the key changes
+    bool graph_ok;                 // graphs usable (BGK_GRAPH != 0, conditional nodes available)
+    int eager_steps;               // steps run eagerly since the last key change (capture after one)
+    cudaStream_t cap_stream, cap_stream2;   // private capture streams (step, conditional bodies)
+    cudaStream_t gstream;          // stream of the last graph launch (reconcile of stream-less calls)
+    uint64_t eager_key;            // key of the last eager step
+    int force_eager;               // steps that must run eagerly (a management change to apply)
+    cudaGraphExec_t gexec[2];
+    uint64_t gkey[2];
+    int64_t* gflag;                // [2] device: [0] a management change skipped the rest, [1] bodies run
+    int64_t gsteps;                // graph steps enqueued since the last reconcile (managed mode)
+    int gfcur0;                    // fcur before the first of them
     int64_t* scan_tmp;  // [1024]
     int32_t* blk_tmp;   // [1024] per-block partial counts of the multi-block scans
     bgk::Geo g;
@@ -216,6 +240,9 @@ void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream
 void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_check_domain(bgk_ctx* c, cudaStream_t s);
 int transport_rows_per_thread(int d, int n1);
+// 2D particle sets: (P, QC) of the instantiated set kernels, and the per-set union build (geometry)
+void set_mapping_2d(int wls_order, int* P, int* QC);
+void launch_set_union(bgk_ctx* c, cudaStream_t s);
 bool make_tensor_maps(bgk_ctx* c);
 // fixed-cloud lattice rows: host-side group detection on the cached geometry, and the kernel
 bgk_status build_rows(bgk_ctx* c, cudaStream_t s);
@@ -227,8 +254,19 @@ __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int
 }
 int launches_neighbors();
 int launches_wls();
-// particle management: one pass (synchronises the stream); *changed = N or indices changed
+// particle management: one pass (synchronises the stream); *changed = N or indices changed.
+// manage_decide enqueues detect + decide only (device report mg.rep, rep[7] = changed);
+// manage_apply reads the report back and applies a change.
 bgk_status manage_pass(bgk_ctx* c, cudaStream_t s, bool* changed);
+void manage_decide(bgk_ctx* c, cudaStream_t s);
+bgk_status manage_apply(bgk_ctx* c, cudaStream_t s, bool* changed);
+// whole-step CUDA graphs (graph.cu): graph_step enqueues one step as a graph launch (false: not
+// possible now -- run the step eagerly); graph_reconcile settles steps a management change skipped;
+// graph_release frees the graphs
+bool graph_step(bgk_ctx* c, cudaStream_t s);
+bgk_status graph_reconcile(bgk_ctx* c, cudaStream_t s);
+void graph_release(bgk_ctx* c);
+void launch_step_eager_body(bgk_ctx* c, cudaStream_t s);
 // kinds/positions on the host -> interior / boundary / order lists, counts, TMA maps
 bgk_status install_lists(bgk_ctx* c, const int8_t* hk, const double* hx, cudaStream_t s);
 

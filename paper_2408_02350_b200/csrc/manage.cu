@@ -427,8 +427,9 @@ __global__ void k_mg_small(const double* __restrict__ x, const int8_t* __restric
     }
 }
 
+// detect + decide (device only): the decisions and the 8-word report m.rep, rep[7] = cloud changed
 template <int D>
-bgk_status run_pass(bgk_ctx* c, cudaStream_t s, bool* changed) {
+void decide_pass(bgk_ctx* c, cudaStream_t s) {
     const int64_t N = c->N;
     const bgk_config& cf = c->cfg;
     const double rm = cf.r_merge > 0.0 ? cf.r_merge : 0.2 * cf.dx;
@@ -463,6 +464,12 @@ bgk_status run_pass(bgk_ctx* c, cudaStream_t s, bool* changed) {
     A.max_nb = c->max_nb;
     A.m = m;
     k_mg_decide<D><<<1, 32, 0, s>>>(A, c->Ncap);
+}
+
+// read the report back (one stream synchronisation) and, if the cloud changed, apply the decisions
+template <int D>
+bgk_status apply_pass(bgk_ctx* c, cudaStream_t s, bool* changed) {
+    Manage& m = c->mg;
     int64_t rep[8];
     cudaError_t e = cudaMemcpyAsync(rep, m.rep, sizeof(rep), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -499,10 +506,26 @@ bgk_status run_pass(bgk_ctx* c, cudaStream_t s, bool* changed) {
 
 }  // namespace
 
+void manage_decide(bgk_ctx* c, cudaStream_t s) {
+    if (!c->cfg.manage || c->N == 0) return;
+    if (c->d == 3) decide_pass<3>(c, s);
+    else decide_pass<2>(c, s);
+}
+
+bgk_status manage_apply(bgk_ctx* c, cudaStream_t s, bool* changed) {
+    *changed = false;
+    if (!c->cfg.manage || c->N == 0) return BGK_OK;
+    const bgk_status st = c->d == 3 ? apply_pass<3>(c, s, changed) : apply_pass<2>(c, s, changed);
+    if (st != BGK_OK) return st;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BGK_OK : BGK_E_CUDA;
+}
+
 bgk_status manage_pass(bgk_ctx* c, cudaStream_t s, bool* changed) {
     *changed = false;
     if (!c->cfg.manage || c->N == 0) return BGK_OK;
-    const bgk_status st = c->d == 3 ? run_pass<3>(c, s, changed) : run_pass<2>(c, s, changed);
+    manage_decide(c, s);
+    const bgk_status st = manage_apply(c, s, changed);
     if (st != BGK_OK) return st;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BGK_OK : BGK_E_CUDA;

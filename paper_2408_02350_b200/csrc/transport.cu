@@ -560,71 +560,381 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
     for (int k = 0; k < G; ++k) transport_epilogue<3, R, false>(A, p0 + k * S, w, k1s, colc, gc, valid, Qf[k], Sc, Sa);
 }
 
-// 2D tail columns (N_v = 32: the 33rd column): warp per (interior particle, chunk of R nodes along
-// v_1), lane r owning row k1s + r, looping over the neighbours (pair record and neighbour index
-// broadcast, one 16-B load of (g1, g2) per lane); the same arithmetic as k_transport (C/2 =
-// sum_e min(y_e, 0), Q and sum C for g1 and g2, the factor 2 in the epilogue).  Moment partials
-// go to slot nchunk*ncg + chunk of the particle.
-template <int R>
-__global__ void __launch_bounds__(128) k_transport_tail(const TArgs A, int tail0, int nchunk) {
-    // warp per (interior particle, chunk): lane r owns node row k1s + r of each tail column
-    static_assert(R <= 32, "one row per lane");
-    const int lane = threadIdx.x & 31;
-    const int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (t >= A.n_int * nchunk) return;
-    const int64_t pos = t / nchunk;
-    const int chunk = (int)(t - pos * nchunk);
-    const int p = A.order[pos];
-    const int k1s = chunk * R;
-    const bool row_ok = lane < R && k1s + lane < A.n1;
-    const int k1 = row_ok ? k1s + lane : k1s;
-    const int64_t off = A.nb_off[p];
-    const int m = (int)(A.nb_off[p + 1] - off);
-    const double W0 = A.W[(int64_t)p * 2], W1 = A.W[(int64_t)p * 2 + 1];
-    const int64_t rowstride = (int64_t)A.ncs * 2;
-    const double v1 = axis_node(A.vmax, A.dv, k1);
-    const double c1 = v1 - W0;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, sE = 0.0, amax = 0.0;
-    for (int col = tail0; col < A.ncol; ++col) {
-        const double v2 = axis_node(A.vmax, A.dv, A.c0 + col);
-        const double c2 = v2 - W1;
-        double Q0 = 0.0, Q1 = 0.0, Sc = 0.0;
-#pragma unroll 4
-        for (int e = 0; e < m; ++e) {
-            const int j = __ldg(A.nb_idx + off + e);
-            const double2 pa = __ldg(reinterpret_cast<const double2*>(A.P + (off + e) * 4));
-            const double2 pb = __ldg(reinterpret_cast<const double2*>(A.P + (off + e) * 4 + 2));
-            const double C = neg_part(fma(pa.y, c2, pa.x * c1)) + neg_part(fma(pb.y, c2, pb.x * c1));
-            const double2 g = __ldg(reinterpret_cast<const double2*>(A.f + ((int64_t)j * A.n1 + k1) * rowstride) + col);
-            Q0 = fma(C, g.x, Q0);
-            Q1 = fma(C, g.y, Q1);
-            Sc += C;
+// ============================================================================
+// 2D particle sets (k_transport2s).  A 2D node carries (g1, g2): a lane's load of
+// f_jk is 16 B against ~4 DP of work per value, so the one-particle warp of the 3D kernel reads
+// twice the bytes per flop and sat at the L2 -> SM limit in 2D (4.7 GB per C2 step).  Here a warp
+// owns a SET of P consecutive interior particles of the cell order and walks the union of their
+// neighbour lists (ascending j): each union entry's box -- a chunk of 32*QC consecutive local
+// nodes k1*ncol + col of f_j, contiguous in the unpadded 2D row, one bulk copy -- is loaded once
+// and applied to every member that has j as a neighbour, with that member's pair record (staged
+// with the box).  Lane l owns nodes t0 + l + 32 q (q < QC) of the chunk, so any column count maps
+// without tail columns.  The projections are y_e = p_e . v_k + b_e with b_e = -p_e . W_i folded
+// into the record at geometry time (2 DFMA each), C/2 = neg(y_n) + neg(y_t) (Z5-Z7),
+// and Q1, Q2, Sc accumulate per (member, node): 8 DP per (i, j, k) triple, the survey's 2D lean
+// count.  The second-order WLS (Z27: the n-term y_n - sign(abar)|y_n|) stores sigma = -s_n and
+// sigma p_n, sigma b_n, so C/2 = sigma neg(sigma y_n) + neg(y_t) (one DFMA in place of the DADD).
+// ============================================================================
+template <int P, typename T>
+__device__ __forceinline__ T pick(const T (&a)[P], int b) {
+    T r = a[0];
+#pragma unroll
+    for (int q = 1; q < P; ++q)
+        if (q == b) r = a[q];
+    return r;
+}
+
+// Union of one set's neighbour lists (warp per set): every (member b, entry e) is ranked in the
+// (j, b) order by binary searches in the other members' sorted lists, the first of each j run
+// writes the union descriptor (j << 8 | members holding j), and every element writes its pair record
+// at its rank -- so the records of union entry u are contiguous, in member order, and the transport
+// finds them by a running popcount.
+template <int P, bool SG>
+__global__ void __launch_bounds__(128) k_set_union2(const int32_t* __restrict__ order, int64_t n_int,
+                                                    const int64_t* __restrict__ nb_off,
+                                                    const int32_t* __restrict__ nb_idx, const double* __restrict__ Pr,
+                                                    const double* __restrict__ W, int su_cap,
+                                                    int32_t* __restrict__ su_n, int32_t* __restrict__ su_desc,
+                                                    double* __restrict__ su_rec) {
+    static_assert(P <= 8, "member mask is 8 bits");
+    constexpr int RD = SG ? kRecD2SG : kRecD2;
+    constexpr int PD = SG ? 6 : 4;                  // CSR pair record: p_n, p_t [, s_n, 0]
+    extern __shared__ unsigned long long skeys[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t s = (int64_t)blockIdx.x * 4 + wib;
+    const int64_t nset = (n_int + P - 1) / P;
+    if (s >= nset) return;
+    unsigned long long* keys = skeys + (size_t)wib * su_cap;
+    int pb[P], mb[P];
+    int64_t ob[P];
+    int total = 0;
+#pragma unroll
+    for (int b = 0; b < P; ++b) {
+        const int64_t pos = s * P + b;
+        const bool in = pos < n_int;
+        pb[b] = in ? order[pos] : 0;
+        ob[b] = in ? nb_off[pb[b]] : 0;
+        mb[b] = in ? (int)(nb_off[pb[b] + 1] - ob[b]) : 0;
+        total += mb[b];
+    }
+    for (int t = lane; t < total; t += 32) {
+        int b = 0, e = t;
+#pragma unroll
+        for (int q = 0; q < P - 1; ++q)
+            if (b == q && e >= mb[q]) {
+                e -= mb[q];
+                b = q + 1;
+            }
+        const int32_t j = nb_idx[pick(ob, b) + e];
+        int rank = e;
+        bool first = true;
+        unsigned mask = 1u << b;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            if (q == b || mb[q] == 0) continue;
+            const int32_t* Lq = nb_idx + ob[q];
+            int lo = 0, hi = mb[q];
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (Lq[mid] < j) lo = mid + 1;
+                else hi = mid;
+            }
+            const bool found = lo < mb[q] && Lq[lo] == j;
+            rank += (q < b) ? lo + (int)found : lo;
+            if (found) {
+                mask |= 1u << q;
+                if (q < b) first = false;
+            }
         }
-        if (row_ok) {
-            const double2 fv = __ldg(reinterpret_cast<const double2*>(A.f + ((int64_t)p * A.n1 + k1) * rowstride) + col);
-            const double o0 = fv.x - 2.0 * A.dt * (Q0 - fv.x * Sc);
-            const double o1 = fv.y - 2.0 * A.dt * (Q1 - fv.y * Sc);
-            reinterpret_cast<double2*>(A.ft + ((int64_t)p * A.n1 + k1) * rowstride)[col] = make_double2(o0, o1);
-            s0 += o0;
-            s1 += v1 * o0;
-            s2 += v2 * o0;
-            sE += (v1 * v1 + v2 * v2) * o0 + o1;
-            amax = fmax(amax, -2.0 * Sc);
+        keys[rank] = ((unsigned long long)(uint32_t)j << 32) | ((unsigned long long)first << 31) |
+                     ((unsigned long long)mask << 16) | ((unsigned long long)b << 12) | (unsigned long long)e;
+    }
+    __syncwarp();
+    int ubase = 0;
+    for (int t0 = 0; t0 < total; t0 += 32) {
+        const int t = t0 + lane;
+        const bool v = t < total;
+        const unsigned long long key = v ? keys[t] : 0ull;
+        const bool first = v && ((key >> 31) & 1ull);
+        const unsigned bal = __ballot_sync(0xffffffffu, first);
+        if (first)
+            su_desc[s * su_cap + ubase + __popc(bal & ((1u << lane) - 1u))] =
+                (int32_t)(((uint32_t)(key >> 32) << 8) | (uint32_t)((key >> 16) & 0xffull));
+        if (v) {
+            const int b = (int)((key >> 12) & 15ull), e = (int)(key & 4095ull);
+            const int p = pick(pb, b);
+            const double* pe = Pr + (pick(ob, b) + e) * PD;
+            const double w0 = W[(int64_t)p * 2], w1 = W[(int64_t)p * 2 + 1];
+            const double sg = SG ? -pe[4] : 1.0;        // sigma = -s_n = sign(abar) (second order)
+            const double pn1 = sg * pe[0], pn2 = sg * pe[1], pt1 = pe[2], pt2 = pe[3];
+            double* r = su_rec + (s * su_cap + t) * RD;
+            r[0] = pn1;
+            r[1] = pn2;
+            r[2] = pt1;
+            r[3] = pt2;
+            r[4] = -(pn1 * w0 + pn2 * w1);
+            r[5] = -(pt1 * w0 + pt2 * w1);
+            if constexpr (SG) {
+                r[6] = sg;
+                r[7] = 0.0;
+            }
+        }
+        ubase += __popc(bal);
+    }
+    if (lane == 0) su_n[s] = ubase;
+}
+
+struct SArgs {
+    const double* __restrict__ f;
+    double* __restrict__ ft;
+    const int32_t* __restrict__ order;
+    const int32_t* __restrict__ su_n;
+    const int32_t* __restrict__ su_desc;
+    const double* __restrict__ su_rec;
+    double* __restrict__ partials;
+    unsigned long long* stab;
+    int64_t n_int, nset, Kloc;
+    int su_cap, ncol, c0, nwpp;
+    double vmax, dv, dt;
+};
+
+template <int P, int QC, int B, bool SG>
+struct SetStage {
+    static constexpr int RD = SG ? kRecD2SG : kRecD2;
+    static constexpr uint32_t BOX = 32 * QC * 16;                     // 32*QC nodes of (g1, g2)
+    static constexpr uint32_t F_BYTES = B * BOX;                      // B union entries per stage
+    static constexpr uint32_t R_BYTES = B * P * RD * sizeof(double);  // their member records (<= P each)
+    static constexpr uint32_t BYTES = (F_BYTES + R_BYTES + 127) / 128 * 128;
+};
+
+// Stage = a batch of B consecutive union entries: B boxes and ONE bulk copy of the batch's records
+// (contiguous in su_rec: records are stored in (j, member) order), all on one mbarrier -- the
+// barrier wait, the expect_tx and the record copy are paid once per B entries.
+template <int P, int QC, int B, int NST, int WPB, bool SG, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) k_transport2s(const SArgs A) {
+    using St = SetStage<P, QC, B, SG>;
+    constexpr int RD = St::RD;
+    static_assert(32 % B == 0, "batches must not straddle descriptor batches");
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* ring = smem_raw + (size_t)wib * NST * St::BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)WPB * NST * St::BYTES) + wib * NST;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t set = (int64_t)blockIdx.x * WPB + wib;
+    if (set >= A.nset) return;                                   // warp-uniform
+    const int chunk = blockIdx.y;
+    const int64_t t0 = (int64_t)chunk * 32 * QC;
+    const uint32_t fbytes = (uint32_t)min((int64_t)(32 * QC), A.Kloc - t0) * 16u;
+    const int U = A.su_n[set];
+    const int nbat = (U + B - 1) / B;
+    const int32_t* desc = A.su_desc + set * A.su_cap;
+    const double* rec = A.su_rec + set * A.su_cap * RD;
+    const double2* fsrc = reinterpret_cast<const double2*>(A.f);
+
+    // union descriptors, 32 per register batch: (cA, cB) for consumption, (iA, iB) for refills
+    int cA = lane < U ? desc[lane] : 0;
+    int cB = 32 + lane < U ? desc[32 + lane] : 0;
+    int iA = cA, iB = cB;
+    int roff = 0;                                   // records issued so far (warp-uniform)
+    // batch k (entries kB .. kB+B) into stage k % NST; called by every lane (the copies by one)
+    auto issue = [&](int k, int da) {
+        const int st = k % NST;
+        unsigned char* sp = ring + st * St::BYTES;
+        int dd[B], cnt = 0;
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            dd[q] = __shfl_sync(0xffffffffu, da, (k * B + q) & 31);
+            if (k * B + q >= U) dd[q] = 0;
+            cnt += __popc(dd[q] & 0xff);
+        }
+        const uint32_t rbytes = (uint32_t)cnt * RD * sizeof(double);
+        if (elect_one()) {
+            uint32_t fb = 0;
+#pragma unroll
+            for (int q = 0; q < B; ++q) fb += k * B + q < U ? fbytes : 0u;
+            mbar_expect_tx(bars + st, fb + rbytes);
+#pragma unroll
+            for (int q = 0; q < B; ++q)
+                if (k * B + q < U)
+                    bulk_load(sp + q * St::BOX, fsrc + (int64_t)((uint32_t)dd[q] >> 8) * A.Kloc + t0, fbytes,
+                              bars + st);
+            bulk_load(sp + St::F_BYTES, rec + (int64_t)roff * RD, rbytes, bars + st);
+        }
+        roff += cnt;
+    };
+#pragma unroll
+    for (int k = 0; k < NST; ++k) {
+        if (k >= nbat) break;
+        issue(k, iA);           // NST * B <= 32: the first stages come from the first descriptor batch
+    }
+    // velocities of the lane's nodes (clamped index past the end: those nodes are never stored)
+    double v1[QC], v2[QC];
+#pragma unroll
+    for (int qq = 0; qq < QC; ++qq) {
+        const int64_t t = min(t0 + lane + 32 * qq, A.Kloc - 1);
+        const int k1 = (int)(t / A.ncol), col = (int)(t - (int64_t)k1 * A.ncol);
+        v1[qq] = axis_node(A.vmax, A.dv, k1);
+        v2[qq] = axis_node(A.vmax, A.dv, A.c0 + col);
+    }
+    double Q1[P][QC], Q2[P][QC], Sc[P][QC], Sa[SG ? P : 1][SG ? QC : 1];
+#pragma unroll
+    for (int b = 0; b < P; ++b)
+#pragma unroll
+        for (int qq = 0; qq < QC; ++qq) {
+            Q1[b][qq] = Q2[b][qq] = Sc[b][qq] = 0.0;
+            if constexpr (SG) Sa[b][qq] = 0.0;
+        }
+    for (int k = 0; k < nbat; ++k) {
+        const int st = k % NST;
+        mbar_wait(bars + st, (uint32_t)(k / NST) & 1u);
+        const unsigned char* sp = ring + st * St::BYTES;
+        const double* rp = reinterpret_cast<const double*>(sp + St::F_BYTES);
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            const int e = k * B + q;
+            if (e >= U) break;                                  // warp-uniform (last batch)
+            const int d = __shfl_sync(0xffffffffu, cA, e & 31);
+            const double2* fj2 = reinterpret_cast<const double2*>(sp + q * St::BOX) + lane;
+            double2 fj[QC];
+#pragma unroll
+            for (int qq = 0; qq < QC; ++qq) fj[qq] = fj2[32 * qq];
+            const unsigned mask = (unsigned)d & 0xffu;
+#pragma unroll
+            for (int b = 0; b < P; ++b) {
+                if (!(mask & (1u << b))) continue;              // warp-uniform
+                const double* pr = rp;                          // broadcast LDS
+                rp += RD;
+                const double pn1 = pr[0], pn2 = pr[1], pt1 = pr[2], pt2 = pr[3], bn = pr[4], bt = pr[5];
+                const double sg = SG ? pr[6] : 1.0;
+#pragma unroll
+                for (int qq = 0; qq < QC; ++qq) {
+                    const double yn = fma(pn1, v1[qq], fma(pn2, v2[qq], bn));
+                    const double yt = fma(pt1, v1[qq], fma(pt2, v2[qq], bt));
+                    double C;                                   // C/2 (the epilogue doubles)
+                    if constexpr (SG) C = fma(sg, neg_part(yn), neg_part(yt));
+                    else C = neg_part(yn) + neg_part(yt);
+                    Q1[b][qq] = fma(C, fj[qq].x, Q1[b][qq]);
+                    Q2[b][qq] = fma(C, fj[qq].y, Q2[b][qq]);
+                    Sc[b][qq] += C;
+                    if constexpr (SG) Sa[b][qq] += fabs(C);
+                }
+            }
+        }
+        if (((k + 1) * B & 31) == 0) {                          // consumed a whole descriptor batch
+            cA = cB;
+            cB = (k + 1) * B + 32 + lane < U ? desc[(k + 1) * B + 32 + lane] : 0;
+        }
+        // refill this stage with batch k + NST
+        const int kn = k + NST;
+        if ((kn * B & 31) == 0 && kn * B >= 32) {               // its descriptors start a new batch
+            iA = iB;
+            iB = kn * B + 32 + lane < U ? desc[kn * B + 32 + lane] : 0;
+        }
+        __syncwarp();                                           // every lane has read the stage
+        if (kn < nbat) issue(kn, iA);
+    }
+    // epilogue per member: ftilde = f - 2 dt (Q - f Sc) for (g1, g2), moment partials of the chunk
+    const double dtq = 2.0 * A.dt;
+    double2* fdst = reinterpret_cast<double2*>(A.ft);
+    double amax = 0.0;
+#pragma unroll
+    for (int b = 0; b < P; ++b) {
+        const int64_t pos = set * P + b;
+        if (pos >= A.n_int) break;
+        const int p = A.order[pos];
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, sE = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < QC; ++qq) {
+            const int64_t t = t0 + lane + 32 * qq;
+            if (t < A.Kloc) {
+                const double2 fi = __ldg(fsrc + (int64_t)p * A.Kloc + t);
+                const double o0 = fi.x - dtq * (Q1[b][qq] - fi.x * Sc[b][qq]);
+                const double o1 = fi.y - dtq * (Q2[b][qq] - fi.y * Sc[b][qq]);
+                fdst[(int64_t)p * A.Kloc + t] = make_double2(o0, o1);
+                s0 += o0;
+                s1 += v1[qq] * o0;
+                s2 += v2[qq] * o0;
+                sE += (v1[qq] * v1[qq] + v2[qq] * v2[qq]) * o0 + o1;
+                amax = fmax(amax, SG ? 2.0 * Sa[b][qq] : -2.0 * Sc[b][qq]);
+            }
+        }
+        s0 = warp_sum(s0);
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        sE = warp_sum(sE);
+        if (lane == 0) {
+            double* pp = A.partials + ((int64_t)p * A.nwpp + chunk) * kPM;
+            pp[0] = s0;
+            pp[1] = s1;
+            pp[2] = s2;
+            pp[3] = sE;
+            pp[4] = 0.0;
         }
     }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    sE = warp_sum(sE);
-    amax = warp_max(amax);
-    if (lane == 0) {
-        double* pp = A.partials + ((int64_t)p * A.nwpp + (int64_t)nchunk * A.ncg + chunk) * kPM;
-        pp[0] = s0;
-        pp[1] = s1;
-        pp[2] = s2;
-        pp[3] = sE;
-        pp[4] = 0.0;
-        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+    amax = warp_max(amax);                                      // one stability atomic per warp
+    if (lane == 0) atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+}
+
+template <int P, int QC, int B, bool SG, int MINB = 1, int NSTMAX = 8>
+void launch_set(const SArgs& a, int nchunk, cudaStream_t s) {
+    constexpr int WPB = 4;
+    using St = SetStage<P, QC, B, SG>;
+    constexpr int WPSM = MINB > 3 ? MINB * WPB : 12;
+    constexpr int NST00 = (200 * 1024) / (WPSM * (int)St::BYTES);   // ring for the resident warps per SM
+    constexpr int NST0 = NST00 > NSTMAX ? NSTMAX : NST00;
+    constexpr int NST1 = NST0 > 8 ? 8 : (NST0 < 2 ? 2 : NST0);
+    constexpr int NST = NST1 * B > 32 ? 32 / B : NST1;         // the prologue reads one descriptor batch
+    constexpr size_t smem = (size_t)WPB * NST * St::BYTES + WPB * NST * 8;
+    static bool configured[kMaxDevices] = {};
+    if (first_use_on_device(configured))
+        cudaFuncSetAttribute(k_transport2s<P, QC, B, NST, WPB, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    const unsigned gx = (unsigned)((a.nset + WPB - 1) / WPB);
+    k_transport2s<P, QC, B, NST, WPB, SG, MINB><<<dim3(gx, (unsigned)nchunk), WPB * 32, smem, s>>>(a);
+}
+
+void launch_transport2s(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
+    SArgs a;
+    a.f = fin;
+    a.ft = fout;
+    a.order = c->g.order;
+    a.su_n = c->su_n;
+    a.su_desc = c->su_desc;
+    a.su_rec = c->su_rec;
+    a.partials = c->partials;
+    a.stab = c->stab;
+    a.n_int = c->N_int;
+    a.nset = (c->N_int + c->set_P - 1) / c->set_P;
+    a.Kloc = c->Kloc;
+    a.su_cap = c->su_cap;
+    a.ncol = c->ncol;
+    a.c0 = c->c0;
+    a.nwpp = c->nwpp;
+    a.vmax = c->cfg.vmax;
+    a.dv = c->dv;
+    a.dt = c->cfg.dt;
+    const int key = c->set_P * 100 + c->set_QC;
+    if (c->wls_order == 2) return launch_set<4, 2, 4, true>(a, c->nchunk, s);
+    static const int var = [] {
+        const char* e = getenv("BGK_SET_VAR");          // tuning experiments (occupancy / ring depth)
+        return e ? atoi(e) : 0;
+    }();
+    if (var == 1) return launch_set<4, 4, 4, false, 3, 3>(a, c->nchunk, s);
+    if (var == 2) return launch_set<4, 2, 4, false, 4, 2>(a, c->nchunk, s);
+    if (var == 3) return launch_set<4, 4, 2, false, 3, 4>(a, c->nchunk, s);
+    if (var == 4) return launch_set<2, 8, 4, false, 3, 3>(a, c->nchunk, s);
+    if (var == 5) return launch_set<4, 2, 2, false, 4, 4>(a, c->nchunk, s);
+    switch (key) {
+        case 402: launch_set<4, 2, 4, false>(a, c->nchunk, s); break;
+        case 404: launch_set<4, 4, 4, false>(a, c->nchunk, s); break;
+        case 803: launch_set<8, 3, 4, false>(a, c->nchunk, s); break;
+        default: launch_set<8, 2, 4, false>(a, c->nchunk, s); break;
     }
 }
 
@@ -660,30 +970,23 @@ void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) 
     launch_one<D, R, kDefaultWarps>(tm, a, s);
 }
 
-template <int D>
-void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    if constexpr (D == 3) {
-        switch (R) {
-            case 25: launch_wpb<D, 25>(wpb, tm, a, s); return;
-            case 21: launch_wpb<D, 21>(wpb, tm, a, s); return;
-            case 15: launch_wpb<D, 15>(wpb, tm, a, s); return;
-            default: break;
-        }
-    }
+void dispatch3(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
     switch (R) {
-        case 17: launch_wpb<D, 17>(wpb, tm, a, s); break;
-        case 13: launch_wpb<D, 13>(wpb, tm, a, s); break;
-        case 11: launch_wpb<D, 11>(wpb, tm, a, s); break;
-        case 9: launch_wpb<D, 9>(wpb, tm, a, s); break;
-        case 7: launch_wpb<D, 7>(wpb, tm, a, s); break;
-        case 5: launch_wpb<D, 5>(wpb, tm, a, s); break;
-        case 3: launch_wpb<D, 3>(wpb, tm, a, s); break;
-        default: launch_wpb<D, 1>(wpb, tm, a, s); break;
+        case 25: launch_wpb<3, 25>(wpb, tm, a, s); return;
+        case 21: launch_wpb<3, 21>(wpb, tm, a, s); return;
+        case 17: launch_wpb<3, 17>(wpb, tm, a, s); return;
+        case 15: launch_wpb<3, 15>(wpb, tm, a, s); return;
+        case 13: launch_wpb<3, 13>(wpb, tm, a, s); return;
+        case 11: launch_wpb<3, 11>(wpb, tm, a, s); return;
+        case 9: launch_wpb<3, 9>(wpb, tm, a, s); return;
+        case 7: launch_wpb<3, 7>(wpb, tm, a, s); return;
+        case 5: launch_wpb<3, 5>(wpb, tm, a, s); return;
+        case 3: launch_wpb<3, 3>(wpb, tm, a, s); return;
+        default: launch_wpb<3, 1>(wpb, tm, a, s); return;
     }
 }
 
 constexpr int kRChoices3[] = {25, 21, 17, 15, 13, 11, 9, 7, 5, 3, 1};
-constexpr int kRChoices2[] = {17, 13, 11, 9, 7, 5, 3, 1};
 
 // the R of `choices` with the lowest modelled cost ceil(n1/R) (R + kRowsOverhead): padded rows
 // plus the per-neighbour fixed cost (barrier, pair record, setup, refill ~ 5 rows of issue)
@@ -708,13 +1011,46 @@ bool listed(const int (&choices)[K], int R) {
 
 }  // namespace
 
-// rows per lane: BGK_TRANSPORT_R if instantiated for the mapping, else the instantiated R with
-// the fewest padded rows (2D keeps three accumulators per row, so it stops at 17)
+// (P, QC) of the 2D particle-set kernel: P = 8 particles per warp, QC = 2 nodes per lane (the union of
+// 8 cell-consecutive lists is 0.30 of their sum on C2/C3 and 48 accumulators fit the registers);
+// BGK_SET_P / BGK_SET_QC select another instantiated pair (4/2, 4/4, 8/3); second order: 4/2
+void set_mapping_2d(int wls_order, int* P, int* QC) {
+    const char* ep = getenv("BGK_SET_P");      // read per context (tests select instantiations)
+    const char* eq = getenv("BGK_SET_QC");
+    int key = (ep ? atoi(ep) : 8) * 100 + (eq ? atoi(eq) : 2);
+    if (wls_order == 2) key = 402;
+    if (key != 402 && key != 404 && key != 803 && key != 802 && key != 208) key = 802;
+    *P = key / 100;
+    *QC = key % 100;
+}
+
+void launch_set_union(bgk_ctx* c, cudaStream_t s) {
+    if (c->N_int == 0) return;
+    const int64_t nset = (c->N_int + c->set_P - 1) / c->set_P;
+    const unsigned g = (unsigned)((nset + 3) / 4);
+    const size_t smem = (size_t)4 * c->su_cap * sizeof(unsigned long long);
+    static bool configured[kMaxDevices] = {};
+    if (first_use_on_device(configured)) {
+        cudaFuncSetAttribute(k_set_union2<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_set_union2<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_set_union2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_set_union2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    }
+#define BGK_SU_ARGS c->g.order, c->N_int, c->g.nb_off, c->g.nb_idx, c->g.P, c->W, c->su_cap, c->su_n, c->su_desc, c->su_rec
+    if (c->wls_order == 2) k_set_union2<4, true><<<g, 128, smem, s>>>(BGK_SU_ARGS);
+    else if (c->set_P == 4) k_set_union2<4, false><<<g, 128, smem, s>>>(BGK_SU_ARGS);
+    else if (c->set_P == 2) k_set_union2<2, false><<<g, 128, smem, s>>>(BGK_SU_ARGS);
+    else k_set_union2<8, false><<<g, 128, smem, s>>>(BGK_SU_ARGS);
+#undef BGK_SU_ARGS
+}
+
+// rows per lane (3D): BGK_TRANSPORT_R if instantiated, else the instantiated R with the fewest
+// padded rows; 2D uses the particle-set kernel (set_mapping_2d) and ignores R
 int transport_rows_per_thread(int d, int n1) {
+    if (d != 3) return 1;
     const char* e = getenv("BGK_TRANSPORT_R");
     const int want = e ? atoi(e) : 0;
-    if (d == 3) return listed(kRChoices3, want) ? want : fewest_padded(kRChoices3, n1);
-    return listed(kRChoices2, want) ? want : fewest_padded(kRChoices2, n1);
+    return listed(kRChoices3, want) ? want : fewest_padded(kRChoices3, n1);
 }
 
 // TMA descriptors: f[b] viewed as a 3D fp64 tensor {ncs*nv (fastest), n1, N}; box {32*nv, R, 1}.
@@ -751,6 +1087,10 @@ bool make_tensor_maps(bgk_ctx* c) {
 
 void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
     if (c->N_int == 0) return;
+    if (c->d == 2) {                                 // particle sets (k_transport2s)
+        launch_transport2s(c, fin, fout, s);
+        return;
+    }
     TArgs a;
     a.f = fin;
     a.ft = fout;
@@ -785,21 +1125,8 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
         return e ? atoi(e) : 0;
     }();
     // 3D, R = 25: blocks of 2 warps (70.2 vs 70.9 ms on C5 with 128-B rows; profiles/r01_tuning.md)
-    const int wpb = wpb_env ? wpb_env : (c->d == 3 && c->R == 25 ? 2 : kDefaultWarps);
-    if (c->d == 3) dispatch<3>(c->R, wpb, tm, a, s);
-    else {
-        if (c->ncg > 0) dispatch<2>(c->R, wpb, tm, a, s);
-        if (c->tail_cols) {
-            const int64_t nt = c->N_int * c->nchunk;             // warps
-            const unsigned gx = (unsigned)((nt + 3) / 4);
-            switch (c->R) {
-                case 17: k_transport_tail<17><<<gx, 128, 0, s>>>(a, c->ncg * 32, c->nchunk); break;
-                case 13: k_transport_tail<13><<<gx, 128, 0, s>>>(a, c->ncg * 32, c->nchunk); break;
-                case 11: k_transport_tail<11><<<gx, 128, 0, s>>>(a, c->ncg * 32, c->nchunk); break;
-                default: k_transport_tail<9><<<gx, 128, 0, s>>>(a, c->ncg * 32, c->nchunk); break;
-            }
-        }
-    }
+    const int wpb = wpb_env ? wpb_env : (c->R == 25 ? 2 : kDefaultWarps);
+    dispatch3(c->R, wpb, tm, a, s);
 }
 
 
