@@ -76,10 +76,12 @@ class CavityConfig:
     max_particles: int = 0
     defects: int = 0          # management workloads: `defects` close pairs + `defects` holes (lattice())
     staging: int = 0          # 1: input staging buffer for overlapped host -> device copies (e2e)
+    rho_init: float = 0.0     # > 0: initial density given directly (the paper's rho0 = 1 case),
+                              # overriding the Kn table; Kn is then k_B/(sqrt(2) pi R d^2 rho L)
 
     @property
     def rho0(self) -> float:
-        return RHO0_BY_KN[self.Kn]
+        return self.rho_init if self.rho_init > 0 else RHO0_BY_KN[self.Kn]
 
     @property
     def dx(self) -> float:

@@ -156,7 +156,14 @@ bgk_status bgk_get_wls(bgk_ctx* ctx, double* S, double* rot, double* frames, dou
 /* n_steps time steps n -> n+1 (S:414 order): [ALE: neighbours + WLS on x^n],
  * transport, moment recovery, relaxation, [ALE: move], diffuse reflection.  Single rank
  * only (col range = all columns); multi-rank runs use the split-phase calls below.
- * Asynchronous; errors are latched (see conventions). */
+ * Asynchronous; errors are latched (see conventions).  From the second step with unchanged
+ * counts each step is replayed as one CUDA graph (BGK_GRAPH=0 disables; not while the caller's
+ * stream is being captured).  With particle management the graph decides on the device: a pass
+ * that changes the cloud skips the rest of that step and of every graph step queued after it,
+ * and the next call that reads or changes the state (any call taking the context except
+ * bgk_step, bgk_destroy, bgk_last_error, bgk_launches_per_step, bgk_transport_info,
+ * bgk_graph_info) synchronises and re-runs the skipped steps, the first one eagerly, so results
+ * are those of the eager path. */
 bgk_status bgk_step(bgk_ctx* ctx, int n_steps, bgk_stream stream);
 
 /* Split phases of one step, for velocity-sharded runs (one rank per GPU):
@@ -287,6 +294,11 @@ bgk_status bgk_count(bgk_ctx* ctx, int64_t* N, int64_t* n_interior, int64_t* n_b
  * lane R of the general kernel, info[2] fixed-cloud lattice-row groups (8 particles each, 0 if
  * the lattice-row kernel is not used), info[3] interior particles left to the general kernel. */
 bgk_status bgk_transport_info(bgk_ctx* ctx, int64_t* info);
+
+/* Whole-step graph use (diagnostics, host int64[4]): info[0] 1 if graphs are enabled and usable,
+ * info[1] steps launched as graphs, info[2] graph captures, info[3] steps re-run after a
+ * management change skipped them. */
+bgk_status bgk_graph_info(bgk_ctx* ctx, int64_t* info);
 
 /* Kinds of the current particles (host or device int8[N]); synchronises. */
 bgk_status bgk_get_kind(bgk_ctx* ctx, int8_t* kind, bgk_stream stream);

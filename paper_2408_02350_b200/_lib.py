@@ -64,6 +64,7 @@ SIGNATURES = {
     "bgk_manage_report": [_P, _P],
     "bgk_get_kind": [_P, _P, _P],
     "bgk_transport_info": [_P, _P],
+    "bgk_graph_info": [_P, _P],
     "bgk_stage_f": [_P, _P, _P],
     "bgk_use_staged_f": [_P, _P],
 }

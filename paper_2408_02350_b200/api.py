@@ -129,6 +129,12 @@ class Bgk:
         self._check(self.L.bgk_transport_info(self.ctx, _ptr(v)))
         return tuple(int(q) for q in v)
 
+    def graph_info(self):
+        """(graphs usable, steps launched as graphs, captures, steps re-run after a skip)."""
+        v = np.zeros(4, dtype=np.int64)
+        self._check(self.L.bgk_graph_info(self.ctx, _ptr(v)))
+        return tuple(int(q) for q in v)
+
     def kinds(self):
         k = np.zeros(self.N, dtype=np.int8)
         self._check(self.L.bgk_get_kind(self.ctx, _ptr(k), self.stream))

@@ -92,8 +92,7 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     // 3D row stride padded to a multiple of 16 doubles (128 B): every 256-B box row of a column group
     // then starts on a cache line and covers exactly 8 L2 sectors (C5 transport: 75.7 ms at 16-B
     // rows, 73.4 at 32 B, 72.8 at 64 B, 71.4 at 128 B; profiles/r01_tuning.md); BGK_NCS_ALIGN overrides.
-    // 2D rows stay unpadded: the particle-set kernel copies a chunk of consecutive local nodes
-    // (k1 * ncol + col) of a neighbour's row with one bulk copy, which needs ncs == ncol.
+    // 2D rows stay unpadded (128-B padding measured no gain on C2/C3, profiles/r01_tuning.md).
     {
         static const int al = [] {
             const char* e = getenv("BGK_NCS_ALIGN");
@@ -122,18 +121,17 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
     c->wls_order = cfg->wls_order == 2 ? 2 : 1;
     c->PD = (c->d == 2 ? 4 : 10) + (c->wls_order == 2 ? 2 : 0);
     c->R = transport_rows_per_thread(c->d, c->n1);
-    if (c->d == 3) {
-        c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
-        c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
-        c->nwpp = c->nchunk * c->ncg;
-    } else {
-        // 2D: a warp = (set of set_P particles, chunk of 32*set_QC consecutive local nodes)
-        set_mapping_2d(c->wls_order, &c->set_P, &c->set_QC);
-        c->nchunk = (int)((c->Kloc + 32 * c->set_QC - 1) / (32 * c->set_QC));
-        c->ncg = 1;
-        c->nwpp = c->nchunk;
-        c->su_cap = c->set_P * c->max_nb;
-    }
+    c->nchunk = (c->n1 + c->R - 1) / c->R;   // the last chunk may be ragged
+    c->ncg = (c->ncol + 31) / 32;           // a warp = (chunk, 32-column group): one TMA box per neighbour
+    // 2D, 33 columns (N_v = 32): a 32-lane group for ONE column would idle 31 lanes -- the box of
+    // the single group carries column 32 as well and lanes 0..R-1 update its R nodes of the chunk
+    // (k_transport XC = 1); instantiated for R = 17, 13, 11, 9, first order
+    c->xc = (c->d == 2 && c->ncol == 33 && (c->R == 17 || c->R == 13 || c->R == 11 || c->R == 9) &&
+             c->wls_order == 1)
+                ? 1
+                : 0;
+    if (c->xc) c->ncg = 1;
+    c->nwpp = c->nchunk * c->ncg;
     c->nslots = c->nwpp * 32;
     // fixed-cloud lattice rows (SURVEY §8(d) "the one lever"): partial slots sized for both mappings
     {
@@ -197,7 +195,7 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->wall_den = k.take<double>(2 * d);
     c->outbuf = k.take<double>(N * (d + 2));
     c->err = k.take<int64_t>(4);
-    c->gflag = k.take<int64_t>(2);
+    c->gflag = k.take<int64_t>(4);
     c->stab = k.take<unsigned long long>(1);
     c->scan_tmp = k.take<int64_t>(1024);
     c->blk_tmp = k.take<int32_t>(1024);
@@ -216,13 +214,6 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->g.bcw = k.take<double>(c->cap);
     c->g.bcnt = k.take<int32_t>(N);
     c->g.order = k.take<int32_t>(N);
-    {   // 2D particle sets: unions and their pair records (every (member, neighbour) pair once)
-        const bool on = c->d == 2;
-        const size_t ns = on ? (size_t)(N + c->set_P - 1) / c->set_P : 1;
-        c->su_n = k.take<int32_t>(ns);
-        c->su_desc = k.take<int32_t>(on ? ns * c->su_cap : 1);
-        c->su_rec = k.take<double>(on ? ns * c->su_cap * kRecD2SG : 1);
-    }
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     {
@@ -337,7 +328,6 @@ bgk_status ensure_geometry(bgk_ctx* c, cudaStream_t s) {
         }
         launch_wls(c, s);
         launch_bnd_union(c, s);
-        if (c->d == 2) launch_set_union(c, s);   // after the WLS: the records carry its pair data
         c->geometry_valid = true;
         c->rows_built = false;
         if (c->rows_on) {                         // fixed cloud: detect the lattice rows once
@@ -404,7 +394,7 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
     }
     const int64_t reset[4] = {0, 0, 0, 0};
     cudaMemcpyAsync(c->err, reset, sizeof(reset), cudaMemcpyHostToDevice, s);
-    cudaMemcpyAsync(c->gflag, reset, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(c->gflag, reset, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, s);
     c->graph_ok = true;
     // padding columns stay zero forever (TMA boxes of the last column group read them): both
     // buffers are cleared over the whole capacity, so rows that management appends past the
@@ -783,8 +773,8 @@ bgk_status bgk_count(bgk_ctx* c, int64_t* N, int64_t* n_interior, int64_t* n_bou
 
 bgk_status bgk_transport_info(bgk_ctx* c, int64_t* info) {
     if (!c || !info) return BGK_E_INVALID_ARG;
-    info[0] = c->d == 2 ? c->set_P : 1;       // particles per transport warp
-    info[1] = c->d == 2 ? c->set_QC : c->R;   // 3D: rows per lane; 2D: nodes per lane
+    info[0] = 1;                      // particles per transport warp
+    info[1] = c->R;
     info[2] = c->rows_built ? c->n_rows : 0;
     info[3] = c->rows_built ? c->n_rest : c->N_int;
     return BGK_OK;

@@ -16,10 +16,6 @@
 namespace bgk {
 
 constexpr int kPM = 5;          // moment partials per particle: s0, s_v (d), s_E  (2D: s0, s1, s2, sE, 0)
-// 2D set pair record (doubles): p_n (2), p_t (2), b_n, b_t with b_e = -p_e.W (first order); the
-// second-order WLS adds sigma = -s_n and a pad, with p_n, b_n pre-multiplied by sigma
-constexpr int kRecD2 = 6;
-constexpr int kRecD2SG = 8;
 constexpr int kMaxCellsPerAxis = 4096;
 
 struct Geo {                    // per-step geometry arrays (device)
@@ -74,16 +70,8 @@ struct bgk_ctx {
     int ncs;                           // stored column stride: ncol rounded up to a multiple of 16 in 3D (128-B rows)
     int64_t N, N_int, N_b, Kloc, Ks, RS;   // Kloc = n1*ncol logical nodes, Ks = n1*ncs stored, RS = Ks*nv doubles
     int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)
-    int ncg;                           // 3D: 32-column groups per chunk (transport)
-    // 2D particle sets (k_transport2s): set_P consecutive interior particles of the
-    // cell order walk the union of their neighbour lists together; a warp owns one set and one chunk
-    // of 32*set_QC consecutive local nodes, each lane set_QC nodes (lane + 32 q)
-    int set_P, set_QC;
-    int64_t nset;                      // sets of the current interior list: ceil(N_int / set_P)
-    int su_cap;                        // union entries per set (set_P * max_nb)
-    int32_t* su_n;                     // [sets] union size
-    int32_t* su_desc;                  // [sets][su_cap] (j << 8) | member mask, ascending j
-    double* su_rec;                    // [sets][su_cap][kRecD2 | kRecD2SG] pair records in (j, member) order
+    int ncg;                           // 32-column groups per chunk (transport)
+    int xc;                            // 2D, 33 columns: column 32 rides in the group's box (k_transport XC)
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
     CUtensorMap tmap_rows[2];          //   the same with the lattice-row kernel's box {32, kRowsR, 1}
     int max_nb;
@@ -94,7 +82,7 @@ struct bgk_ctx {
     double dv, vmin;
     int PD;                     // doubles of pair data per CSR entry
     int wls_order;              // 1 or 2 (second order adds the signed tail to the pair record)
-    int R, nchunk, nslots, nwpp; // transport mapping (2D: nchunk = node chunks of 32*set_QC)
+    int R, nchunk, nslots, nwpp; // transport mapping
     int bnd_chunk, bnd_nch;     // boundary node chunking
     bool geometry_valid;
     int fcur;
@@ -150,9 +138,11 @@ struct bgk_ctx {
     int force_eager;               // steps that must run eagerly (a management change to apply)
     cudaGraphExec_t gexec[2];
     uint64_t gkey[2];
-    int64_t* gflag;                // [2] device: [0] a management change skipped the rest, [1] bodies run
+    int64_t* gflag;                // [4] device: [0] a management change skipped the rest, [1] bodies run,
+                                   // [2] bodies in total, [3] test hook fired (graph.cu)
     int64_t gsteps;                // graph steps enqueued since the last reconcile (managed mode)
     int gfcur0;                    // fcur before the first of them
+    int64_t gstat[3];              // graph launches, captures, re-run steps (bgk_graph_info)
     int64_t* scan_tmp;  // [1024]
     int32_t* blk_tmp;   // [1024] per-block partial counts of the multi-block scans
     bgk::Geo g;
@@ -240,9 +230,7 @@ void launch_to_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream
 void launch_from_canonical(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_check_domain(bgk_ctx* c, cudaStream_t s);
 int transport_rows_per_thread(int d, int n1);
-// 2D particle sets: (P, QC) of the instantiated set kernels, and the per-set union build (geometry)
-void set_mapping_2d(int wls_order, int* P, int* QC);
-void launch_set_union(bgk_ctx* c, cudaStream_t s);
+
 bool make_tensor_maps(bgk_ctx* c);
 // fixed-cloud lattice rows: host-side group detection on the cached geometry, and the kernel
 bgk_status build_rows(bgk_ctx* c, cudaStream_t s);

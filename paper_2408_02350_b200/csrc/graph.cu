@@ -26,13 +26,25 @@ __global__ void k_gate_pending(cudaGraphConditionalHandle h, const int64_t* __re
     cudaGraphSetConditional(h, flag[0] == 0 ? 1u : 0u);
 }
 
-__global__ void k_gate_changed(cudaGraphConditionalHandle h, const int64_t* __restrict__ rep, int64_t* flag) {
-    const bool changed = rep[7] != 0;
+// flag[0]: a change skipped the rest (sticky until reconciled), flag[1]: bodies run since the last
+// reconcile, flag[2]: bodies run in total, flag[3]: the test hook below has fired.  skip_at >= 0
+// (BGK_TEST_GRAPH_SKIP_AT, tests only) treats graph step number skip_at as a change once, so the
+// skip / reconcile / re-run machinery is exercised on clouds where no pass ever changes anything.
+__global__ void k_gate_changed(cudaGraphConditionalHandle h, const int64_t* __restrict__ rep, int64_t* flag,
+                               int64_t skip_at) {
+    bool changed = rep[7] != 0;
+    if (!changed && skip_at >= 0 && flag[3] == 0 && flag[2] == skip_at) {
+        changed = true;
+        flag[3] = 1;
+    }
     if (changed) flag[0] = 1;
     cudaGraphSetConditional(h, changed ? 0u : 1u);
 }
 
-__global__ void k_step_done(int64_t* flag) { flag[1] += 1; }
+__global__ void k_step_done(int64_t* flag) {
+    flag[1] += 1;
+    flag[2] += 1;
+}
 
 uint64_t mix(uint64_t h, uint64_t v) {
     h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
@@ -50,7 +62,9 @@ uint64_t graph_key(const bgk_ctx* c) {
     return h | 1ull;    // 0 = empty slot
 }
 
-bool enabled() {
+}  // namespace
+
+bool graph_enabled() {
     static const bool on = [] {
         const char* e = getenv("BGK_GRAPH");
         return !(e && atoi(e) == 0);
@@ -58,11 +72,12 @@ bool enabled() {
     return on;
 }
 
+namespace {
+
 // the part of ensure_geometry after neighbours and management (ALE: every step)
 void geometry_tail(bgk_ctx* c, cudaStream_t s) {
     launch_wls(c, s);
     launch_bnd_union(c, s);
-    if (c->d == 2) launch_set_union(c, s);
 }
 
 // transport .. boundary fill with the current parity (fcur is flipped by the caller)
@@ -130,7 +145,8 @@ bool capture(bgk_ctx* c, int slot) {
             ok = add_if(cs, bs, h1, [&](cudaStream_t b) {
                 launch_build_neighbors(c, b);
                 manage_decide(c, b);
-                k_gate_changed<<<1, 1, 0, b>>>(h2, c->mg.rep, c->gflag);
+                const char* sk = getenv("BGK_TEST_GRAPH_SKIP_AT");
+                k_gate_changed<<<1, 1, 0, b>>>(h2, c->mg.rep, c->gflag, sk ? atoll(sk) : -1);
             });
         }
         ok = ok && add_if(cs, bs, h2, [&](cudaStream_t b) {
@@ -155,7 +171,7 @@ bool capture(bgk_ctx* c, int slot) {
 }  // namespace
 
 bool graph_step(bgk_ctx* c, cudaStream_t s) {
-    if (!enabled() || !c->graph_ok || c->ncol != c->ncol_g) return false;
+    if (!graph_enabled() || !c->graph_ok || c->ncol != c->ncol_g) return false;
     cudaStreamCaptureStatus cst;
     if (cudaStreamIsCapturing(s, &cst) != cudaSuccess || cst != cudaStreamCaptureStatusNone) return false;
     if (!c->cfg.ale && !c->geometry_valid) return false;     // fixed cloud: first step builds it eagerly
@@ -177,6 +193,7 @@ bool graph_step(bgk_ctx* c, cudaStream_t s) {
             return false;
         }
         c->gkey[slot] = key;
+        ++c->gstat[1];
     }
     if (c->cfg.manage && c->cfg.ale) {
         if (c->gsteps == 0) c->gfcur0 = c->fcur;
@@ -190,6 +207,7 @@ bool graph_step(bgk_ctx* c, cudaStream_t s) {
     }
     c->gstream = s;
     c->fcur = 1 - c->fcur;
+    ++c->gstat[0];
     return true;
 }
 
@@ -197,7 +215,7 @@ bgk_status graph_reconcile(bgk_ctx* c, cudaStream_t s) {
     if (c->gsteps == 0) return BGK_OK;
     const int64_t n = c->gsteps;
     c->gsteps = 0;
-    int64_t fl[2] = {0, 0};
+    int64_t fl[2] = {0, 0};     // flag[0], flag[1]; flag[2], flag[3] persist
     int64_t rep[8];
     cudaError_t e = cudaStreamSynchronize(s);
     if (e == cudaSuccess) e = cudaMemcpy(fl, c->gflag, sizeof(fl), cudaMemcpyDeviceToHost);
@@ -208,6 +226,7 @@ bgk_status graph_reconcile(bgk_ctx* c, cudaStream_t s) {
     for (int r = 0; r < 6; ++r) c->mg_report[r] = rep[r];
     if (fl[0] == 0) return BGK_OK;                      // every enqueued step ran
     const int64_t done = fl[1];
+    c->gstat[2] += n - done;
     c->fcur = (int)((c->gfcur0 + done) & 1);            // the state is the start of step `done`
     c->eager_key = 0;
     c->force_eager = 1;
@@ -217,6 +236,19 @@ bgk_status graph_reconcile(bgk_ctx* c, cudaStream_t s) {
     if (st != BGK_OK) return st;
     return graph_reconcile(c, s);
 }
+
+}  // namespace bgk
+
+extern "C" bgk_status bgk_graph_info(bgk_ctx* c, int64_t* info) {
+    if (!c || !info) return BGK_E_INVALID_ARG;
+    info[0] = (bgk::graph_enabled() && c->graph_ok) ? 1 : 0;
+    info[1] = c->gstat[0];
+    info[2] = c->gstat[1];
+    info[3] = c->gstat[2];
+    return BGK_OK;
+}
+
+namespace bgk {
 
 void graph_release(bgk_ctx* c) {
     for (int b = 0; b < 2; ++b)

@@ -11,6 +11,7 @@
 //                    interior f^{n+1} (Z17, Z19) + rank-local incoming wall flux partials
 //  k_wall_reduce   : per boundary particle, fixed-order sum of the flux partials
 //  k_bnd_fill      : rho_w = -flux_in / sum_{v.n>0}(v.n) M_w ; outgoing half = rho_w M_w
+#include "async.cuh"
 #include "bgk_internal.cuh"
 
 namespace bgk {
@@ -95,6 +96,19 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
     const int64_t bi = blockIdx.x;
     if (bi >= A.n) return;
     const int p = A.ids[bi];
+    // 16-byte accesses: in 3D two adjacent columns (ncs is even), in 2D the (g1, g2) pair of a node.
+    // The first round of each thread's loads is issued before the moment recovery and the
+    // exponentials below, so its latency overlaps them (short 2D rows: one round per thread).
+    double2* fp2 = reinterpret_cast<double2*>(A.f + (int64_t)p * A.Ks * NV);
+    const int P = (D == 3) ? A.ncs / 2 : A.ncs;              // 16-B elements per stored row
+    const int n2 = P * A.n1;
+    constexpr int U = 4;
+    double2 g[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const int u = threadIdx.x + q * blockDim.x;
+        if (u < n2) g[q] = fp2[u];
+    }
     if (threadIdx.x == 0) {
         const double* s = A.sums + (int64_t)p * kPM;
         double dvd = A.dv * A.dv;
@@ -156,13 +170,8 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
         colf[c] = cf;
     }
     __syncthreads();
-    double2* fp2 = reinterpret_cast<double2*>(A.f + (int64_t)p * A.Ks * NV);
-    // 16-byte accesses: in 3D two adjacent columns (ncs is even), in 2D the (g1, g2) pair of a node.
     // Four independent loads in flight per thread; (row, column) of each advance incrementally
     // (no integer division in the streaming loop).
-    const int P = (D == 3) ? A.ncs / 2 : A.ncs;              // 16-B elements per stored row
-    const int n2 = P * A.n1;
-    constexpr int U = 4;
     const int stride = U * blockDim.x;
     const int dk = stride / P, dc = stride - dk * P;
     int kr[U], cq[U];
@@ -173,11 +182,12 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
         cq[q] = u - kr[q] * P;
     }
     for (int u0 = threadIdx.x; u0 < n2; u0 += stride) {
-        double2 g[U];
+        if (u0 != (int)threadIdx.x) {
 #pragma unroll
-        for (int q = 0; q < U; ++q) {
-            const int u = u0 + q * blockDim.x;
-            if (u < n2) g[q] = fp2[u];
+            for (int q = 0; q < U; ++q) {
+                const int u = u0 + q * blockDim.x;
+                if (u < n2) g[q] = fp2[u];
+            }
         }
 #pragma unroll
         for (int q = 0; q < U; ++q) {
@@ -580,6 +590,146 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp_u(const int32_t* __res
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Boundary interpolation with the union rows staged by bulk copies (k_bnd_interp_t).  Block =
+// (group of G face-consecutive boundary particles, chunk of 256*NPT stored nodes).  The group's
+// union rows (k_bnd_union) stream through an NS-deep shared-memory ring: one contiguous
+// cp.async.bulk per (row, chunk) on a "full" mbarrier, released by every warp on an "empty"
+// mbarrier before thread 0 refills it NS rows ahead -- the row traffic is in flight asynchronously
+// instead of waiting on each thread's loads (the __ldg form of k_bnd_interp_u sat at ~4 TB/s of
+// useful L2 traffic, latency-bound).  Each thread applies a staged row to its NPT nodes for all G
+// members (dense G-column weights).  A chunk with no incoming node for any member (walls normal to
+// v_1: half the rows) only writes zero flux partials.
+// ---------------------------------------------------------------------------------------------
+template <int D, int G, int NPT, int NS>
+__global__ void __launch_bounds__(256) k_bnd_interp_t(const int32_t* __restrict__ bids, int64_t nb,
+                                                      const int8_t* __restrict__ kind,
+                                                      const int32_t* __restrict__ bu_j,
+                                                      const double* __restrict__ bu_w,
+                                                      const int32_t* __restrict__ bu_n, int cap,
+                                                      double* __restrict__ f, double* __restrict__ wallpart,
+                                                      int nch, int n1, int ncol, int ncs, int c0, int64_t Kloc,
+                                                      double vmax, double dv) {
+    constexpr int NV = (D == 2) ? 2 : 1;
+    constexpr int CH = 256 * NPT;                             // stored nodes per chunk
+    constexpr uint32_t SB = CH * NV * sizeof(double);         // bytes per ring stage
+    extern __shared__ __align__(128) unsigned char sm[];
+    double* ring = reinterpret_cast<double*>(sm);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * SB);
+    uint64_t* empty = full + NS;
+    double* sW = reinterpret_cast<double*>(empty + NS);       // [U][G]
+    int32_t* sJ = reinterpret_cast<int32_t*>(sW + (size_t)cap * G);
+    __shared__ double sh[32];
+    const int64_t g = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int U = bu_n[g];
+    int b[G], axis[G];
+    bool live[G];
+    double sgn[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        const int64_t bi = g * G + q;
+        live[q] = bi < nb;
+        b[q] = live[q] ? bids[bi] : 0;
+        const int wid = live[q] ? kind[b[q]] : 1;
+        axis[q] = (wid - 1) / 2;
+        sgn[q] = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
+    }
+    int64_t t[NPT];
+    double v[NPT][3];
+    bool inc[G][NPT];
+    bool any = false;
+#pragma unroll
+    for (int n = 0; n < NPT; ++n) {
+        t[n] = (int64_t)blockIdx.y * CH + n * 256 + tid;
+        v[n][0] = v[n][1] = v[n][2] = 0.0;
+        const bool in_range = t[n] < Kloc && node_vel_s<D>(t[n], ncs, ncol, c0, n1, vmax, dv, v[n]);
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            inc[q][n] = live[q] && in_range && sgn[q] * v[n][axis[q]] <= 0.0;
+            any = any || inc[q][n];
+        }
+    }
+    if (!__syncthreads_or(any) || U == 0) {                   // nothing incoming in this chunk
+        if (tid < G && g * G + tid < nb) wallpart[(g * G + tid) * nch + blockIdx.y] = 0.0;
+        return;
+    }
+    for (int i = tid; i < U * G; i += blockDim.x) sW[i] = bu_w[g * cap * G + i];
+    for (int i = tid; i < U; i += blockDim.x) sJ[i] = bu_j[g * cap + i];
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 256 / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t c0n = (int64_t)blockIdx.y * CH;
+    const uint32_t bytes = (uint32_t)(min((int64_t)CH, Kloc - c0n) * NV * sizeof(double));
+    auto issue = [&](int u) {                                 // thread 0: row u's chunk into stage u % NS
+        const int s = u % NS;
+        mbar_expect_tx(full + s, bytes);
+        bulk_load(ring + (size_t)s * CH * NV, f + ((int64_t)sJ[u] * Kloc + c0n) * NV, bytes, full + s);
+    };
+    if (tid == 0)
+        for (int u = 0; u < NS && u < U; ++u) issue(u);
+    double acc[G][NPT][NV];
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+        for (int n = 0; n < NPT; ++n)
+#pragma unroll
+            for (int c = 0; c < NV; ++c) acc[q][n][c] = 0.0;
+    for (int u = 0; u < U; ++u) {
+        const int s = u % NS;
+        const uint32_t ph = (uint32_t)(u / NS) & 1u;
+        mbar_wait(full + s, ph);
+        const double* st = ring + (size_t)s * CH * NV;
+        double fv[NPT][NV];
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) {
+            if constexpr (NV == 1) {
+                fv[n][0] = st[n * 256 + tid];
+            } else {
+                const double2 gv = reinterpret_cast<const double2*>(st)[n * 256 + tid];
+                fv[n][0] = gv.x;
+                fv[n][1] = gv.y;
+            }
+        }
+        const double* wu = sW + u * G;
+#pragma unroll
+        for (int q = 0; q < G; ++q) {
+            const double w = wu[q];
+#pragma unroll
+            for (int n = 0; n < NPT; ++n)
+#pragma unroll
+                for (int c = 0; c < NV; ++c) acc[q][n][c] = fma(w, fv[n][c], acc[q][n][c]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);                // this warp is done with stage s
+        if (tid == 0 && u + NS < U) {
+            mbar_wait(empty + s, ph);
+            issue(u + NS);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        double flux = 0.0;
+#pragma unroll
+        for (int n = 0; n < NPT; ++n) {
+            if (!inc[q][n]) continue;
+            if constexpr (NV == 1) f[(int64_t)b[q] * Kloc + t[n]] = acc[q][n][0];
+            else reinterpret_cast<double2*>(f)[(int64_t)b[q] * Kloc + t[n]] = make_double2(acc[q][n][0], acc[q][n][1]);
+            const double vn = sgn[q] * v[n][axis[q]];
+            if (vn < 0.0) flux += vn * acc[q][n][0];
+        }
+        const double tot = block_sum<256>(flux, sh);
+        if (threadIdx.x == 0 && live[q]) wallpart[(g * G + q) * nch + blockIdx.y] = tot;
+    }
+}
+
 __global__ void k_wall_reduce(const int32_t* __restrict__ bids, int64_t nb, const double* __restrict__ wallpart,
                               int nch, double* __restrict__ wallnum) {
     const int64_t bi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -763,8 +913,35 @@ void bnd_interp_g(bgk_ctx* c, double* fnew, cudaStream_t s) {
                                                      c->c0, c->Ks, c->cfg.vmax, c->dv);
 }
 
+template <int D, int G>
+void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
+    constexpr int NPT = D == 3 ? 4 : 2, NS = 6, CH = 256 * NPT;
+    constexpr int NV = D == 2 ? 2 : 1;
+    const size_t smem = (size_t)NS * CH * NV * sizeof(double) + 2 * NS * sizeof(uint64_t) +
+                        (size_t)c->bu_cap * (G * sizeof(double) + sizeof(int32_t));
+    static bool configured[kMaxDevices] = {};
+    if (first_use_on_device(configured))
+        cudaFuncSetAttribute(k_bnd_interp_t<D, G, NPT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int nch = (int)((c->Ks + CH - 1) / CH);
+    dim3 gg((unsigned)((c->N_b + G - 1) / G), (unsigned)nch);
+    k_bnd_interp_t<D, G, NPT, NS><<<gg, 256, smem, s>>>(c->boundary, c->N_b, c->kind, c->bu_j, c->bu_w, c->bu_n,
+                                                        c->bu_cap, fnew, c->wallpart, nch, c->n1, c->ncol, c->ncs,
+                                                        c->c0, c->Ks, c->cfg.vmax, c->dv);
+    k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart, nch,
+                                                                    c->wallnum);
+}
+
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
+    static const bool ring = [] {
+        const char* e = getenv("BGK_BND_RING");        // 0: the __ldg union kernel (k_bnd_interp_u)
+        return !(e && atoi(e) == 0);
+    }();
+    if (c->bnd_g && ring) {
+        if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_t<3, 4>(c, fnew, s) : bnd_interp_t<3, 8>(c, fnew, s));
+        else (c->bnd_g == 4 ? bnd_interp_t<2, 4>(c, fnew, s) : bnd_interp_t<2, 8>(c, fnew, s));
+        return;
+    }
     if (c->bnd_g) {
         if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_g<3, 4>(c, fnew, s) : bnd_interp_g<3, 8>(c, fnew, s));
         else (c->bnd_g == 4 ? bnd_interp_g<2, 4>(c, fnew, s) : bnd_interp_g<2, 8>(c, fnew, s));

@@ -35,6 +35,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "async.cuh"
 #include "bgk_internal.cuh"
 
 namespace bgk {
@@ -58,78 +59,8 @@ struct TArgs {
     int n1, ncol, ncs, c0, ncg, nwpp;   // nwpp: partial slots per particle (stride)
     int nw_grid;                        // (chunk x column group) items of this launch
     double vmax, dv, dt;
+    int xc;                             // 2D, 33 columns: the box carries column 32 too (Stage XC)
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-// one elected lane of a fully active warp (elect.sync): the TMA operands it uses are warp-uniform,
-// so the compiler issues them from uniform registers without a per-lane serialisation loop
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "elect.sync _|p, 0xffffffff;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(pred));
-    return pred != 0;
-}
-
-// non-blocking phase test: 1 if the phase with the given parity has completed
-__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok;
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
 
 // min(t, 0) without the fp64 pipe: the high word's sign decides, min(hi, 0) on the integer
 // pipe keeps a negative t exactly and turns a positive one into the denormal lo * 2^-1074
@@ -169,10 +100,10 @@ __device__ __forceinline__ void pair_coeffs(const double* pv, const double (&c0v
 // Epilogue of one (particle, chunk, column group) item: ftilde = f - dt (sum_j C f_j - f sum_j C)
 // on the lane's R rows, the warp's moment partials (fixed-order shuffles: deterministic) and
 // max_k sum_j |C_ijk| into the stability word.
-template <int D, int R, bool SG, int NV = (D == 2 ? 2 : 1)>
+template <int D, int R, bool SG, int XC = 0, int NV = (D == 2 ? 2 : 1)>
 __device__ __forceinline__ void transport_epilogue(const TArgs& A, int p, int w, int k1s, int colc, int gc,
                                                    bool valid, const double (&Qf)[R][NV], const double (&Sc)[R],
-                                                   const double (&Sa)[SG ? R : 1]) {
+                                                   const double (&Sa)[SG ? R : 1], const double (&Qt)[3]) {
     const int lane = threadIdx.x & 31;
     const int64_t rowstride = (int64_t)A.ncs * NV;
     const int64_t lane_off = (int64_t)k1s * rowstride + (int64_t)colc * NV;
@@ -217,6 +148,22 @@ __device__ __forceinline__ void transport_epilogue(const TArgs& A, int p, int w,
             else amax = fmax(amax, -cq * Sc[r]);
         }
     }
+    if constexpr (XC) {                                  // lane l < R: node (k1s + l, column 32)
+        const int kr = k1s + lane;
+        if (lane < R && kr < A.n1) {
+            const int64_t o = ((int64_t)p * A.n1 + kr) * rowstride + 32 * NV;
+            const double2 fv = __ldg(reinterpret_cast<const double2*>(A.f + o));
+            const double o0 = fv.x - dtq * (Qt[0] - fv.x * Qt[2]);
+            const double o1 = fv.y - dtq * (Qt[1] - fv.y * Qt[2]);
+            *reinterpret_cast<double2*>(A.ft + o) = make_double2(o0, o1);
+            const double v1 = axis_node(A.vmax, A.dv, kr), v2 = axis_node(A.vmax, A.dv, A.c0 + 32);
+            s0 += o0;
+            s1 += v1 * o0;
+            s2 += v2 * o0;
+            sE += (v1 * v1 + v2 * v2) * o0 + o1;
+            amax = fmax(amax, -cq * Qt[2]);
+        }
+    }
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
@@ -242,20 +189,25 @@ __device__ __forceinline__ void transport_epilogue(const TArgs& A, int p, int w,
 // One ring stage: the neighbour's box of f (R rows x 32 columns x nv) and its pair data P_e.
 // SG (second-order WLS): the pair record carries s_n = -sign(abar) after the first-order fields,
 // and C's n-term is y_n + s_n |y_n| (abar may be negative; P:408-410 applied literally).
-template <int D, int R, bool SG = false>
+// XC = 1 (2D, 33 columns): the box also carries the column after the group (33 columns), whose R
+// nodes of the chunk lanes 0..R-1 update one each (no separate tail kernel).
+template <int D, int R, bool SG = false, int XC = 0>
 struct Stage {
     static constexpr int NV = (D == 2) ? 2 : 1;
     static constexpr int PD0 = (D == 2) ? 4 : 10;
     static constexpr int PD = SG ? PD0 + 2 : PD0;
-    static constexpr int ROW = 32 * NV;                                  // doubles per staged row
+    static constexpr int ROW = (32 + XC) * NV;                           // doubles per staged row
     static constexpr uint32_t F_BYTES = R * ROW * sizeof(double);
     static constexpr uint32_t P_BYTES = PD * sizeof(double);
     static constexpr uint32_t BYTES = (F_BYTES + P_BYTES + 127) / 128 * 128;
 };
 
-template <int D, int R, int NST, int WPB, bool SG, int MINB = 1>
-__global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
-    using St = Stage<D, R, SG>;
+template <int D, int R, int NST, int WPB, bool SG, int XC = 0>
+// minBlocks = 1 is explicit on purpose: with __launch_bounds__(64) alone ptxas capped the R = 25
+// instantiation at 164 registers (229 with it) and C5 transport went from 69 to 93 ms.
+__global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
+    static_assert(XC == 0 || (D == 2 && !SG && R <= 32), "extra column: 2D first order, one row per lane");
+    using St = Stage<D, R, SG, XC>;
     constexpr int NV = St::NV;
     constexpr int PD = St::PD;
     constexpr int ROW = St::ROW;
@@ -299,7 +251,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
         const int s = (int)((g0 + (uint32_t)e) % NST);
         unsigned char* st = ring + s * St::BYTES;
         mbar_expect_tx(bars + s, St::F_BYTES + St::P_BYTES);
-        tma_load_3d(st, &tmap, cg * ROW, k1s, jn, bars + s);
+        tma_load_3d(st, &tmap, cg * 32 * NV, k1s, jn, bars + s);
         bulk_load(st + St::F_BYTES, Pp + (int64_t)e * PD, St::P_BYTES, bars + s);
     };
 #pragma unroll
@@ -321,6 +273,12 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
     } else {
         c0v[1] = axis_node(A.vmax, A.dv, gc) - Wp[1];
     }
+    // XC: this lane's node of the extra column (row k1s + lane, column 32) relative to W_p
+    double ct1 = 0.0, ct2 = 0.0, Qt[3] = {0.0, 0.0, 0.0};   // Qt: Q(g1), Q(g2), sum C of that node
+    if constexpr (XC) {
+        ct1 = axis_node(A.vmax, A.dv, min(k1s + lane, A.n1 - 1)) - Wp[0];
+        ct2 = axis_node(A.vmax, A.dv, A.c0 + 32) - Wp[1];
+    }
     double Qf[R][NV], Sc[R], Sa[SG ? R : 1];   // Sa: sum_j |C| (= -Sc when every C <= 0)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -332,6 +290,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
     // per-neighbour coefficients at the chunk's first node: y_e = P_e . c0, dy_e = dv P_e[0],
     // L = sum_e y_e, dL = sum_e dy_e (read from the stage's pair-data slot)
     const double c1dv = c0v[0] / A.dv;
+    double pr[4] = {0.0, 0.0, 0.0, 0.0};   // XC: the 2D pair record of the current neighbour
     auto coeffs = [&](int e, double (&y)[D], double (&dy)[D], double& Lc, double& dL, double& sn) {
         const double* ps =
             reinterpret_cast<const double*>(ring + ((g0 + (uint32_t)e) % NST) * St::BYTES + St::F_BYTES);
@@ -340,6 +299,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
         for (int q = 0; q < PD; ++q) pv[q] = ps[q];       // broadcast LDS
         pair_coeffs<D>(pv, c0v, c1dv, A.dv, y, dy, Lc, dL);
         if constexpr (SG) sn = pv[St::PD0];
+        if constexpr (XC) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pr[q] = pv[q];
+        }
     };
     // The readiness of the NEXT stage is tested (non-blocking mbarrier.test_wait) before this
     // neighbour's rows, so the barrier check's latency overlaps the row arithmetic; only if the
@@ -397,6 +360,15 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
                 }
                 Sc[r] += C;
             }
+            if constexpr (XC) {     // the extra column: lane l < R takes row k1s + l (8 DP, whole warp)
+                const double* sb = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES);
+                const double2 v = *reinterpret_cast<const double2*>(sb + min(lane, R - 1) * ROW + 32 * NV);
+                const double yn = fma(pr[1], ct2, pr[0] * ct1), yt = fma(pr[3], ct2, pr[2] * ct1);
+                const double C = neg_part(yn) + neg_part(yt);
+                Qt[0] = fma(C, v.x, Qt[0]);
+                Qt[1] = fma(C, v.y, Qt[1]);
+                Qt[2] += C;
+            }
         }
         // refill stage of neighbour e with neighbour e + NST (index from the register batches)
         const int t = e + NST;
@@ -413,7 +385,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
             coeffs(e + 1, y, dy, Lc, dL, sn);
         }
     }
-    transport_epilogue<D, R, SG>(A, p, w, k1s, colc, gc, valid, Qf, Sc, Sa);
+    transport_epilogue<D, R, SG, XC>(A, p, w, k1s, colc, gc, valid, Qf, Sc, Sa, Qt);
     }
 }
 
@@ -555,410 +527,32 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
         e0 = n0;
         e1 = n1;
     }
-    const double Sa[1] = {0.0};
+    const double Sa[1] = {0.0}, Qt[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int k = 0; k < G; ++k) transport_epilogue<3, R, false>(A, p0 + k * S, w, k1s, colc, gc, valid, Qf[k], Sc, Sa);
+    for (int k = 0; k < G; ++k)
+        transport_epilogue<3, R, false>(A, p0 + k * S, w, k1s, colc, gc, valid, Qf[k], Sc, Sa, Qt);
 }
 
-// ============================================================================
-// 2D particle sets (k_transport2s).  A 2D node carries (g1, g2): a lane's load of
-// f_jk is 16 B against ~4 DP of work per value, so the one-particle warp of the 3D kernel reads
-// twice the bytes per flop and sat at the L2 -> SM limit in 2D (4.7 GB per C2 step).  Here a warp
-// owns a SET of P consecutive interior particles of the cell order and walks the union of their
-// neighbour lists (ascending j): each union entry's box -- a chunk of 32*QC consecutive local
-// nodes k1*ncol + col of f_j, contiguous in the unpadded 2D row, one bulk copy -- is loaded once
-// and applied to every member that has j as a neighbour, with that member's pair record (staged
-// with the box).  Lane l owns nodes t0 + l + 32 q (q < QC) of the chunk, so any column count maps
-// without tail columns.  The projections are y_e = p_e . v_k + b_e with b_e = -p_e . W_i folded
-// into the record at geometry time (2 DFMA each), C/2 = neg(y_n) + neg(y_t) (Z5-Z7),
-// and Q1, Q2, Sc accumulate per (member, node): 8 DP per (i, j, k) triple, the survey's 2D lean
-// count.  The second-order WLS (Z27: the n-term y_n - sign(abar)|y_n|) stores sigma = -s_n and
-// sigma p_n, sigma b_n, so C/2 = sigma neg(sigma y_n) + neg(y_t) (one DFMA in place of the DADD).
-// ============================================================================
-template <int P, typename T>
-__device__ __forceinline__ T pick(const T (&a)[P], int b) {
-    T r = a[0];
-#pragma unroll
-    for (int q = 1; q < P; ++q)
-        if (q == b) r = a[q];
-    return r;
-}
-
-// Union of one set's neighbour lists (warp per set): every (member b, entry e) is ranked in the
-// (j, b) order by binary searches in the other members' sorted lists, the first of each j run
-// writes the union descriptor (j << 8 | members holding j), and every element writes its pair record
-// at its rank -- so the records of union entry u are contiguous, in member order, and the transport
-// finds them by a running popcount.
-template <int P, bool SG>
-__global__ void __launch_bounds__(128) k_set_union2(const int32_t* __restrict__ order, int64_t n_int,
-                                                    const int64_t* __restrict__ nb_off,
-                                                    const int32_t* __restrict__ nb_idx, const double* __restrict__ Pr,
-                                                    const double* __restrict__ W, int su_cap,
-                                                    int32_t* __restrict__ su_n, int32_t* __restrict__ su_desc,
-                                                    double* __restrict__ su_rec) {
-    static_assert(P <= 8, "member mask is 8 bits");
-    constexpr int RD = SG ? kRecD2SG : kRecD2;
-    constexpr int PD = SG ? 6 : 4;                  // CSR pair record: p_n, p_t [, s_n, 0]
-    extern __shared__ unsigned long long skeys[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t s = (int64_t)blockIdx.x * 4 + wib;
-    const int64_t nset = (n_int + P - 1) / P;
-    if (s >= nset) return;
-    unsigned long long* keys = skeys + (size_t)wib * su_cap;
-    int pb[P], mb[P];
-    int64_t ob[P];
-    int total = 0;
-#pragma unroll
-    for (int b = 0; b < P; ++b) {
-        const int64_t pos = s * P + b;
-        const bool in = pos < n_int;
-        pb[b] = in ? order[pos] : 0;
-        ob[b] = in ? nb_off[pb[b]] : 0;
-        mb[b] = in ? (int)(nb_off[pb[b] + 1] - ob[b]) : 0;
-        total += mb[b];
-    }
-    for (int t = lane; t < total; t += 32) {
-        int b = 0, e = t;
-#pragma unroll
-        for (int q = 0; q < P - 1; ++q)
-            if (b == q && e >= mb[q]) {
-                e -= mb[q];
-                b = q + 1;
-            }
-        const int32_t j = nb_idx[pick(ob, b) + e];
-        int rank = e;
-        bool first = true;
-        unsigned mask = 1u << b;
-#pragma unroll
-        for (int q = 0; q < P; ++q) {
-            if (q == b || mb[q] == 0) continue;
-            const int32_t* Lq = nb_idx + ob[q];
-            int lo = 0, hi = mb[q];
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (Lq[mid] < j) lo = mid + 1;
-                else hi = mid;
-            }
-            const bool found = lo < mb[q] && Lq[lo] == j;
-            rank += (q < b) ? lo + (int)found : lo;
-            if (found) {
-                mask |= 1u << q;
-                if (q < b) first = false;
-            }
-        }
-        keys[rank] = ((unsigned long long)(uint32_t)j << 32) | ((unsigned long long)first << 31) |
-                     ((unsigned long long)mask << 16) | ((unsigned long long)b << 12) | (unsigned long long)e;
-    }
-    __syncwarp();
-    int ubase = 0;
-    for (int t0 = 0; t0 < total; t0 += 32) {
-        const int t = t0 + lane;
-        const bool v = t < total;
-        const unsigned long long key = v ? keys[t] : 0ull;
-        const bool first = v && ((key >> 31) & 1ull);
-        const unsigned bal = __ballot_sync(0xffffffffu, first);
-        if (first)
-            su_desc[s * su_cap + ubase + __popc(bal & ((1u << lane) - 1u))] =
-                (int32_t)(((uint32_t)(key >> 32) << 8) | (uint32_t)((key >> 16) & 0xffull));
-        if (v) {
-            const int b = (int)((key >> 12) & 15ull), e = (int)(key & 4095ull);
-            const int p = pick(pb, b);
-            const double* pe = Pr + (pick(ob, b) + e) * PD;
-            const double w0 = W[(int64_t)p * 2], w1 = W[(int64_t)p * 2 + 1];
-            const double sg = SG ? -pe[4] : 1.0;        // sigma = -s_n = sign(abar) (second order)
-            const double pn1 = sg * pe[0], pn2 = sg * pe[1], pt1 = pe[2], pt2 = pe[3];
-            double* r = su_rec + (s * su_cap + t) * RD;
-            r[0] = pn1;
-            r[1] = pn2;
-            r[2] = pt1;
-            r[3] = pt2;
-            r[4] = -(pn1 * w0 + pn2 * w1);
-            r[5] = -(pt1 * w0 + pt2 * w1);
-            if constexpr (SG) {
-                r[6] = sg;
-                r[7] = 0.0;
-            }
-        }
-        ubase += __popc(bal);
-    }
-    if (lane == 0) su_n[s] = ubase;
-}
-
-struct SArgs {
-    const double* __restrict__ f;
-    double* __restrict__ ft;
-    const int32_t* __restrict__ order;
-    const int32_t* __restrict__ su_n;
-    const int32_t* __restrict__ su_desc;
-    const double* __restrict__ su_rec;
-    double* __restrict__ partials;
-    unsigned long long* stab;
-    int64_t n_int, nset, Kloc;
-    int su_cap, ncol, c0, nwpp;
-    double vmax, dv, dt;
-};
-
-template <int P, int QC, int B, bool SG>
-struct SetStage {
-    static constexpr int RD = SG ? kRecD2SG : kRecD2;
-    static constexpr uint32_t BOX = 32 * QC * 16;                     // 32*QC nodes of (g1, g2)
-    static constexpr uint32_t F_BYTES = B * BOX;                      // B union entries per stage
-    static constexpr uint32_t R_BYTES = B * P * RD * sizeof(double);  // their member records (<= P each)
-    static constexpr uint32_t BYTES = (F_BYTES + R_BYTES + 127) / 128 * 128;
-};
-
-// Stage = a batch of B consecutive union entries: B boxes and ONE bulk copy of the batch's records
-// (contiguous in su_rec: records are stored in (j, member) order), all on one mbarrier -- the
-// barrier wait, the expect_tx and the record copy are paid once per B entries.
-template <int P, int QC, int B, int NST, int WPB, bool SG, int MINB>
-__global__ void __launch_bounds__(WPB * 32, MINB) k_transport2s(const SArgs A) {
-    using St = SetStage<P, QC, B, SG>;
-    constexpr int RD = St::RD;
-    static_assert(32 % B == 0, "batches must not straddle descriptor batches");
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned char* ring = smem_raw + (size_t)wib * NST * St::BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)WPB * NST * St::BYTES) + wib * NST;
-    if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < NST; ++s) mbar_init(bars + s, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncwarp();
-    const int64_t set = (int64_t)blockIdx.x * WPB + wib;
-    if (set >= A.nset) return;                                   // warp-uniform
-    const int chunk = blockIdx.y;
-    const int64_t t0 = (int64_t)chunk * 32 * QC;
-    const uint32_t fbytes = (uint32_t)min((int64_t)(32 * QC), A.Kloc - t0) * 16u;
-    const int U = A.su_n[set];
-    const int nbat = (U + B - 1) / B;
-    const int32_t* desc = A.su_desc + set * A.su_cap;
-    const double* rec = A.su_rec + set * A.su_cap * RD;
-    const double2* fsrc = reinterpret_cast<const double2*>(A.f);
-
-    // union descriptors, 32 per register batch: (cA, cB) for consumption, (iA, iB) for refills
-    int cA = lane < U ? desc[lane] : 0;
-    int cB = 32 + lane < U ? desc[32 + lane] : 0;
-    int iA = cA, iB = cB;
-    int roff = 0;                                   // records issued so far (warp-uniform)
-    // batch k (entries kB .. kB+B) into stage k % NST; called by every lane (the copies by one)
-    auto issue = [&](int k, int da) {
-        const int st = k % NST;
-        unsigned char* sp = ring + st * St::BYTES;
-        int dd[B], cnt = 0;
-#pragma unroll
-        for (int q = 0; q < B; ++q) {
-            dd[q] = __shfl_sync(0xffffffffu, da, (k * B + q) & 31);
-            if (k * B + q >= U) dd[q] = 0;
-            cnt += __popc(dd[q] & 0xff);
-        }
-        const uint32_t rbytes = (uint32_t)cnt * RD * sizeof(double);
-        if (elect_one()) {
-            uint32_t fb = 0;
-#pragma unroll
-            for (int q = 0; q < B; ++q) fb += k * B + q < U ? fbytes : 0u;
-            mbar_expect_tx(bars + st, fb + rbytes);
-#pragma unroll
-            for (int q = 0; q < B; ++q)
-                if (k * B + q < U)
-                    bulk_load(sp + q * St::BOX, fsrc + (int64_t)((uint32_t)dd[q] >> 8) * A.Kloc + t0, fbytes,
-                              bars + st);
-            bulk_load(sp + St::F_BYTES, rec + (int64_t)roff * RD, rbytes, bars + st);
-        }
-        roff += cnt;
-    };
-#pragma unroll
-    for (int k = 0; k < NST; ++k) {
-        if (k >= nbat) break;
-        issue(k, iA);           // NST * B <= 32: the first stages come from the first descriptor batch
-    }
-    // velocities of the lane's nodes (clamped index past the end: those nodes are never stored)
-    double v1[QC], v2[QC];
-#pragma unroll
-    for (int qq = 0; qq < QC; ++qq) {
-        const int64_t t = min(t0 + lane + 32 * qq, A.Kloc - 1);
-        const int k1 = (int)(t / A.ncol), col = (int)(t - (int64_t)k1 * A.ncol);
-        v1[qq] = axis_node(A.vmax, A.dv, k1);
-        v2[qq] = axis_node(A.vmax, A.dv, A.c0 + col);
-    }
-    double Q1[P][QC], Q2[P][QC], Sc[P][QC], Sa[SG ? P : 1][SG ? QC : 1];
-#pragma unroll
-    for (int b = 0; b < P; ++b)
-#pragma unroll
-        for (int qq = 0; qq < QC; ++qq) {
-            Q1[b][qq] = Q2[b][qq] = Sc[b][qq] = 0.0;
-            if constexpr (SG) Sa[b][qq] = 0.0;
-        }
-    for (int k = 0; k < nbat; ++k) {
-        const int st = k % NST;
-        mbar_wait(bars + st, (uint32_t)(k / NST) & 1u);
-        const unsigned char* sp = ring + st * St::BYTES;
-        const double* rp = reinterpret_cast<const double*>(sp + St::F_BYTES);
-#pragma unroll
-        for (int q = 0; q < B; ++q) {
-            const int e = k * B + q;
-            if (e >= U) break;                                  // warp-uniform (last batch)
-            const int d = __shfl_sync(0xffffffffu, cA, e & 31);
-            const double2* fj2 = reinterpret_cast<const double2*>(sp + q * St::BOX) + lane;
-            double2 fj[QC];
-#pragma unroll
-            for (int qq = 0; qq < QC; ++qq) fj[qq] = fj2[32 * qq];
-            const unsigned mask = (unsigned)d & 0xffu;
-#pragma unroll
-            for (int b = 0; b < P; ++b) {
-                if (!(mask & (1u << b))) continue;              // warp-uniform
-                const double* pr = rp;                          // broadcast LDS
-                rp += RD;
-                const double pn1 = pr[0], pn2 = pr[1], pt1 = pr[2], pt2 = pr[3], bn = pr[4], bt = pr[5];
-                const double sg = SG ? pr[6] : 1.0;
-#pragma unroll
-                for (int qq = 0; qq < QC; ++qq) {
-                    const double yn = fma(pn1, v1[qq], fma(pn2, v2[qq], bn));
-                    const double yt = fma(pt1, v1[qq], fma(pt2, v2[qq], bt));
-                    double C;                                   // C/2 (the epilogue doubles)
-                    if constexpr (SG) C = fma(sg, neg_part(yn), neg_part(yt));
-                    else C = neg_part(yn) + neg_part(yt);
-                    Q1[b][qq] = fma(C, fj[qq].x, Q1[b][qq]);
-                    Q2[b][qq] = fma(C, fj[qq].y, Q2[b][qq]);
-                    Sc[b][qq] += C;
-                    if constexpr (SG) Sa[b][qq] += fabs(C);
-                }
-            }
-        }
-        if (((k + 1) * B & 31) == 0) {                          // consumed a whole descriptor batch
-            cA = cB;
-            cB = (k + 1) * B + 32 + lane < U ? desc[(k + 1) * B + 32 + lane] : 0;
-        }
-        // refill this stage with batch k + NST
-        const int kn = k + NST;
-        if ((kn * B & 31) == 0 && kn * B >= 32) {               // its descriptors start a new batch
-            iA = iB;
-            iB = kn * B + 32 + lane < U ? desc[kn * B + 32 + lane] : 0;
-        }
-        __syncwarp();                                           // every lane has read the stage
-        if (kn < nbat) issue(kn, iA);
-    }
-    // epilogue per member: ftilde = f - 2 dt (Q - f Sc) for (g1, g2), moment partials of the chunk
-    const double dtq = 2.0 * A.dt;
-    double2* fdst = reinterpret_cast<double2*>(A.ft);
-    double amax = 0.0;
-#pragma unroll
-    for (int b = 0; b < P; ++b) {
-        const int64_t pos = set * P + b;
-        if (pos >= A.n_int) break;
-        const int p = A.order[pos];
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, sE = 0.0;
-#pragma unroll
-        for (int qq = 0; qq < QC; ++qq) {
-            const int64_t t = t0 + lane + 32 * qq;
-            if (t < A.Kloc) {
-                const double2 fi = __ldg(fsrc + (int64_t)p * A.Kloc + t);
-                const double o0 = fi.x - dtq * (Q1[b][qq] - fi.x * Sc[b][qq]);
-                const double o1 = fi.y - dtq * (Q2[b][qq] - fi.y * Sc[b][qq]);
-                fdst[(int64_t)p * A.Kloc + t] = make_double2(o0, o1);
-                s0 += o0;
-                s1 += v1[qq] * o0;
-                s2 += v2[qq] * o0;
-                sE += (v1[qq] * v1[qq] + v2[qq] * v2[qq]) * o0 + o1;
-                amax = fmax(amax, SG ? 2.0 * Sa[b][qq] : -2.0 * Sc[b][qq]);
-            }
-        }
-        s0 = warp_sum(s0);
-        s1 = warp_sum(s1);
-        s2 = warp_sum(s2);
-        sE = warp_sum(sE);
-        if (lane == 0) {
-            double* pp = A.partials + ((int64_t)p * A.nwpp + chunk) * kPM;
-            pp[0] = s0;
-            pp[1] = s1;
-            pp[2] = s2;
-            pp[3] = sE;
-            pp[4] = 0.0;
-        }
-    }
-    amax = warp_max(amax);                                      // one stability atomic per warp
-    if (lane == 0) atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
-}
-
-template <int P, int QC, int B, bool SG, int MINB = 1, int NSTMAX = 8>
-void launch_set(const SArgs& a, int nchunk, cudaStream_t s) {
-    constexpr int WPB = 4;
-    using St = SetStage<P, QC, B, SG>;
-    constexpr int WPSM = MINB > 3 ? MINB * WPB : 12;
-    constexpr int NST00 = (200 * 1024) / (WPSM * (int)St::BYTES);   // ring for the resident warps per SM
-    constexpr int NST0 = NST00 > NSTMAX ? NSTMAX : NST00;
-    constexpr int NST1 = NST0 > 8 ? 8 : (NST0 < 2 ? 2 : NST0);
-    constexpr int NST = NST1 * B > 32 ? 32 / B : NST1;         // the prologue reads one descriptor batch
-    constexpr size_t smem = (size_t)WPB * NST * St::BYTES + WPB * NST * 8;
-    static bool configured[kMaxDevices] = {};
-    if (first_use_on_device(configured))
-        cudaFuncSetAttribute(k_transport2s<P, QC, B, NST, WPB, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    const unsigned gx = (unsigned)((a.nset + WPB - 1) / WPB);
-    k_transport2s<P, QC, B, NST, WPB, SG, MINB><<<dim3(gx, (unsigned)nchunk), WPB * 32, smem, s>>>(a);
-}
-
-void launch_transport2s(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
-    SArgs a;
-    a.f = fin;
-    a.ft = fout;
-    a.order = c->g.order;
-    a.su_n = c->su_n;
-    a.su_desc = c->su_desc;
-    a.su_rec = c->su_rec;
-    a.partials = c->partials;
-    a.stab = c->stab;
-    a.n_int = c->N_int;
-    a.nset = (c->N_int + c->set_P - 1) / c->set_P;
-    a.Kloc = c->Kloc;
-    a.su_cap = c->su_cap;
-    a.ncol = c->ncol;
-    a.c0 = c->c0;
-    a.nwpp = c->nwpp;
-    a.vmax = c->cfg.vmax;
-    a.dv = c->dv;
-    a.dt = c->cfg.dt;
-    const int key = c->set_P * 100 + c->set_QC;
-    if (c->wls_order == 2) return launch_set<4, 2, 4, true>(a, c->nchunk, s);
-    static const int var = [] {
-        const char* e = getenv("BGK_SET_VAR");          // tuning experiments (occupancy / ring depth)
-        return e ? atoi(e) : 0;
-    }();
-    if (var == 1) return launch_set<4, 4, 4, false, 3, 3>(a, c->nchunk, s);
-    if (var == 2) return launch_set<4, 2, 4, false, 4, 2>(a, c->nchunk, s);
-    if (var == 3) return launch_set<4, 4, 2, false, 3, 4>(a, c->nchunk, s);
-    if (var == 4) return launch_set<2, 8, 4, false, 3, 3>(a, c->nchunk, s);
-    if (var == 5) return launch_set<4, 2, 2, false, 4, 4>(a, c->nchunk, s);
-    switch (key) {
-        case 402: launch_set<4, 2, 4, false>(a, c->nchunk, s); break;
-        case 404: launch_set<4, 4, 4, false>(a, c->nchunk, s); break;
-        case 803: launch_set<8, 3, 4, false>(a, c->nchunk, s); break;
-        default: launch_set<8, 2, 4, false>(a, c->nchunk, s); break;
-    }
-}
-
-template <int D, int R, int WPB, bool SG, int MINB = 1>
+template <int D, int R, int WPB, bool SG, int XC = 0>
 constexpr int stages_for() {
     // ring depth: keep NST-1 neighbour boxes in flight; bounded by 227 KB of shared memory
-    // (sized for max(8, MINB WPB) resident warps per SM: blocks of WPB warps)
-    constexpr int blocks0 = WPB >= 8 ? 1 : 8 / WPB;
-    constexpr int blocks = MINB > blocks0 ? MINB : blocks0;
-    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R, SG>::BYTES);
+    // (sized for 8 resident warps per SM: blocks of WPB warps)
+    constexpr int blocks = WPB >= 8 ? 1 : 8 / WPB;
+    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R, SG, XC>::BYTES);
     return n > 8 ? 8 : (n < 2 ? 2 : n);
 }
 
-template <int D, int R, int WPB, bool SG = false, int MINB = 1>
+template <int D, int R, int WPB, bool SG = false, int XC = 0>
 void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int NST = stages_for<D, R, WPB, SG, MINB>();
-    constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG>::BYTES + WPB * NST * 8;
+    constexpr int NST = stages_for<D, R, WPB, SG, XC>();
+    constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG, XC>::BYTES + WPB * NST * 8;
     static bool configured[kMaxDevices] = {};
     if (first_use_on_device(configured)) {
-        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, XC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     }
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
-    k_transport<D, R, NST, WPB, SG, MINB><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(tm, a);
+    k_transport<D, R, NST, WPB, SG, XC><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(tm, a);
 }
 
 template <int D, int R>
@@ -967,26 +561,36 @@ void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) 
     if constexpr (D == 3 && R == 25) {
         if (wpb == 2) return launch_one<D, R, 2>(tm, a, s);
     }
+    if constexpr (D == 2 && (R == 17 || R == 13 || R == 11 || R == 9)) {
+        if (a.xc) return launch_one<D, R, kDefaultWarps, false, 1>(tm, a, s);   // 33 columns
+    }
     launch_one<D, R, kDefaultWarps>(tm, a, s);
 }
 
-void dispatch3(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
+template <int D>
+void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
+    if constexpr (D == 3) {
+        switch (R) {
+            case 25: launch_wpb<D, 25>(wpb, tm, a, s); return;
+            case 21: launch_wpb<D, 21>(wpb, tm, a, s); return;
+            case 15: launch_wpb<D, 15>(wpb, tm, a, s); return;
+            default: break;
+        }
+    }
     switch (R) {
-        case 25: launch_wpb<3, 25>(wpb, tm, a, s); return;
-        case 21: launch_wpb<3, 21>(wpb, tm, a, s); return;
-        case 17: launch_wpb<3, 17>(wpb, tm, a, s); return;
-        case 15: launch_wpb<3, 15>(wpb, tm, a, s); return;
-        case 13: launch_wpb<3, 13>(wpb, tm, a, s); return;
-        case 11: launch_wpb<3, 11>(wpb, tm, a, s); return;
-        case 9: launch_wpb<3, 9>(wpb, tm, a, s); return;
-        case 7: launch_wpb<3, 7>(wpb, tm, a, s); return;
-        case 5: launch_wpb<3, 5>(wpb, tm, a, s); return;
-        case 3: launch_wpb<3, 3>(wpb, tm, a, s); return;
-        default: launch_wpb<3, 1>(wpb, tm, a, s); return;
+        case 17: launch_wpb<D, 17>(wpb, tm, a, s); break;
+        case 13: launch_wpb<D, 13>(wpb, tm, a, s); break;
+        case 11: launch_wpb<D, 11>(wpb, tm, a, s); break;
+        case 9: launch_wpb<D, 9>(wpb, tm, a, s); break;
+        case 7: launch_wpb<D, 7>(wpb, tm, a, s); break;
+        case 5: launch_wpb<D, 5>(wpb, tm, a, s); break;
+        case 3: launch_wpb<D, 3>(wpb, tm, a, s); break;
+        default: launch_wpb<D, 1>(wpb, tm, a, s); break;
     }
 }
 
 constexpr int kRChoices3[] = {25, 21, 17, 15, 13, 11, 9, 7, 5, 3, 1};
+constexpr int kRChoices2[] = {17, 13, 11, 9, 7, 5, 3, 1};
 
 // the R of `choices` with the lowest modelled cost ceil(n1/R) (R + kRowsOverhead): padded rows
 // plus the per-neighbour fixed cost (barrier, pair record, setup, refill ~ 5 rows of issue)
@@ -1011,46 +615,13 @@ bool listed(const int (&choices)[K], int R) {
 
 }  // namespace
 
-// (P, QC) of the 2D particle-set kernel: P = 8 particles per warp, QC = 2 nodes per lane (the union of
-// 8 cell-consecutive lists is 0.30 of their sum on C2/C3 and 48 accumulators fit the registers);
-// BGK_SET_P / BGK_SET_QC select another instantiated pair (4/2, 4/4, 8/3); second order: 4/2
-void set_mapping_2d(int wls_order, int* P, int* QC) {
-    const char* ep = getenv("BGK_SET_P");      // read per context (tests select instantiations)
-    const char* eq = getenv("BGK_SET_QC");
-    int key = (ep ? atoi(ep) : 8) * 100 + (eq ? atoi(eq) : 2);
-    if (wls_order == 2) key = 402;
-    if (key != 402 && key != 404 && key != 803 && key != 802 && key != 208) key = 802;
-    *P = key / 100;
-    *QC = key % 100;
-}
-
-void launch_set_union(bgk_ctx* c, cudaStream_t s) {
-    if (c->N_int == 0) return;
-    const int64_t nset = (c->N_int + c->set_P - 1) / c->set_P;
-    const unsigned g = (unsigned)((nset + 3) / 4);
-    const size_t smem = (size_t)4 * c->su_cap * sizeof(unsigned long long);
-    static bool configured[kMaxDevices] = {};
-    if (first_use_on_device(configured)) {
-        cudaFuncSetAttribute(k_set_union2<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_set_union2<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_set_union2<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_set_union2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    }
-#define BGK_SU_ARGS c->g.order, c->N_int, c->g.nb_off, c->g.nb_idx, c->g.P, c->W, c->su_cap, c->su_n, c->su_desc, c->su_rec
-    if (c->wls_order == 2) k_set_union2<4, true><<<g, 128, smem, s>>>(BGK_SU_ARGS);
-    else if (c->set_P == 4) k_set_union2<4, false><<<g, 128, smem, s>>>(BGK_SU_ARGS);
-    else if (c->set_P == 2) k_set_union2<2, false><<<g, 128, smem, s>>>(BGK_SU_ARGS);
-    else k_set_union2<8, false><<<g, 128, smem, s>>>(BGK_SU_ARGS);
-#undef BGK_SU_ARGS
-}
-
-// rows per lane (3D): BGK_TRANSPORT_R if instantiated, else the instantiated R with the fewest
-// padded rows; 2D uses the particle-set kernel (set_mapping_2d) and ignores R
+// rows per lane: BGK_TRANSPORT_R if instantiated for the mapping, else the instantiated R with
+// the fewest padded rows (2D keeps three accumulators per row, so it stops at 17)
 int transport_rows_per_thread(int d, int n1) {
-    if (d != 3) return 1;
     const char* e = getenv("BGK_TRANSPORT_R");
     const int want = e ? atoi(e) : 0;
-    return listed(kRChoices3, want) ? want : fewest_padded(kRChoices3, n1);
+    if (d == 3) return listed(kRChoices3, want) ? want : fewest_padded(kRChoices3, n1);
+    return listed(kRChoices2, want) ? want : fewest_padded(kRChoices2, n1);
 }
 
 // TMA descriptors: f[b] viewed as a 3D fp64 tensor {ncs*nv (fastest), n1, N}; box {32*nv, R, 1}.
@@ -1067,7 +638,7 @@ bool make_tensor_maps(bgk_ctx* c) {
     const cuuint64_t dims[3] = {(cuuint64_t)c->ncs * c->nv, (cuuint64_t)c->n1, (cuuint64_t)c->N};
     const cuuint64_t strides[2] = {(cuuint64_t)c->ncs * c->nv * sizeof(double),
                                    (cuuint64_t)c->ncs * c->nv * c->n1 * sizeof(double)};
-    const cuuint32_t box[3] = {(cuuint32_t)(32 * c->nv), (cuuint32_t)c->R, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)((32 + c->xc) * c->nv), (cuuint32_t)c->R, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const cuuint32_t box_rows[3] = {(cuuint32_t)(32 * c->nv), (cuuint32_t)kRowsR, 1};
     for (int b = 0; b < 2; ++b) {
@@ -1087,10 +658,6 @@ bool make_tensor_maps(bgk_ctx* c) {
 
 void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
     if (c->N_int == 0) return;
-    if (c->d == 2) {                                 // particle sets (k_transport2s)
-        launch_transport2s(c, fin, fout, s);
-        return;
-    }
     TArgs a;
     a.f = fin;
     a.ft = fout;
@@ -1113,6 +680,7 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.dv = c->dv;
     a.dt = c->cfg.dt;
     a.signed_n = c->wls_order == 2;
+    a.xc = c->xc;
     const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
     if (c->rows_built && c->n_rows > 0) {          // fixed-cloud lattice rows + the general kernel on the rest
         launch_transport_rows(c, fin, fout, s);
@@ -1125,8 +693,9 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
         return e ? atoi(e) : 0;
     }();
     // 3D, R = 25: blocks of 2 warps (70.2 vs 70.9 ms on C5 with 128-B rows; profiles/r01_tuning.md)
-    const int wpb = wpb_env ? wpb_env : (c->R == 25 ? 2 : kDefaultWarps);
-    dispatch3(c->R, wpb, tm, a, s);
+    const int wpb = wpb_env ? wpb_env : (c->d == 3 && c->R == 25 ? 2 : kDefaultWarps);
+    if (c->d == 3) dispatch<3>(c->R, wpb, tm, a, s);
+    else dispatch<2>(c->R, wpb, tm, a, s);
 }
 
 
