@@ -132,6 +132,17 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
                 : 0;
     if (c->xc) c->ncg = 1;
     c->nwpp = c->nchunk * c->ncg;
+    // 3D: a last column group of at most 16 columns (e.g. 78-79 columns per rank at P = 8 on C5) runs
+    // folded -- 16 columns x two halves of v_1 in one warp -- instead of a full-width pass with half
+    // the lanes idle (k_transport FD = 1); needs the whole v_1 axis in one chunk and n1 <= 2 kFoldR
+    {
+        const char* e = getenv("BGK_FOLD");
+        const int wl = c->ncol - 32 * (c->ncg - 1);
+        c->fold = (c->d == 3 && c->wls_order == 1 && c->nchunk == 1 && c->n1 <= 2 * kFoldR && wl >= 1 &&
+                   wl <= 16 && !(e && atoi(e) == 0))
+                      ? 1
+                      : 0;
+    }
     c->nslots = c->nwpp * 32;
     // fixed-cloud lattice rows (SURVEY §8(d) "the one lever"): partial slots sized for both mappings
     {
@@ -217,8 +228,10 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     {
-        const char* e = getenv("BGK_BND_G");        // boundary interpolation groups: 4 (default), 8, 0 = per particle
-        c->bnd_g = e ? atoi(e) : 4;
+        // boundary interpolation groups: 8 in 3D / 4 in 2D (default; ring kernel k_bnd_interp_t, C5 2.71 ms
+        // at 8 against 2.91 at 4), or BGK_BND_G = 4, 8, 0 (per particle)
+        const char* e = getenv("BGK_BND_G");
+        c->bnd_g = e ? atoi(e) : (c->d == 3 ? 8 : 4);
         if (c->bnd_g != 4 && c->bnd_g != 8) c->bnd_g = 0;
         c->bu_cap = c->bnd_g ? std::min(c->bnd_g * c->max_nb, 512) : 1;   // union rows per group (CAPACITY beyond)
         const size_t ng = c->bnd_g ? (size_t)N / c->bnd_g + 1 : 1;

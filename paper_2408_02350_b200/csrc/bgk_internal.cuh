@@ -43,6 +43,7 @@ constexpr int kManageMaxNew = 4096;   // new particles (merges + inserts) per pa
 #endif
 constexpr int kRowsG = 8;            // particles per lattice-row group (fixed-cloud transport)
 constexpr int kRowsR = BGK_ROWS_R;   // velocity nodes per lane along v_1 in the lattice-row kernel
+constexpr int kFoldR = 13;           // rows per lane of a folded column group (2 kFoldR >= n1)
 struct Manage {
     uint8_t* flag;      // [Ncap] bit0: merge candidate (a j > i closer than r_merge), bit1: < m_min neighbours
     int32_t* status;    // [Ncap] 0 live, -1 removed (merged into its partner), q+1: slot holds merged particle q
@@ -74,6 +75,8 @@ struct bgk_ctx {
     int xc;                            // 2D, 33 columns: column 32 rides in the group's box (k_transport XC)
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
     CUtensorMap tmap_rows[2];          //   the same with the lattice-row kernel's box {32, kRowsR, 1}
+    CUtensorMap tmap_fold[2];          //   the folded last group's box {16, 2 kFoldR, 1} (fold)
+    int fold;                          // 3D: the last column group (<= 16 columns) runs folded (FD = 1)
     int max_nb;
     int64_t cap;
     int nc[3];

@@ -87,6 +87,52 @@ struct RelaxArgs {
     double vmax, dv, dt, R, kb, dmol, L, clamp_eps;
 };
 
+// rho, U, T from the all-reduced sums (single pass, Z25), tau,
+// the relaxation weights and the Maxwellian's prefactor into par[0 .. 4+D] (par[5..] = U), the
+// recovered macro state, and in ALE mode W <- U and the clamped move x += dt U
+template <int D>
+__device__ __forceinline__ void relax_params(const RelaxArgs& A, int p, double* par) {
+    const double* s = A.sums + (int64_t)p * kPM;
+    double dvd = A.dv * A.dv;
+    if (D == 3) dvd *= A.dv;
+    const double rho = s[0] * dvd;
+    double U[D], uu = 0.0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) { U[a] = s[1 + a] / s[0]; uu += U[a] * U[a]; }
+    const double e3 = s[1 + D] * dvd - rho * uu;          // 3 rho R T
+    const double T = e3 / (3.0 * rho * A.R);
+    bool bad = !(rho > 0.0) || !(T > 1e-12);
+    if (bad) latch_error(A.err, BGK_E_DEGENERATE_STATE, p);
+    const double RT = A.R * T;
+    const double lambda = A.kb / (sqrt(2.0) * kPi * rho * A.R * A.dmol * A.dmol);
+    const double Cbar = sqrt(8.0 * RT / kPi);
+    const double tau = 4.0 * lambda / (kPi * Cbar);
+    const double inv = 1.0 / (tau + A.dt);
+    const double twoPiRT = 2.0 * kPi * RT;
+    const double pref = (D == 3) ? rho / (twoPiRT * sqrt(twoPiRT)) : rho / twoPiRT;
+    par[0] = bad ? 1.0 : tau * inv;   // a1: degenerate rows are left as ftilde
+    par[1] = bad ? 0.0 : A.dt * inv;  // a2
+    par[2] = pref;
+    par[3] = RT;
+    par[4] = 1.0 / (2.0 * RT);
+#pragma unroll
+    for (int a = 0; a < D; ++a) par[5 + a] = U[a];
+    double* mo = A.macro + (int64_t)p * (D + 2);
+    mo[0] = rho;
+#pragma unroll
+    for (int a = 0; a < D; ++a) mo[1 + a] = U[a];
+    mo[1 + D] = T;
+    if (A.ale && !bad) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            A.W[(int64_t)p * D + a] = U[a];
+            double xn = A.x[(int64_t)p * D + a] + A.dt * U[a];
+            xn = fmin(fmax(xn, A.clamp_eps), A.L - A.clamp_eps);
+            A.x[(int64_t)p * D + a] = xn;
+        }
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
     constexpr int NV = (D == 2) ? 2 : 1;
@@ -109,47 +155,7 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
         const int u = threadIdx.x + q * blockDim.x;
         if (u < n2) g[q] = fp2[u];
     }
-    if (threadIdx.x == 0) {
-        const double* s = A.sums + (int64_t)p * kPM;
-        double dvd = A.dv * A.dv;
-        if (D == 3) dvd *= A.dv;
-        const double rho = s[0] * dvd;
-        double U[D], uu = 0.0;
-#pragma unroll
-        for (int a = 0; a < D; ++a) { U[a] = s[1 + a] / s[0]; uu += U[a] * U[a]; }
-        const double e3 = s[1 + D] * dvd - rho * uu;          // 3 rho R T
-        const double T = e3 / (3.0 * rho * A.R);
-        bool bad = !(rho > 0.0) || !(T > 1e-12);
-        if (bad) latch_error(A.err, BGK_E_DEGENERATE_STATE, p);
-        const double RT = A.R * T;
-        const double lambda = A.kb / (sqrt(2.0) * kPi * rho * A.R * A.dmol * A.dmol);
-        const double Cbar = sqrt(8.0 * RT / kPi);
-        const double tau = 4.0 * lambda / (kPi * Cbar);
-        const double inv = 1.0 / (tau + A.dt);
-        const double twoPiRT = 2.0 * kPi * RT;
-        const double pref = (D == 3) ? rho / (twoPiRT * sqrt(twoPiRT)) : rho / twoPiRT;
-        par[0] = bad ? 1.0 : tau * inv;   // a1: degenerate rows are left as ftilde
-        par[1] = bad ? 0.0 : A.dt * inv;  // a2
-        par[2] = pref;
-        par[3] = RT;
-        par[4] = 1.0 / (2.0 * RT);
-#pragma unroll
-        for (int a = 0; a < D; ++a) par[5 + a] = U[a];
-        double* mo = A.macro + (int64_t)p * (D + 2);
-        mo[0] = rho;
-#pragma unroll
-        for (int a = 0; a < D; ++a) mo[1 + a] = U[a];
-        mo[1 + D] = T;
-        if (A.ale && !bad) {
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                A.W[(int64_t)p * D + a] = U[a];
-                double xn = A.x[(int64_t)p * D + a] + A.dt * U[a];
-                xn = fmin(fmax(xn, A.clamp_eps), A.L - A.clamp_eps);
-                A.x[(int64_t)p * D + a] = xn;
-            }
-        }
-    }
+    if (threadIdx.x == 0) relax_params<D>(A, p, par);
     __syncthreads();
     const double inv2RT = par[4];
     for (int t = threadIdx.x; t < D * A.n1; t += blockDim.x) {
@@ -209,6 +215,74 @@ __global__ void __launch_bounds__(256) k_relax(const RelaxArgs A) {
             kr[q] += dk;
             if (cq[q] >= P) {
                 cq[q] -= P;
+                ++kr[q];
+            }
+        }
+    }
+}
+
+// 2D relaxation, one warp per particle: a 2D row is short (C2/C3: 1089 nodes, 17 KB), so a
+// 256-thread block per particle spent its time in the block-wide prologue (moments -> tau, the
+// 2 x (Nv+1) exponentials, three __syncthreads) with one round of loads per thread; here the lanes
+// share the prologue and each streams ~34 (g1, g2) pairs with four loads in flight.
+__global__ void __launch_bounds__(256) k_relax_w2(const RelaxArgs A) {
+    __shared__ double e[8][2][64];
+    __shared__ double par[8][8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t bi = (int64_t)blockIdx.x * 8 + wib;
+    if (bi >= A.n) return;
+    const int p = A.ids[bi];
+    double2* fp2 = reinterpret_cast<double2*>(A.f + (int64_t)p * A.Ks * 2);
+    const int n2 = A.ncs * A.n1;                      // 16-B (g1, g2) pairs of the stored row
+    constexpr int U = 4;
+    double2 g[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const int u = lane + 32 * q;
+        if (u < n2) g[q] = fp2[u];
+    }
+    if (lane == 0) relax_params<2>(A, p, par[wib]);
+    __syncwarp();
+    const double inv2RT = par[wib][4];
+    for (int t = lane; t < 2 * A.n1; t += 32) {
+        const int a = t / A.n1, j = t - a * A.n1;
+        const double dvel = axis_node(A.vmax, A.dv, j) - par[wib][5 + a];
+        e[wib][a][j] = exp(-dvel * dvel * inv2RT);
+    }
+    __syncwarp();
+    const double a1 = par[wib][0], a2 = par[wib][1], pref = par[wib][2], RT = par[wib][3];
+    const double* e0 = e[wib][0];
+    const double* e1 = e[wib][1] + A.c0;
+    // (row, column) of element u = lane + 32 (q + U k) advance incrementally
+    int kr[U], cq[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        const int u = lane + 32 * q;
+        kr[q] = u / A.ncs;
+        cq[q] = u - kr[q] * A.ncs;
+    }
+    const int stride = 32 * U, dk = stride / A.ncs, dc = stride - dk * A.ncs;
+    for (int u0 = lane; u0 < n2; u0 += stride) {
+        if (u0 != lane) {
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int u = u0 + 32 * q;
+                if (u < n2) g[q] = fp2[u];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int u = u0 + 32 * q;
+            if (u < n2) {
+                const double M = pref * e0[kr[q]] * e1[cq[q]];
+                g[q].x = a1 * g[q].x + a2 * M;
+                g[q].y = a1 * g[q].y + a2 * (RT * M);
+                fp2[u] = g[q];
+            }
+            cq[q] += dc;
+            kr[q] += dk;
+            if (cq[q] >= A.ncs) {
+                cq[q] -= A.ncs;
                 ++kr[q];
             }
         }
@@ -882,6 +956,7 @@ void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
     a.clamp_eps = 1e-3 * c->cfg.dx;
     const size_t smem = sizeof(double) * c->ncs;   // column factors of the separable Maxwellian
     if (c->d == 3) k_relax<3><<<(unsigned)c->N_int, 256, smem, s>>>(a);
+    else if (c->n1 <= 64) k_relax_w2<<<(unsigned)((c->N_int + 7) / 8), 256, 0, s>>>(a);
     else k_relax<2><<<(unsigned)c->N_int, 256, smem, s>>>(a);
 }
 

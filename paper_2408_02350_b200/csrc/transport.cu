@@ -60,6 +60,8 @@ struct TArgs {
     int nw_grid;                        // (chunk x column group) items of this launch
     double vmax, dv, dt;
     int xc;                             // 2D, 33 columns: the box carries column 32 too (Stage XC)
+    int ncg_l;                          // column groups in this launch (the grid's y = chunk x group)
+    int cg_fold;                        // FD launch: the folded (last) column group
 };
 
 // min(t, 0) without the fp64 pipe: the high word's sign decides, min(hi, 0) on the integer
@@ -191,23 +193,29 @@ __device__ __forceinline__ void transport_epilogue(const TArgs& A, int p, int w,
 // and C's n-term is y_n + s_n |y_n| (abar may be negative; P:408-410 applied literally).
 // XC = 1 (2D, 33 columns): the box also carries the column after the group (33 columns), whose R
 // nodes of the chunk lanes 0..R-1 update one each (no separate tail kernel).
-template <int D, int R, bool SG = false, int XC = 0>
+// FD = 1 (3D, a last column group of <= 16 columns): the warp folds its 32 lanes onto 16 columns x
+// two halves of the v_1 axis (lane l: column l & 15, rows (l >> 4) R .. + R), the box is 16 columns
+// x 2R rows (rows past N_v zero-filled by the TMA unit) -- the group costs one R-row pass instead of
+// a full-width pass with half the lanes idle (multi-GPU column shards).
+template <int D, int R, bool SG = false, int XC = 0, int FD = 0>
 struct Stage {
     static constexpr int NV = (D == 2) ? 2 : 1;
     static constexpr int PD0 = (D == 2) ? 4 : 10;
     static constexpr int PD = SG ? PD0 + 2 : PD0;
-    static constexpr int ROW = (32 + XC) * NV;                           // doubles per staged row
-    static constexpr uint32_t F_BYTES = R * ROW * sizeof(double);
+    static constexpr int ROW = FD ? 16 * NV : (32 + XC) * NV;            // doubles per staged row
+    static constexpr int ROWS = FD ? 2 * R : R;                          // staged rows
+    static constexpr uint32_t F_BYTES = ROWS * ROW * sizeof(double);
     static constexpr uint32_t P_BYTES = PD * sizeof(double);
     static constexpr uint32_t BYTES = (F_BYTES + P_BYTES + 127) / 128 * 128;
 };
 
-template <int D, int R, int NST, int WPB, bool SG, int XC = 0>
+template <int D, int R, int NST, int WPB, bool SG, int XC = 0, int FD = 0>
 // minBlocks = 1 is explicit on purpose: with __launch_bounds__(64) alone ptxas capped the R = 25
 // instantiation at 164 registers (229 with it) and C5 transport went from 69 to 93 ms.
 __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
     static_assert(XC == 0 || (D == 2 && !SG && R <= 32), "extra column: 2D first order, one row per lane");
-    using St = Stage<D, R, SG, XC>;
+    static_assert(FD == 0 || (D == 3 && !SG && XC == 0), "folded group: 3D first order");
+    using St = Stage<D, R, SG, XC, FD>;
     constexpr int NV = St::NV;
     constexpr int PD = St::PD;
     constexpr int ROW = St::ROW;
@@ -229,14 +237,16 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
     // indexing below keeps the running stage offset g0 so items could be chained.)
     const uint32_t g0 = 0;
     {
-    const int w = blockIdx.y;
     const int64_t pos = (int64_t)blockIdx.x * WPB + wib;
     if (pos >= A.n_int) return;                           // warp-uniform
-    const int chunk = w / A.ncg, cg = w - chunk * A.ncg;
+    const int chunk = FD ? 0 : (int)blockIdx.y / A.ncg_l;
+    const int cg = FD ? A.cg_fold : (int)blockIdx.y - chunk * A.ncg_l;
+    const int w = chunk * A.ncg + cg;                     // partial slot of (chunk, group)
     const int p = A.order[pos];
-    const int col = cg * 32 + lane;
+    const int cl = FD ? (lane & 15) : lane;               // column within the group
+    const int col = cg * 32 + cl;
     const bool valid = col < A.ncol;
-    const int k1s = chunk * R;
+    const int k1s = FD ? (lane >> 4) * R : chunk * R;     // FD: the lane's half of the v_1 axis
     const int colc = valid ? col : 0;
     const int gc = A.c0 + colc;
     const int64_t off = A.nb_off[p];
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
         const int s = (int)((g0 + (uint32_t)e) % NST);
         unsigned char* st = ring + s * St::BYTES;
         mbar_expect_tx(bars + s, St::F_BYTES + St::P_BYTES);
-        tma_load_3d(st, &tmap, cg * 32 * NV, k1s, jn, bars + s);
+        tma_load_3d(st, &tmap, cg * 32 * NV, FD ? 0 : k1s, jn, bars + s);
         bulk_load(st + St::F_BYTES, Pp + (int64_t)e * PD, St::P_BYTES, bars + s);
     };
 #pragma unroll
@@ -316,7 +326,8 @@ __global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant
         const uint32_t ge = g0 + (uint32_t)e;
         const bool more = e + 1 < m;
         const uint32_t nready = more ? mbar_test(bars + (ge + 1) % NST, ((ge + 1) / NST) & 1u) : 1u;
-        const double* st = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) + lane * NV;
+        const double* st = reinterpret_cast<const double*>(ring + (ge % NST) * St::BYTES) +
+                           (FD ? ((lane >> 4) * R * ROW + cl) : lane * NV);
         // y_e and L advance by one add per node along v_1 (all DADD: measured ~2 % faster than
         // the independent-FMA form y_e(r) = fma(r, dy_e, y_e(0)))
         if constexpr (SG) {
@@ -533,26 +544,27 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
         transport_epilogue<3, R, false>(A, p0 + k * S, w, k1s, colc, gc, valid, Qf[k], Sc, Sa, Qt);
 }
 
-template <int D, int R, int WPB, bool SG, int XC = 0>
+template <int D, int R, int WPB, bool SG, int XC = 0, int FD = 0>
 constexpr int stages_for() {
     // ring depth: keep NST-1 neighbour boxes in flight; bounded by 227 KB of shared memory
     // (sized for 8 resident warps per SM: blocks of WPB warps)
     constexpr int blocks = WPB >= 8 ? 1 : 8 / WPB;
-    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R, SG, XC>::BYTES);
+    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R, SG, XC, FD>::BYTES);
     return n > 8 ? 8 : (n < 2 ? 2 : n);
 }
 
-template <int D, int R, int WPB, bool SG = false, int XC = 0>
+template <int D, int R, int WPB, bool SG = false, int XC = 0, int FD = 0>
 void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int NST = stages_for<D, R, WPB, SG, XC>();
-    constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG, XC>::BYTES + WPB * NST * 8;
+    constexpr int NST = stages_for<D, R, WPB, SG, XC, FD>();
+    constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG, XC, FD>::BYTES + WPB * NST * 8;
     static bool configured[kMaxDevices] = {};
     if (first_use_on_device(configured)) {
-        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, XC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, XC, FD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     }
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
-    k_transport<D, R, NST, WPB, SG, XC><<<dim3(gx, (unsigned)a.nw_grid), WPB * 32, smem, s>>>(tm, a);
+    const unsigned gy = FD ? 1u : (unsigned)a.nw_grid;
+    k_transport<D, R, NST, WPB, SG, XC, FD><<<dim3(gx, gy), WPB * 32, smem, s>>>(tm, a);
 }
 
 template <int D, int R>
@@ -646,6 +658,13 @@ bool make_tensor_maps(bgk_ctx* c) {
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return false;
+        if (c->fold) {
+            const cuuint32_t box_fold[3] = {16, (cuuint32_t)(2 * kFoldR), 1};
+            r = encode(&c->tmap_fold[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->f[b], dims, strides, box_fold, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return false;
+        }
         if (c->rows_on) {
             r = encode(&c->tmap_rows[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->f[b], dims, strides, box_rows, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -681,6 +700,8 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.dt = c->cfg.dt;
     a.signed_n = c->wls_order == 2;
     a.xc = c->xc;
+    a.ncg_l = c->ncg;
+    a.cg_fold = 0;
     const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
     if (c->rows_built && c->n_rows > 0) {          // fixed-cloud lattice rows + the general kernel on the rest
         launch_transport_rows(c, fin, fout, s);
@@ -694,6 +715,15 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     }();
     // 3D, R = 25: blocks of 2 warps (70.2 vs 70.9 ms on C5 with 128-B rows; profiles/r01_tuning.md)
     const int wpb = wpb_env ? wpb_env : (c->d == 3 && c->R == 25 ? 2 : kDefaultWarps);
+    if (c->d == 3 && c->fold) {                     // full groups at R, the narrow last group folded
+        TArgs b = a;
+        b.ncg_l = c->ncg - 1;
+        b.nw_grid = c->nchunk * b.ncg_l;
+        if (b.ncg_l > 0) dispatch<3>(c->R, wpb, tm, b, s);
+        b.cg_fold = c->ncg - 1;
+        launch_one<3, kFoldR, kDefaultWarps, false, 0, 1>(c->tmap_fold[fin == c->f[0] ? 0 : 1], b, s);
+        return;
+    }
     if (c->d == 3) dispatch<3>(c->R, wpb, tm, a, s);
     else dispatch<2>(c->R, wpb, tm, a, s);
 }

@@ -168,7 +168,8 @@ def test_stable_dt(torch_cuda):
 
 
 # --------------------------------------------- velocity sharding on one device
-@pytest.mark.parametrize("cfg,P", [(bi.C1, 3), (bi.CavityConfig("C4s", 3, 12, 8), 4)])
+@pytest.mark.parametrize("cfg,P", [(bi.C1, 3), (bi.CavityConfig("C4s", 3, 12, 8), 4),
+                                   (bi.CavityConfig("C5s8", 3, 8, 24), 8)])   # 78/79 columns: folded last group
 def test_column_sharded_step_matches(torch_cuda, cfg, P):
     """P contexts, each owning a column shard, exchanging only the two summed buffers
     (what the NCCL all-reduce does across GPUs) reproduce the single-context run."""
