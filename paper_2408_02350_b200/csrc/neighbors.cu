@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) k_compact_write(const int32_t* __restrict
 }
 
 
-template <int D, bool FILL>
+template <int D, bool FILL, bool PAD = false>
 __global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, const int32_t* __restrict__ cell_of,
                             const int32_t* __restrict__ cell_start, const int32_t* __restrict__ cell_pts, int nc0,
                             int nc1, int nc2, int max_nb, int32_t* __restrict__ nb_cnt,
@@ -281,22 +281,36 @@ __global__ void k_neighbors(const double* __restrict__ x, int64_t N, double h2, 
             }
         }
     }
-    if (!FILL) {
+    if (!FILL || PAD) {
         if (lane == 0) {            // an overflowing list is left empty: no later kernel reads
             nb_cnt[i] = m > max_nb ? 0 : m;   // past the per-particle capacity (error latched)
             if (m > max_nb) latch_error(err, BGK_E_CAPACITY, i);
         }
-        return;
+        if (!FILL) return;
     }
     __syncwarp();
-    const int64_t off = nb_off[i];
-    if (m > max_nb || off + m > cap) return;  // capacity error already latched / reported by host
+    // PAD: the sorted list goes to row i of a padded scratch [N][max_nb] (nb_idx is the scratch),
+    // compacted into the CSR by k_nb_compact after the scan -- one distance sweep instead of two
+    const int64_t off = PAD ? i * (int64_t)max_nb : nb_off[i];
+    if (m > max_nb || (!PAD && off + m > cap)) return;   // capacity error already latched / reported
     for (int q = lane; q < m; q += 32) {      // rank sort: lists are short (< max_nb)
         const int v = buf[q];
         int rank = 0;
         for (int r = 0; r < m; ++r) rank += (buf[r] < v);
         nb_idx[off + rank] = v;
     }
+}
+
+// padded scratch rows -> CSR (warp per particle, coalesced copies)
+__global__ void k_nb_compact(const int32_t* __restrict__ pad, int64_t N, int max_nb,
+                             const int32_t* __restrict__ nb_cnt, const int64_t* __restrict__ nb_off,
+                             int32_t* __restrict__ nb_idx) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= N) return;
+    const int m = nb_cnt[i];
+    const int64_t off = nb_off[i];
+    for (int q = lane; q < m; q += 32) nb_idx[off + q] = pad[i * (int64_t)max_nb + q];
 }
 
 }  // namespace
@@ -328,23 +342,19 @@ void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
     const int wpb = 8;
     const unsigned nbw = (unsigned)((N + wpb - 1) / wpb);
     const size_t smem = sizeof(int32_t) * wpb * c->max_nb;
-    if (c->d == 3) {
-        k_neighbors<3, false><<<nbw, wpb * 32, 0, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
-                                                      c->g.cell_pts, c->nc[0], c->nc[1], c->nc[2], c->max_nb,
-                                                      c->g.nb_cnt, nullptr, nullptr, c->cap, c->err);
-        scan_counts(c, c->g.nb_cnt, c->g.nb_off, N, s);
-        k_neighbors<3, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
-                                                        c->g.cell_pts, c->nc[0], c->nc[1], c->nc[2], c->max_nb,
-                                                        c->g.nb_cnt, c->g.nb_off, c->g.nb_idx, c->cap, c->err);
-    } else {
-        k_neighbors<2, false><<<nbw, wpb * 32, 0, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
-                                                      c->g.cell_pts, c->nc[0], c->nc[1], 1, c->max_nb,
-                                                      c->g.nb_cnt, nullptr, nullptr, c->cap, c->err);
-        scan_counts(c, c->g.nb_cnt, c->g.nb_off, N, s);
-        k_neighbors<2, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
-                                                        c->g.cell_pts, c->nc[0], c->nc[1], 1, c->max_nb,
-                                                        c->g.nb_cnt, c->g.nb_off, c->g.nb_idx, c->cap, c->err);
-    }
+    // one distance sweep: sorted lists into a padded scratch (the WLS pair-record array, rewritten
+    // after the neighbours), counts, scan, compaction into the CSR
+    int32_t* pad = reinterpret_cast<int32_t*>(c->g.P);
+    if (c->d == 3)
+        k_neighbors<3, true, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
+                                                              c->g.cell_pts, c->nc[0], c->nc[1], c->nc[2], c->max_nb,
+                                                              c->g.nb_cnt, nullptr, pad, c->cap, c->err);
+    else
+        k_neighbors<2, true, true><<<nbw, wpb * 32, smem, s>>>(c->x, N, c->cfg.h2, c->g.cell_of, c->g.cell_start,
+                                                              c->g.cell_pts, c->nc[0], c->nc[1], 1, c->max_nb,
+                                                              c->g.nb_cnt, nullptr, pad, c->cap, c->err);
+    scan_counts(c, c->g.nb_cnt, c->g.nb_off, N, s);
+    k_nb_compact<<<nbw, wpb * 32, 0, s>>>(pad, N, c->max_nb, c->g.nb_cnt, c->g.nb_off, c->g.nb_idx);
 }
 
 }  // namespace bgk

@@ -675,8 +675,8 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp_u(const int32_t* __res
 // members (dense G-column weights).  A chunk with no incoming node for any member (walls normal to
 // v_1: half the rows) only writes zero flux partials.
 // ---------------------------------------------------------------------------------------------
-template <int D, int G, int NPT, int NS>
-__global__ void __launch_bounds__(256) k_bnd_interp_t(const int32_t* __restrict__ bids, int64_t nb,
+template <int D, int G, int NPT, int NS, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_bnd_interp_t(const int32_t* __restrict__ bids, int64_t nb,
                                                       const int8_t* __restrict__ kind,
                                                       const int32_t* __restrict__ bu_j,
                                                       const double* __restrict__ bu_w,
@@ -988,18 +988,19 @@ void bnd_interp_g(bgk_ctx* c, double* fnew, cudaStream_t s) {
                                                      c->c0, c->Ks, c->cfg.vmax, c->dv);
 }
 
-template <int D, int G>
+template <int D, int G, int NPT, int NS, int MINB = 2>
 void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
-    constexpr int NPT = D == 3 ? 4 : 2, NS = 6, CH = 256 * NPT;
+    constexpr int CH = 256 * NPT;
     constexpr int NV = D == 2 ? 2 : 1;
     const size_t smem = (size_t)NS * CH * NV * sizeof(double) + 2 * NS * sizeof(uint64_t) +
                         (size_t)c->bu_cap * (G * sizeof(double) + sizeof(int32_t));
     static bool configured[kMaxDevices] = {};
     if (first_use_on_device(configured))
-        cudaFuncSetAttribute(k_bnd_interp_t<D, G, NPT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_bnd_interp_t<D, G, NPT, NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
     const int nch = (int)((c->Ks + CH - 1) / CH);
     dim3 gg((unsigned)((c->N_b + G - 1) / G), (unsigned)nch);
-    k_bnd_interp_t<D, G, NPT, NS><<<gg, 256, smem, s>>>(c->boundary, c->N_b, c->kind, c->bu_j, c->bu_w, c->bu_n,
+    k_bnd_interp_t<D, G, NPT, NS, MINB><<<gg, 256, smem, s>>>(c->boundary, c->N_b, c->kind, c->bu_j, c->bu_w, c->bu_n,
                                                         c->bu_cap, fnew, c->wallpart, nch, c->n1, c->ncol, c->ncs,
                                                         c->c0, c->Ks, c->cfg.vmax, c->dv);
     k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart, nch,
@@ -1012,9 +1013,18 @@ void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
         const char* e = getenv("BGK_BND_RING");        // 0: the __ldg union kernel (k_bnd_interp_u)
         return !(e && atoi(e) == 0);
     }();
+    static const int var = [] {
+        const char* e = getenv("BGK_BND_VAR");        // tuning: 1 = 3D with 2 nodes per thread, 8 stages
+        return e ? atoi(e) : 0;
+    }();
     if (c->bnd_g && ring) {
-        if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_t<3, 4>(c, fnew, s) : bnd_interp_t<3, 8>(c, fnew, s));
-        else (c->bnd_g == 4 ? bnd_interp_t<2, 4>(c, fnew, s) : bnd_interp_t<2, 8>(c, fnew, s));
+        if (c->d == 3) {
+            if (var == 1) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 2, 8, 3>(c, fnew, s) : bnd_interp_t<3, 8, 2, 8, 3>(c, fnew, s));
+            else if (var == 2) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 4, 3>(c, fnew, s) : bnd_interp_t<3, 8, 4, 4, 3>(c, fnew, s));
+            else (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
+        } else {
+            (c->bnd_g == 4 ? bnd_interp_t<2, 4, 2, 6>(c, fnew, s) : bnd_interp_t<2, 8, 2, 6>(c, fnew, s));
+        }
         return;
     }
     if (c->bnd_g) {
