@@ -135,7 +135,8 @@ struct bgk_ctx {
     // whole-step CUDA graphs (graph.cu): one executable per buffer parity, rebuilt when the key changes
     bool graph_ok;                 // graphs usable (BGK_GRAPH != 0, conditional nodes available)
     int eager_steps;               // steps run eagerly since the last key change (capture after one)
-    cudaStream_t cap_stream, cap_stream2;   // private capture streams (step, conditional bodies)
+    cudaStream_t cap_stream, cap_stream2, cap_stream3;   // private capture streams (step, bodies, fork)
+    cudaEvent_t cap_fork, cap_join;    // fork / join of the boundary half of the WLS inside a capture
     cudaStream_t gstream;          // stream of the last graph launch (reconcile of stream-less calls)
     uint64_t eager_key;            // key of the last eager step
     int force_eager;               // steps that must run eagerly (a management change to apply)
@@ -219,6 +220,8 @@ inline bool first_use_on_device(bool (&done)[kMaxDevices]) {
 void launch_build_neighbors(bgk_ctx* c, cudaStream_t s);
 void launch_wls(bgk_ctx* c, cudaStream_t s);
 void launch_wls_export(bgk_ctx* c, double* rot, double* frames, cudaStream_t s);
+void launch_wls_interior(bgk_ctx* c, cudaStream_t s);
+void launch_wls_boundary(bgk_ctx* c, cudaStream_t s);
 void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_moment_reduce(bgk_ctx* c, cudaStream_t s);
 void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s);
@@ -243,7 +246,7 @@ __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int
     const int64_t k1 = t / ncol;
     return k1 * ncs + (t - k1 * ncol);
 }
-int launches_neighbors();
+int launches_neighbors(const bgk_ctx* c);
 int launches_wls();
 // particle management: one pass (synchronises the stream); *changed = N or indices changed.
 // manage_decide enqueues detect + decide only (device report mg.rep, rep[7] = changed);

@@ -74,10 +74,17 @@ bool graph_enabled() {
 
 namespace {
 
-// the part of ensure_geometry after neighbours and management (ALE: every step)
+// the part of ensure_geometry after neighbours and management (ALE: every step).  The boundary
+// half of the WLS and the interpolation unions (k_wls_boundary -> k_bnd_union, small single-wave
+// kernels) run on a forked branch beside the interior WLS: they write disjoint rows.
 void geometry_tail(bgk_ctx* c, cudaStream_t s) {
-    launch_wls(c, s);
-    launch_bnd_union(c, s);
+    cudaEventRecord(c->cap_fork, s);
+    cudaStreamWaitEvent(c->cap_stream3, c->cap_fork, 0);
+    launch_wls_boundary(c, c->cap_stream3);
+    launch_bnd_union(c, c->cap_stream3);
+    launch_wls_interior(c, s);
+    cudaEventRecord(c->cap_join, c->cap_stream3);
+    cudaStreamWaitEvent(s, c->cap_join, 0);
 }
 
 // transport .. boundary fill with the current parity (fcur is flipped by the caller)
@@ -122,6 +129,9 @@ bool capture(bgk_ctx* c, int slot) {
     if (!c->cap_stream) {
         if (cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) return false;
         if (cudaStreamCreateWithFlags(&c->cap_stream2, cudaStreamNonBlocking) != cudaSuccess) return false;
+        if (cudaStreamCreateWithFlags(&c->cap_stream3, cudaStreamNonBlocking) != cudaSuccess) return false;
+        if (cudaEventCreateWithFlags(&c->cap_fork, cudaEventDisableTiming) != cudaSuccess) return false;
+        if (cudaEventCreateWithFlags(&c->cap_join, cudaEventDisableTiming) != cudaSuccess) return false;
     }
     cudaStream_t cs = c->cap_stream, bs = c->cap_stream2;
     const bool managed = c->cfg.manage && c->cfg.ale;
@@ -255,6 +265,9 @@ void graph_release(bgk_ctx* c) {
         if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->cap_stream2) cudaStreamDestroy(c->cap_stream2);
+    if (c->cap_stream3) cudaStreamDestroy(c->cap_stream3);
+    if (c->cap_fork) cudaEventDestroy(c->cap_fork);
+    if (c->cap_join) cudaEventDestroy(c->cap_join);
 }
 
 }  // namespace bgk

@@ -177,6 +177,10 @@ __global__ void __launch_bounds__(256) k_bscan(const int32_t* __restrict__ in, i
 }
 
 void scan_counts(bgk_ctx* c, const int32_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+    if (n <= 32768) {                    // small clouds (2D workloads): one block, one launch
+        k_scan<int64_t><<<1, kScanThreads, 0, s>>>(in, out, n);
+        return;
+    }
     const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(1000, (n + 2047) / 2048));
     const int64_t chunk = (n + nblk - 1) / nblk;
     k_bsum<<<(unsigned)nblk, 256, 0, s>>>(in, n, chunk, c->blk_tmp);
@@ -315,7 +319,7 @@ __global__ void k_nb_compact(const int32_t* __restrict__ pad, int64_t N, int max
 
 }  // namespace
 
-int launches_neighbors() { return 12; }
+int launches_neighbors(const bgk_ctx* c) { return c->N <= 32768 ? 10 : 12; }   // scan: 1 or 3 kernels
 
 void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
     const int64_t N = c->N;
@@ -333,7 +337,7 @@ void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
     k_cell_fill<<<nb, tpb, 0, s>>>(N, c->g.cell_of, c->g.cell_start, c->g.cell_fill, c->g.cell_pts);
     k_cell_sort<<<(c->ncell + 3) / 4, 128, 0, s>>>(c->ncell, c->g.cell_start, c->g.cell_pts);
     {
-        const int64_t nblk = std::min<int64_t>(1000, (N + 2047) / 2048);
+        const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(1000, (N + 255) / 256));   // 256 ids per block
         const int64_t chunk = (N + nblk - 1) / nblk;
         k_compact_count<<<(unsigned)nblk, 256, 0, s>>>(c->g.cell_pts, c->kind, N, chunk, c->g.nb_cnt);
         k_scan<int64_t><<<1, kScanThreads, 0, s>>>(c->g.nb_cnt, c->scan_tmp, nblk);

@@ -1013,15 +1013,9 @@ void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
         const char* e = getenv("BGK_BND_RING");        // 0: the __ldg union kernel (k_bnd_interp_u)
         return !(e && atoi(e) == 0);
     }();
-    static const int var = [] {
-        const char* e = getenv("BGK_BND_VAR");        // tuning: 1 = 3D with 2 nodes per thread, 8 stages
-        return e ? atoi(e) : 0;
-    }();
     if (c->bnd_g && ring) {
         if (c->d == 3) {
-            if (var == 1) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 2, 8, 3>(c, fnew, s) : bnd_interp_t<3, 8, 2, 8, 3>(c, fnew, s));
-            else if (var == 2) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 4, 3>(c, fnew, s) : bnd_interp_t<3, 8, 4, 4, 3>(c, fnew, s));
-            else (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
+            (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
         } else {
             (c->bnd_g == 4 ? bnd_interp_t<2, 4, 2, 6>(c, fnew, s) : bnd_interp_t<2, 8, 2, 6>(c, fnew, s));
         }

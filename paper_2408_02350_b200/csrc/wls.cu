@@ -300,6 +300,28 @@ static void run_wls(bgk_ctx* c, double* rot, double* frames, cudaStream_t s) {
 
 void launch_wls(bgk_ctx* c, cudaStream_t s) { run_wls(c, nullptr, nullptr, s); }
 
+// the two halves of launch_wls on separate streams (graph.cu forks them: they write disjoint rows)
+void launch_wls_interior(bgk_ctx* c, cudaStream_t s) {
+    const int wpb = 4;
+    const unsigned gi = (unsigned)((c->N_int + wpb - 1) / wpb);
+    if (!gi) return;
+    if (c->d == 3) launch_interior<3>(c, gi, wpb, nullptr, nullptr, s);
+    else launch_interior<2>(c, gi, wpb, nullptr, nullptr, s);
+}
+
+void launch_wls_boundary(bgk_ctx* c, cudaStream_t s) {
+    const int wpb = 4;
+    const unsigned gb = (unsigned)((c->N_b + wpb - 1) / wpb);
+    if (!gb) return;
+    const double h = c->cfg.h, h2 = c->cfg.h2, al = c->cfg.alpha_w;
+    if (c->d == 3)
+        k_wls_boundary<3><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h, h2,
+                                                 al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
+    else
+        k_wls_boundary<2><<<gb, wpb * 32, 0, s>>>(c->x, c->kind, c->boundary, c->N_b, c->g.nb_off, c->g.nb_idx, h, h2,
+                                                 al, c->g.cw, c->g.bidx, c->g.bcw, c->g.bcnt, c->err);
+}
+
 void launch_wls_export(bgk_ctx* c, double* rot, double* frames, cudaStream_t s) { run_wls(c, rot, frames, s); }
 
 }  // namespace bgk
