@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __restrict
     const int64_t b = t * chunk, e = min(n, b + chunk);
     int64_t local = 0;
     for (int64_t i = b; i < e; ++i) local += in[i];
+    __syncwarp();                    // reconverge after the data-dependent loop before the shuffles
     // block exclusive scan of `local`
     const int lane = t & 31, wid = t >> 5;
     int64_t v = local;

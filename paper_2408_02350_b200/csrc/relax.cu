@@ -667,9 +667,10 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_interp_u(const int32_t* __res
 // ---------------------------------------------------------------------------------------------
 // Boundary interpolation with the union rows staged by bulk copies (k_bnd_interp_t).  Block =
 // (group of G face-consecutive boundary particles, chunk of 256*NPT stored nodes).  The group's
-// union rows (k_bnd_union) stream through an NS-deep shared-memory ring: one contiguous
-// cp.async.bulk per (row, chunk) on a "full" mbarrier, released by every warp on an "empty"
-// mbarrier before thread 0 refills it NS rows ahead -- the row traffic is in flight asynchronously
+// union rows (k_bnd_union) stream through an NS-deep shared-memory ring, one contiguous
+// cp.async.bulk per (row, chunk) on a "full" mbarrier; the ring is refilled half by half: after
+// the block has consumed the NS/2 rows of one half (__syncthreads), thread 0 issues the next NS/2
+// rows into it while the other half is applied -- the row traffic is in flight asynchronously
 // instead of waiting on each thread's loads (the __ldg form of k_bnd_interp_u sat at ~4 TB/s of
 // useful L2 traffic, latency-bound).  Each thread applies a staged row to its NPT nodes for all G
 // members (dense G-column weights).  A chunk with no incoming node for any member (walls normal to
@@ -689,13 +690,14 @@ __global__ void __launch_bounds__(256, MINB) k_bnd_interp_t(const int32_t* __res
     constexpr uint32_t SB = CH * NV * sizeof(double);         // bytes per ring stage
     extern __shared__ __align__(128) unsigned char sm[];
     double* ring = reinterpret_cast<double*>(sm);
+    static_assert(NS % 2 == 0, "the ring is refilled half by half");
+    constexpr int NH = NS / 2;
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * SB);
-    uint64_t* empty = full + NS;
-    double* sW = reinterpret_cast<double*>(empty + NS);       // [U][G]
+    double* sW = reinterpret_cast<double*>(full + 2 * NS);    // [U][G] (2 NS words reserved)
     int32_t* sJ = reinterpret_cast<int32_t*>(sW + (size_t)cap * G);
     __shared__ double sh[32];
     const int64_t g = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const int U = bu_n[g];
     int b[G], axis[G];
     bool live[G];
@@ -732,10 +734,7 @@ __global__ void __launch_bounds__(256, MINB) k_bnd_interp_t(const int32_t* __res
     for (int i = tid; i < U; i += blockDim.x) sJ[i] = bu_j[g * cap + i];
     if (tid == 0) {
 #pragma unroll
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(empty + s, 256 / 32);
-        }
+        for (int s = 0; s < NS; ++s) mbar_init(full + s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -781,11 +780,10 @@ __global__ void __launch_bounds__(256, MINB) k_bnd_interp_t(const int32_t* __res
 #pragma unroll
                 for (int c = 0; c < NV; ++c) acc[q][n][c] = fma(w, fv[n][c], acc[q][n][c]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);                // this warp is done with stage s
-        if (tid == 0 && u + NS < U) {
-            mbar_wait(empty + s, ph);
-            issue(u + NS);
+        if (u % NH == NH - 1 && u + 1 < U) {                  // a half consumed by every warp:
+            __syncthreads();                                  // refill it NS rows ahead
+            if (tid == 0)
+                for (int q = u + 1 - NH + NS; q <= u + NS && q < U; ++q) issue(q);
         }
     }
 #pragma unroll
