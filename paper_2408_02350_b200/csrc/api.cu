@@ -154,10 +154,8 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
         if (c->rows_on) c->nwpp = std::max(c->nchunk, c->rows_nchunk) * c->ncg;
     }
     c->bnd_chunk = 256;
-#ifndef BGK_BND_NPT
-#define BGK_BND_NPT 2
-#endif
-    c->bnd_nch = (int)((c->Ks + 256 * BGK_BND_NPT - 1) / (256 * BGK_BND_NPT));   // k_bnd_interp: 256 threads x NPT nodes
+    // k_bnd_interp_t chunks: 256 threads x NPT stored nodes (NPT = 4 in 3D, 2 in 2D)
+    c->bnd_nch = (int)((c->Ks + 256 * (c->d == 3 ? 4 : 2) - 1) / (256 * (c->d == 3 ? 4 : 2)));
 }
 
 // particle-management scratch (only when cfg.manage): decision arrays over the capacity, the
@@ -228,15 +226,15 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     {
-        // boundary interpolation groups: 8 in 3D / 4 in 2D (default; ring kernel k_bnd_interp_t, C5 2.71 ms
-        // at 8 against 2.91 at 4), or BGK_BND_G = 4, 8, 0 (per particle)
+        // boundary interpolation groups: 8 in 3D / 4 in 2D (ring kernel k_bnd_interp_t, C5 2.46 ms at 8
+        // against 2.91 at 4), or BGK_BND_G = 4 / 8
         const char* e = getenv("BGK_BND_G");
         c->bnd_g = e ? atoi(e) : (c->d == 3 ? 8 : 4);
-        if (c->bnd_g != 4 && c->bnd_g != 8) c->bnd_g = 0;
-        c->bu_cap = c->bnd_g ? std::min(c->bnd_g * c->max_nb, 512) : 1;   // union rows per group (CAPACITY beyond)
-        const size_t ng = c->bnd_g ? (size_t)N / c->bnd_g + 1 : 1;
+        if (c->bnd_g != 4 && c->bnd_g != 8) c->bnd_g = c->d == 3 ? 8 : 4;
+        c->bu_cap = std::min(c->bnd_g * c->max_nb, 512);   // union rows per group (CAPACITY beyond)
+        const size_t ng = (size_t)N / c->bnd_g + 1;
         c->bu_j = k.take<int32_t>(ng * c->bu_cap);
-        c->bu_w = k.take<double>(ng * c->bu_cap * std::max(c->bnd_g, 1));
+        c->bu_w = k.take<double>(ng * c->bu_cap * c->bnd_g);
         c->bu_n = k.take<int32_t>(ng);
     }
     c->rows_p0 = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
@@ -693,7 +691,7 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
     if (!c || !n) return BGK_E_INVALID_ARG;
     int64_t k = 0;
     if (c->cfg.ale) k += launches_neighbors(c) + launches_wls() - (c->N_b ? 0 : 1) - (c->N_int ? 0 : 1);
-    if (c->cfg.ale && c->N_b && c->bnd_g) k += 1;   // k_bnd_union
+    if (c->cfg.ale && c->N_b) k += 1;   // k_bnd_union
     if (c->cfg.ale && c->cfg.manage) k += 2;   // k_mg_detect_w + k_mg_decide (plus 3 more and a neighbour
                                                // rebuild in the rare steps where the cloud changes)
     if (c->cfg.ale && c->cfg.manage && c->graph_ok && c->ncol == c->ncol_g)

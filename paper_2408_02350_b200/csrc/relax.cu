@@ -387,96 +387,13 @@ __global__ void __launch_bounds__(256) k_wall_den(double* __restrict__ den, int 
 
 constexpr int kBndChunk = 256;
 
-// Block = (group of kBndGroup consecutive boundary particles of the face-sorted list, chunk of
-// 256 stored nodes).  Neighbouring boundary particles share most interior neighbours, so the
-// rows loaded for one particle of the group are L1 hits for the next.
-constexpr int kBndGroup = 8;
-#ifndef BGK_BND_NPT
-#define BGK_BND_NPT 2
-#endif
-#ifndef BGK_BND_UNROLL
-#define BGK_BND_UNROLL 4
-#endif
-constexpr int kBndNPT = BGK_BND_NPT;   // nodes per thread in k_bnd_interp
-constexpr int kBndUnroll = BGK_BND_UNROLL;   // interior neighbours in flight per thread
-
-template <int D>
-__global__ void __launch_bounds__(kBndChunk) k_bnd_interp(const int32_t* __restrict__ bids, int64_t nb,
-                                                          const int8_t* __restrict__ kind,
-                                                          const int64_t* __restrict__ nb_off,
-                                                          const int32_t* __restrict__ bidx,
-                                                          const double* __restrict__ bcw,
-                                                          const int32_t* __restrict__ bcnt, double* __restrict__ f,
-                                                          double* __restrict__ wallpart, int nch, int n1, int ncol,
-                                                          int ncs, int c0, int64_t Kloc, double vmax, double dv) {
-    // Kloc here is the STORED node count per row (n1 * ncs).  Each thread owns kBndNPT nodes of
-    // the block's chunk (independent load/FMA streams for memory-level parallelism).
-    constexpr int NV = (D == 2) ? 2 : 1;
-    __shared__ double sh[32];
-    int64_t t[kBndNPT];
-    double v[kBndNPT][3];
-    bool in_range[kBndNPT];
-#pragma unroll
-    for (int q = 0; q < kBndNPT; ++q) {
-        t[q] = (int64_t)blockIdx.y * kBndChunk * kBndNPT + q * kBndChunk + threadIdx.x;
-        v[q][0] = v[q][1] = v[q][2] = 0.0;
-        in_range[q] = t[q] < Kloc && node_vel_s<D>(t[q], ncs, ncol, c0, n1, vmax, dv, v[q]);
-    }
-    for (int g = 0; g < kBndGroup; ++g) {
-        const int64_t bi = (int64_t)blockIdx.x * kBndGroup + g;
-        if (bi >= nb) break;                                // block-uniform
-        const int b = bids[bi];
-        const int64_t off = nb_off[b];
-        const int mi = bcnt[b];                             // interior neighbours (compacted by k_wls_boundary)
-        const int wid = kind[b];
-        const int axis = (wid - 1) / 2;
-        const double sgn = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
-        double vn[kBndNPT];
-        bool incoming[kBndNPT];
-        double acc[kBndNPT][NV];
-#pragma unroll
-        for (int q = 0; q < kBndNPT; ++q) {
-            vn[q] = sgn * v[q][axis];
-            incoming[q] = in_range[q] && vn[q] <= 0.0;
-#pragma unroll
-            for (int c = 0; c < NV; ++c) acc[q][c] = 0.0;
-        }
-#pragma unroll kBndUnroll
-        for (int e = 0; e < mi; ++e) {
-            const int64_t j = __ldg(bidx + off + e);
-            const double c = __ldg(bcw + off + e);
-#pragma unroll
-            for (int q = 0; q < kBndNPT; ++q) {
-                if (!incoming[q]) continue;
-                if constexpr (NV == 1) {
-                    acc[q][0] = fma(c, __ldg(f + j * Kloc + t[q]), acc[q][0]);
-                } else {
-                    const double2 gv = __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t[q]);
-                    acc[q][0] = fma(c, gv.x, acc[q][0]);
-                    acc[q][1] = fma(c, gv.y, acc[q][1]);
-                }
-            }
-        }
-        double flux = 0.0;
-#pragma unroll
-        for (int q = 0; q < kBndNPT; ++q) {
-            if (!incoming[q]) continue;
-            if constexpr (NV == 1) f[(int64_t)b * Kloc + t[q]] = acc[q][0];
-            else reinterpret_cast<double2*>(f)[(int64_t)b * Kloc + t[q]] = make_double2(acc[q][0], acc[q][1]);
-            if (vn[q] < 0.0) flux += vn[q] * acc[q][0];
-        }
-        const double tot = block_sum<kBndChunk>(flux, sh);
-        if (threadIdx.x == 0) wallpart[bi * nch + blockIdx.y] = tot;
-    }
-}
-
 // ---------------------------------------------------------------------------------------------
 // Boundary interpolation by groups of G consecutive particles of the face-sorted boundary list
-// (BGK_BND_G = 4, the default / 8; 0 = the per-particle kernel above).  C5: 2.83 ms at G = 4
-// against 3.20 ms per particle and 3.27 ms at G = 8 (the FMAs grow with G, the row loads shrink).  k_bnd_union (per geometry build) merges
+// (G = 8 in 3D, 4 in 2D; BGK_BND_G = 4 or 8 overrides).  k_bnd_union (per geometry build) merges
 // their compacted (neighbour, weight) lists into one union with a dense G-column weight matrix;
-// k_bnd_interp_u loads each union row's chunk ONCE for the group and applies it to every member
-// (weight 0 if not its neighbour): fewer row loads for more FMAs.
+// k_bnd_interp_t loads each union row's chunk ONCE for the group and applies it to every member
+// (weight 0 if not its neighbour): fewer row loads for more FMAs.  Round 1 measured the per-particle
+// form at 3.20 ms on C5 and an __ldg union of 4 at 2.83-2.89 ms (both removed in round 2).
 // ---------------------------------------------------------------------------------------------
 template <int G>
 __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ bids, int64_t nb,
@@ -558,109 +475,6 @@ __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ b
             else hi = mid;
         }
         W[upos[i] * G + q] = bcw[off + lo];
-    }
-}
-
-template <int D, int G>
-__global__ void __launch_bounds__(kBndChunk) k_bnd_interp_u(const int32_t* __restrict__ bids, int64_t nb,
-                                                            const int8_t* __restrict__ kind,
-                                                            const int32_t* __restrict__ bu_j,
-                                                            const double* __restrict__ bu_w,
-                                                            const int32_t* __restrict__ bu_n, int cap,
-                                                            double* __restrict__ f, double* __restrict__ wallpart,
-                                                            int nch, int n1, int ncol, int ncs, int c0, int64_t Kloc,
-                                                            double vmax, double dv) {
-    constexpr int NV = (D == 2) ? 2 : 1;
-    constexpr int NPT = 2;
-    extern __shared__ double sW[];                          // [U][G] weights, then [U] rows
-    __shared__ double sh[32];
-    const int64_t g = blockIdx.x;
-    const int U = bu_n[g];
-    int32_t* sJ = reinterpret_cast<int32_t*>(sW + (size_t)cap * G);
-    for (int i = threadIdx.x; i < U * G; i += blockDim.x) sW[i] = bu_w[g * cap * G + i];
-    for (int i = threadIdx.x; i < U; i += blockDim.x) sJ[i] = bu_j[g * cap + i];
-    int b[G], axis[G];
-    bool live[G];
-    double sgn[G];
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-        const int64_t bi = g * G + q;
-        live[q] = bi < nb;
-        b[q] = live[q] ? bids[bi] : 0;
-        const int wid = live[q] ? kind[b[q]] : 1;
-        axis[q] = (wid - 1) / 2;
-        sgn[q] = ((wid - 1) % 2 == 0) ? 1.0 : -1.0;
-    }
-    int64_t t[NPT];
-    double v[NPT][3];
-    bool need[NPT], inc[G][NPT];
-#pragma unroll
-    for (int n = 0; n < NPT; ++n) {
-        t[n] = (int64_t)blockIdx.y * kBndChunk * NPT + n * kBndChunk + threadIdx.x;
-        v[n][0] = v[n][1] = v[n][2] = 0.0;
-        const bool in_range = t[n] < Kloc && node_vel_s<D>(t[n], ncs, ncol, c0, n1, vmax, dv, v[n]);
-        need[n] = false;
-#pragma unroll
-        for (int q = 0; q < G; ++q) {
-            inc[q][n] = live[q] && in_range && sgn[q] * v[n][axis[q]] <= 0.0;
-            need[n] = need[n] || inc[q][n];
-        }
-    }
-    __syncthreads();
-    double acc[G][NPT][NV];
-#pragma unroll
-    for (int q = 0; q < G; ++q)
-#pragma unroll
-        for (int n = 0; n < NPT; ++n)
-#pragma unroll
-            for (int c = 0; c < NV; ++c) acc[q][n][c] = 0.0;
-    constexpr int UB = 4;                                   // rows in flight per thread
-    for (int u0 = 0; u0 < U; u0 += UB) {
-        double fv[UB][NPT][NV];
-#pragma unroll
-        for (int uu = 0; uu < UB; ++uu) {
-            const int u = u0 + uu;
-            const int64_t j = u < U ? sJ[u] : 0;
-#pragma unroll
-            for (int n = 0; n < NPT; ++n) {
-                const bool ld = need[n] && u < U;
-                if constexpr (NV == 1) {
-                    fv[uu][n][0] = ld ? __ldg(f + j * Kloc + t[n]) : 0.0;
-                } else {
-                    const double2 gv = ld ? __ldg(reinterpret_cast<const double2*>(f) + j * Kloc + t[n])
-                                          : make_double2(0.0, 0.0);
-                    fv[uu][n][0] = gv.x;
-                    fv[uu][n][1] = gv.y;
-                }
-            }
-        }
-#pragma unroll
-        for (int uu = 0; uu < UB; ++uu) {
-            if (u0 + uu >= U) break;
-            const double* wu = sW + (u0 + uu) * G;
-#pragma unroll
-            for (int q = 0; q < G; ++q) {
-                const double w = wu[q];
-#pragma unroll
-                for (int n = 0; n < NPT; ++n)
-#pragma unroll
-                    for (int c = 0; c < NV; ++c) acc[q][n][c] = fma(w, fv[uu][n][c], acc[q][n][c]);
-            }
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-        double flux = 0.0;
-#pragma unroll
-        for (int n = 0; n < NPT; ++n) {
-            if (!inc[q][n]) continue;
-            if constexpr (NV == 1) f[(int64_t)b[q] * Kloc + t[n]] = acc[q][n][0];
-            else reinterpret_cast<double2*>(f)[(int64_t)b[q] * Kloc + t[n]] = make_double2(acc[q][n][0], acc[q][n][1]);
-            const double vn = sgn[q] * v[n][axis[q]];
-            if (vn < 0.0) flux += vn * acc[q][n][0];
-        }
-        const double tot = block_sum<kBndChunk>(flux, sh);
-        if (threadIdx.x == 0 && live[q]) wallpart[(g * G + q) * nch + blockIdx.y] = tot;
     }
 }
 
@@ -968,22 +782,9 @@ void bnd_union_g(bgk_ctx* c, cudaStream_t s) {
 }
 
 void launch_bnd_union(bgk_ctx* c, cudaStream_t s) {
-    if (!c->N_b || !c->bnd_g) return;
+    if (!c->N_b) return;
     if (c->bnd_g == 4) bnd_union_g<4>(c, s);
     else bnd_union_g<8>(c, s);
-}
-
-template <int D, int G>
-void bnd_interp_g(bgk_ctx* c, double* fnew, cudaStream_t s) {
-    const size_t smem = (size_t)c->bu_cap * (G * sizeof(double) + sizeof(int32_t));
-    static bool configured[kMaxDevices] = {};
-    if (first_use_on_device(configured)) {
-        cudaFuncSetAttribute(k_bnd_interp_u<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    }
-    dim3 gg((unsigned)((c->N_b + G - 1) / G), (unsigned)c->bnd_nch);
-    k_bnd_interp_u<D, G><<<gg, kBndChunk, smem, s>>>(c->boundary, c->N_b, c->kind, c->bu_j, c->bu_w, c->bu_n,
-                                                     c->bu_cap, fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs,
-                                                     c->c0, c->Ks, c->cfg.vmax, c->dv);
 }
 
 template <int D, int G, int NPT, int NS, int MINB = 2>
@@ -996,7 +797,7 @@ void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (first_use_on_device(configured))
         cudaFuncSetAttribute(k_bnd_interp_t<D, G, NPT, NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              200 * 1024);
-    const int nch = (int)((c->Ks + CH - 1) / CH);
+    const int nch = c->bnd_nch;                              // = ceil(Ks / CH) (api.cu derive)
     dim3 gg((unsigned)((c->N_b + G - 1) / G), (unsigned)nch);
     k_bnd_interp_t<D, G, NPT, NS, MINB><<<gg, 256, smem, s>>>(c->boundary, c->N_b, c->kind, c->bu_j, c->bu_w, c->bu_n,
                                                         c->bu_cap, fnew, c->wallpart, nch, c->n1, c->ncol, c->ncs,
@@ -1007,36 +808,8 @@ void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
 
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
-    static const bool ring = [] {
-        const char* e = getenv("BGK_BND_RING");        // 0: the __ldg union kernel (k_bnd_interp_u)
-        return !(e && atoi(e) == 0);
-    }();
-    if (c->bnd_g && ring) {
-        if (c->d == 3) {
-            (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
-        } else {
-            (c->bnd_g == 4 ? bnd_interp_t<2, 4, 2, 6>(c, fnew, s) : bnd_interp_t<2, 8, 2, 6>(c, fnew, s));
-        }
-        return;
-    }
-    if (c->bnd_g) {
-        if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_g<3, 4>(c, fnew, s) : bnd_interp_g<3, 8>(c, fnew, s));
-        else (c->bnd_g == 4 ? bnd_interp_g<2, 4>(c, fnew, s) : bnd_interp_g<2, 8>(c, fnew, s));
-        k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart,
-                                                                        c->bnd_nch, c->wallnum);
-        return;
-    }
-    dim3 g((unsigned)((c->N_b + kBndGroup - 1) / kBndGroup), (unsigned)c->bnd_nch);
-    if (c->d == 3)
-        k_bnd_interp<3><<<g, kBndChunk, 0, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.bidx, c->g.bcw,
-                                                c->g.bcnt, fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0,
-                                                c->Ks, c->cfg.vmax, c->dv);
-    else
-        k_bnd_interp<2><<<g, kBndChunk, 0, s>>>(c->boundary, c->N_b, c->kind, c->g.nb_off, c->g.bidx, c->g.bcw,
-                                                c->g.bcnt, fnew, c->wallpart, c->bnd_nch, c->n1, c->ncol, c->ncs, c->c0,
-                                                c->Ks, c->cfg.vmax, c->dv);
-    k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart, c->bnd_nch,
-                                                                    c->wallnum);
+    if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
+    else (c->bnd_g == 4 ? bnd_interp_t<2, 4, 2, 6>(c, fnew, s) : bnd_interp_t<2, 8, 2, 6>(c, fnew, s));
 }
 
 void launch_boundary_fill(bgk_ctx* c, double* fnew, cudaStream_t s) {
