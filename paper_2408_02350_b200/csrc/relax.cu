@@ -808,6 +808,12 @@ void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
 
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
+    static const int ns = [] {
+        const char* e = getenv("BGK_BND_NS");          // tuning: ring depth 6 (default), 8, 10
+        return e ? atoi(e) : 6;
+    }();
+    if (c->d == 3 && c->bnd_g == 8 && ns == 8) return bnd_interp_t<3, 8, 4, 8>(c, fnew, s);
+    if (c->d == 3 && c->bnd_g == 8 && ns == 10) return bnd_interp_t<3, 8, 4, 10>(c, fnew, s);
     if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
     else (c->bnd_g == 4 ? bnd_interp_t<2, 4, 2, 6>(c, fnew, s) : bnd_interp_t<2, 8, 2, 6>(c, fnew, s));
 }
