@@ -261,6 +261,7 @@ extern "C" bgk_status bgk_graph_info(bgk_ctx* c, int64_t* info) {
 namespace bgk {
 
 void graph_release(bgk_ctx* c) {
+    if (c->gstat[0] > 0) cudaStreamSynchronize(c->gstream);   // graph launches still in flight
     for (int b = 0; b < 2; ++b)
         if (c->gexec[b]) cudaGraphExecDestroy(c->gexec[b]);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);

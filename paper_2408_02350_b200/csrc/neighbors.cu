@@ -320,7 +320,8 @@ __global__ void k_nb_compact(const int32_t* __restrict__ pad, int64_t N, int max
 
 }  // namespace
 
-int launches_neighbors(const bgk_ctx* c) { return c->N <= 32768 ? 10 : 12; }   // scan: 1 or 3 kernels
+// cells: 7 kernels; neighbours: sweep + scan (1 or 3 kernels) + compaction
+int launches_neighbors(const bgk_ctx* c) { return 7 + 2 + (c->N <= 32768 ? 1 : 3); }
 
 void launch_build_neighbors(bgk_ctx* c, cudaStream_t s) {
     const int64_t N = c->N;

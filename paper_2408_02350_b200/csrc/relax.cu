@@ -444,20 +444,35 @@ __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ b
             __syncthreads();
         }
     int32_t* upos = keys + n2;
-    if (threadIdx.x == 0) {
-        int u = -1, prev = -1;
-        for (int i = 0; i < tot; ++i) {
-            const int j = keys[i] >> 3;
-            if (j != prev) {
-                ++u;
-                prev = j;
-                if (u < cap) bu_j[g * cap + u] = j;
-            }
-            upos[i] = u;
+    // union slot of every sorted entry: a block-wide scan of "first of its j" flags, 256 at a time
+    // (a serial walk by one thread was the kernel's latency on the 2D workloads)
+    __shared__ int wcnt[8];
+    int ubase = 0;
+    for (int i0 = 0; i0 < tot; i0 += 256) {
+        const int i = i0 + threadIdx.x;
+        const int j = i < tot ? keys[i] >> 3 : -1;
+        const bool first = i < tot && (i == 0 || (keys[i - 1] >> 3) != j);
+        const unsigned bal = __ballot_sync(0xffffffffu, first);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (lane == 0) wcnt[wid] = __popc(bal);
+        __syncthreads();
+        int before = ubase, total = 0;
+        for (int w = 0; w < 8; ++w) {
+            before += w < wid ? wcnt[w] : 0;
+            total += wcnt[w];
         }
-        s_n = u + 1;
-        if (u + 1 > cap) latch_error(err, BGK_E_CAPACITY, bids[g * G]);
-        bu_n[g] = u + 1 > cap ? 0 : u + 1;
+        const int u = before + __popc(bal & ((1u << lane) - 1u)) + (first ? 0 : -1);   // slot of entry i
+        if (i < tot) {
+            upos[i] = u;
+            if (first && u < cap) bu_j[g * cap + u] = j;
+        }
+        ubase += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s_n = ubase;
+        if (ubase > cap) latch_error(err, BGK_E_CAPACITY, bids[g * G]);
+        bu_n[g] = ubase > cap ? 0 : ubase;
     }
     __syncthreads();
     if (s_n > cap) return;
@@ -808,12 +823,7 @@ void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
 
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
-    static const int ns = [] {
-        const char* e = getenv("BGK_BND_NS");          // tuning: ring depth 6 (default), 8, 10
-        return e ? atoi(e) : 6;
-    }();
-    if (c->d == 3 && c->bnd_g == 8 && ns == 8) return bnd_interp_t<3, 8, 4, 8>(c, fnew, s);
-    if (c->d == 3 && c->bnd_g == 8 && ns == 10) return bnd_interp_t<3, 8, 4, 10>(c, fnew, s);
+    // ring depth 6 (C5: 2.48 ms; 8 stages the same, 10 stages 3.82 ms -- one block per SM)
     if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
     else (c->bnd_g == 4 ? bnd_interp_t<2, 4, 2, 6>(c, fnew, s) : bnd_interp_t<2, 8, 2, 6>(c, fnew, s));
 }

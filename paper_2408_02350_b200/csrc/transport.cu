@@ -647,6 +647,13 @@ bool make_tensor_maps(bgk_ctx* c) {
             return false;
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
+    static const CUtensorMapL2promotion promo = [] {   // tuning knob: L2 sector promotion of box fetches
+        const char* e = getenv("BGK_L2PROMO");
+        const int v = e ? atoi(e) : 256;
+        return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                      : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }();
     const cuuint64_t dims[3] = {(cuuint64_t)c->ncs * c->nv, (cuuint64_t)c->n1, (cuuint64_t)c->N};
     const cuuint64_t strides[2] = {(cuuint64_t)c->ncs * c->nv * sizeof(double),
                                    (cuuint64_t)c->ncs * c->nv * c->n1 * sizeof(double)};
@@ -656,7 +663,7 @@ bool make_tensor_maps(bgk_ctx* c) {
     for (int b = 0; b < 2; ++b) {
         CUresult r = encode(&c->tmap[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->f[b], dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                            promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return false;
         if (c->fold) {
             const cuuint32_t box_fold[3] = {16, (cuuint32_t)(2 * kFoldR), 1};
