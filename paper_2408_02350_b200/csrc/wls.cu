@@ -90,12 +90,6 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
     double At[NT];
 #pragma unroll
     for (int t = 0; t < NT; ++t) At[t] = 0.0;
-    // first order: the offsets and weights of a lane's first kCache entries stay in registers for
-    // the coefficient pass (no second gather of x_j, no second exp); entries past kCache * 32 (lists
-    // longer than 128) are recomputed
-    constexpr int kCache = ORDER == 1 ? 4 : 1;
-    double cdd[kCache][D], cwt[kCache];
-    int cj[kCache];
     for (int e = lane; e < m; e += 32) {
         const int j = nb_idx[off + e];
         double xj[D], dd[D], mv[NU];
@@ -103,17 +97,6 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
         for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; dd[a] = (xj[a] - xi[a]) * inv_h; }
         T::mono(dd, mv);
         const double wgt = exp(-alpha * dist2_rn<D>(xi, xj) / h2);
-        const int k = (e - lane) >> 5;
-        if (ORDER == 1 && k < kCache) {
-#pragma unroll
-            for (int q = 0; q < kCache; ++q)
-                if (q == k) {
-#pragma unroll
-                    for (int a = 0; a < D; ++a) cdd[q][a] = dd[a];
-                    cwt[q] = wgt;
-                    cj[q] = j;
-                }
-        }
         int t = 0;
 #pragma unroll
         for (int r = 0; r < NU; ++r)
@@ -146,31 +129,12 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
             for (int q = 0; q < D; ++q) S_out[(int64_t)p * D * D + r * D + q] = Si[r][q] * inv_h * inv_h;
     }
     for (int e = lane; e < m; e += 32) {
-        const int k = (e - lane) >> 5;
-        int j;
-        double dd[D], mv[NU], wgt;
-        if (ORDER == 1 && k < kCache) {
-            j = cj[0];
-            wgt = cwt[0];
+        const int j = nb_idx[off + e];
+        double xj[D], dd[D], mv[NU];
 #pragma unroll
-            for (int a = 0; a < D; ++a) dd[a] = cdd[0][a];
-#pragma unroll
-            for (int q = 1; q < kCache; ++q)
-                if (q == k) {
-                    j = cj[q];
-                    wgt = cwt[q];
-#pragma unroll
-                    for (int a = 0; a < D; ++a) dd[a] = cdd[q][a];
-                }
-        } else {
-            j = nb_idx[off + e];
-            double xj[D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; dd[a] = (xj[a] - xi[a]) * inv_h; }
-            wgt = exp(-alpha * dist2_rn<D>(xi, xj) / h2);
-        }
-        (void)j;
+        for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; dd[a] = (xj[a] - xi[a]) * inv_h; }
         T::mono(dd, mv);
+        const double wgt = exp(-alpha * dist2_rn<D>(xi, xj) / h2);
         double av[D];   // a_j = w_j [(M^T W M)^{-1} m_j]_{0:d} / h, physical units 1/m
 #pragma unroll
         for (int r = 0; r < D; ++r) {
