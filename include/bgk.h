@@ -272,9 +272,11 @@ bgk_status bgk_use_staged_f(bgk_ctx* ctx, bgk_stream stream);
  *     the midpoint (slot of the smaller index), its f row, transport velocity W and macro state
  *     interpolated (linear WLS with a constant term, the boundary-interpolation construction of
  *     Z19) from every other particle within h of the midpoint;
- *  2. fill: interior particles with fewer than m_min neighbours propose x +- 0.5 h e_a; proposals
- *     inside the open box and farther than 0.45 dx from every particle are inserted (appended),
- *     interpolated the same way;
+ *  2. fill: interior particles with fewer than m_min neighbours propose x +- 0.5 h e_a, and wall
+ *     particles whose interpolation stencil has fewer than dims + 2 interior members propose
+ *     x + 0.5 h (sum of their inward wall normals) and x + 0.5 h n_a per wall (Z30);
+ *     proposals inside the open box and farther than 0.45 dx from every particle are inserted
+ *     (appended), interpolated the same way;
  *  3. the surviving particles keep their relative order, inserted ones follow.
  * Deficient interpolation stencils keep the pair / skip the proposal; inserts stop at the
  * capacity.  One pass creates at most 4096 new particles (merged + inserted): pairs past that

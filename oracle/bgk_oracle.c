@@ -843,12 +843,16 @@ static int interp_new(const or_cfg* c, int64_t N, const double* x, const double*
  *     pair is replaced by ONE particle at m = (x_i + x_j) * 0.5 in slot i (slot j is removed);
  *     its f row, W and macro are interpolated from every other particle of the OLD cloud
  *     within h of m.  A deficient stencil keeps the pair (reported).
- *  2. fill: for interior i ascending, not processed in 1, with |N(i)| < m_min: the candidates
- *     p = x_i + s (0.5 h) e_a (a = 0..d-1; s = +1, then -1) strictly inside (0, L)^d and
- *     farther than 0.45 dx from every particle of the CURRENT cloud (old particles minus the
- *     removed slots, merged particles at their midpoints, candidates inserted so far) are
- *     appended, interpolated from the OLD cloud within h of p.  Deficient candidates are
- *     skipped; insertion stops at the capacity cap (both reported).
+ *  2. fill: for i ascending, not processed in 1, either interior with |N(i)| < m_min -- the
+ *     candidates p = x_i + s (0.5 h) e_a (a = 0..d-1; s = +1, then -1) -- or a boundary particle
+ *     whose interpolation system (its interior neighbours, Z19) is deficient -- fewer than d + 2
+ *     members or lambda_min < 1e-12 lambda_max, the test of or_boundary_weights_one -- the
+ *     candidates x_i + s h N, N = sum of the inward normals of the walls it lies on, s = 1/2, 1/4,
+ *     3/4 in that order, of which it takes the first accepted one (Z30) --
+ *     those strictly inside (0, L)^d and farther than 0.45 dx from every particle of the CURRENT
+ *     cloud (old particles minus the removed slots, merged particles at their midpoints,
+ *     candidates inserted so far) are appended, interpolated from the OLD cloud within h of p.
+ *     Deficient candidates are skipped; insertion stops at the capacity cap (both reported).
  *  3. compaction: the surviving slots in ascending old order, then the appended particles.
  * Outputs (capacity cap): x_out, kind_out, f_out, W_out, macro_out;
  * report[6] = {merges, merges kept (deficient), fills, fills skipped (deficient),
@@ -909,21 +913,47 @@ int or_manage(const or_cfg* c, int64_t N, const double* x, const int8_t* kind, c
     double* fW = (double*)malloc(sizeof(double) * (size_t)((fcap > 0 ? fcap : 1) * d));
     double* fM = (double*)malloc(sizeof(double) * (size_t)((fcap > 0 ? fcap : 1) * (d + 2)));
     for (int64_t i = 0; i < N; ++i) {
-        if (kind[i] != 0 || processed[i] || off[i + 1] - off[i] >= m_min) continue;
-        for (int a = 0; a < d; ++a)
-            for (int sgn = 0; sgn < 2; ++sgn) {
+        if (processed[i]) continue;
+        double cand[6][3];                        /* the candidates of i, in proposal order */
+        int nc = 0;
+        if (kind[i] == 0) {
+            if (off[i + 1] - off[i] >= m_min) continue;
+            for (int a = 0; a < d; ++a)
+                for (int sgn = 0; sgn < 2; ++sgn) {
+                    for (int q = 0; q < d; ++q) cand[nc][q] = x[i * d + q];
+                    cand[nc][a] = sgn == 0 ? x[i * d + a] + hh : x[i * d + a] - hh;
+                    ++nc;
+                }
+        } else {
+            /* a wall particle whose interpolation system (Z19: its interior neighbours) is
+             * deficient -- fewer than d + 2 members or lambda_min < 1e-12 lambda_max (Z30) */
+            int mb = (int)(off[i + 1] - off[i]);
+            double* cwt = (double*)malloc(sizeof(double) * (size_t)(mb > 0 ? mb : 1));
+            int st_b = or_boundary_weights_one(d, x, kind, i, mb, idx + off[i], c->h2, c->alpha_w, cwt);
+            free(cwt);
+            if (st_b == OR_OK) continue;
+            double nrm[3] = {0.0, 0.0, 0.0};      /* sum of the inward normals of its walls */
+            for (int a = 0; a < d; ++a) {
+                if (x[i * d + a] == 0.0) nrm[a] = 1.0;
+                else if (x[i * d + a] == c->L) nrm[a] = -1.0;
+            }
+            const double hs[3] = {0.5 * c->h, 0.25 * c->h, 0.75 * c->h};
+            for (int k = 0; k < 3; ++k, ++nc)
+                for (int q = 0; q < d; ++q) cand[nc][q] = x[i * d + q] + hs[k] * nrm[q];
+        }
+        const int wall = kind[i] != 0;            /* a wall particle takes its first accepted candidate */
+        for (int k = 0; k < nc && k < 2 * d; ++k) {
                 double p[3];
-                for (int q = 0; q < d; ++q) p[q] = x[i * d + q];
-                p[a] = sgn == 0 ? x[i * d + a] + hh : x[i * d + a] - hh;
+                for (int q = 0; q < d; ++q) p[q] = cand[k][q];
                 int inside = 1;
                 for (int q = 0; q < d; ++q)
                     if (!(p[q] > 0.0 && p[q] < c->L)) inside = 0;
                 if (!inside) continue;
                 int clear = 1;
-                for (int64_t k = 0; k < N && clear; ++k)
-                    if (!removed[k] && !(dist2(d, p, cur + k * d) > thr2)) clear = 0;
-                for (int64_t k = 0; k < nf && clear; ++k)
-                    if (!(dist2(d, p, fx + k * d) > thr2)) clear = 0;
+                for (int64_t k2 = 0; k2 < N && clear; ++k2)
+                    if (!removed[k2] && !(dist2(d, p, cur + k2 * d) > thr2)) clear = 0;
+                for (int64_t k2 = 0; k2 < nf && clear; ++k2)
+                    if (!(dist2(d, p, fx + k2 * d) > thr2)) clear = 0;
                 if (!clear) continue;
                 if (nf >= fcap) { ++report[4]; continue; }
                 if (interp_new(c, N, x, f, W, macro, p, -1, -1, ff + nf * RK, fW + nf * d,
@@ -933,7 +963,8 @@ int or_manage(const or_cfg* c, int64_t N, const double* x, const int8_t* kind, c
                 }
                 for (int q = 0; q < d; ++q) fx[nf * d + q] = p[q];
                 ++nf;
-            }
+                if (wall) break;
+        }
     }
     report[2] = nf;
     /* 3. compaction */

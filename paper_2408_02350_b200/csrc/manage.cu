@@ -41,14 +41,15 @@ template <int D>
 __global__ void __launch_bounds__(256) k_mg_detect_w(const double* __restrict__ x, const int8_t* __restrict__ kind,
                                                      int64_t N, const int64_t* __restrict__ nb_off,
                                                      const int32_t* __restrict__ nb_idx, double rm2, int m_min,
+                                                     double inv_h, double h2, double alpha,
                                                      uint8_t* __restrict__ flag, int32_t* __restrict__ counts) {
     const int lane = threadIdx.x & 31;
     const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= N) return;
     uint8_t fl = 0;
+    const int64_t off = nb_off[i];
+    const int m = (int)(nb_off[i + 1] - off);
     if (kind[i] == 0) {
-        const int64_t off = nb_off[i];
-        const int m = (int)(nb_off[i + 1] - off);
         if (m < m_min) fl |= kDeficient;
         double xi[3];
 #pragma unroll
@@ -63,6 +64,42 @@ __global__ void __launch_bounds__(256) k_mg_detect_w(const double* __restrict__ 
             close = close || dist2_rn<D>(xi, xj) < rm2;
         }
         if (__any_sync(0xffffffffu, close)) fl |= kMergeCand;
+    } else {
+        // a wall particle whose interpolation system (Z19: linear WLS with a constant term over its
+        // interior neighbours, offsets in units of h) is deficient -- fewer than d + 2 members or
+        // lambda_min < 1e-12 lambda_max, the test of k_wls_boundary: the fill pass proposes points
+        // inward of it (Z30)
+        constexpr int n = D + 1;
+        double xb[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) xb[a] = x[i * D + a];
+        double B[n][n];
+#pragma unroll
+        for (int r = 0; r < n; ++r)
+#pragma unroll
+            for (int q = 0; q < n; ++q) B[r][q] = 0.0;
+        int n_int = 0;
+        for (int e = lane; e < m; e += 32) {
+            const int j = nb_idx[off + e];
+            if (kind[j] != 0) continue;
+            ++n_int;
+            double xj[3], Pv[n];
+            Pv[0] = 1.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; Pv[1 + a] = (xj[a] - xb[a]) * inv_h; }
+            const double w = exp(-alpha * dist2_rn<D>(xb, xj) / h2);
+#pragma unroll
+            for (int r = 0; r < n; ++r)
+#pragma unroll
+                for (int q = 0; q < n; ++q) B[r][q] += w * Pv[r] * Pv[q];
+        }
+        n_int = warp_sum(n_int);
+#pragma unroll
+        for (int r = 0; r < n; ++r)
+#pragma unroll
+            for (int q = 0; q < n; ++q) B[r][q] = warp_sum(B[r][q]);
+        double Bi[n][n];
+        if (!(n_int >= D + 2 && well_conditioned<n>(B) && small_inverse<n>(B, Bi))) fl |= kDeficient;
     }
     if (lane == 0) {
         flag[i] = fl;
@@ -311,12 +348,35 @@ __global__ void __launch_bounds__(32) k_mg_decide(const MgArgs A, int64_t fill_c
             bal &= bal - 1;
             __syncwarp();
             if (m.flag[i] & kProcessed) continue;
-            for (int a = 0; a < D; ++a)
-                for (int sgn = 0; sgn < 2; ++sgn) {
+            // candidates in proposal order: interior x_i +- 0.5 h e_a (a ascending, + before -);
+            // wall particle (Z30): x_i + s h N, N = sum of its inward wall normals, s = 1/2, 1/4, 3/4,
+            // the first accepted one only
+            double cand[2 * D > 3 ? 2 * D : 3][3];
+            int nc = 0;
+            if (A.kind[i] == 0) {
+                for (int a = 0; a < D; ++a)
+                    for (int sgn = 0; sgn < 2; ++sgn) {
+#pragma unroll
+                        for (int b = 0; b < D; ++b) cand[nc][b] = A.x[i * D + b];
+                        cand[nc][a] = sgn == 0 ? __dadd_rn(cand[nc][a], A.hh) : __dsub_rn(cand[nc][a], A.hh);
+                        ++nc;
+                    }
+            } else {
+                double nrm[3] = {0.0, 0.0, 0.0};    // sum of the inward normals of its walls
+                for (int a = 0; a < D; ++a) {
+                    const double v = A.x[i * D + a];
+                    if (v == 0.0) nrm[a] = 1.0;
+                    else if (v == A.L) nrm[a] = -1.0;
+                }
+                const double hs[3] = {0.5 * A.h, 0.25 * A.h, 0.75 * A.h};
+                for (int k = 0; k < 3; ++k, ++nc)
+                    for (int b = 0; b < D; ++b) cand[nc][b] = __dadd_rn(A.x[i * D + b], __dmul_rn(hs[k], nrm[b]));
+            }
+            const bool wall = A.kind[i] != 0;       // a wall particle takes its first accepted candidate
+            for (int k = 0; k < nc; ++k) {
                     double p[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int b = 0; b < D; ++b) p[b] = A.x[i * D + b];
-                    p[a] = sgn == 0 ? __dadd_rn(p[a], A.hh) : __dsub_rn(p[a], A.hh);
+                    for (int b = 0; b < D; ++b) p[b] = cand[k][b];
                     bool inside = true;
 #pragma unroll
                     for (int b = 0; b < D; ++b)
@@ -343,7 +403,8 @@ __global__ void __launch_bounds__(32) k_mg_decide(const MgArgs A, int64_t fill_c
                     __syncwarp();
                     ++q;
                     ++nf;
-                }
+                    if (wall) break;
+            }
         }
     }
     rep[2] = nf;
@@ -444,7 +505,7 @@ void decide_pass(bgk_ctx* c, cudaStream_t s) {
     cudaMemsetAsync(m.counts, 0, 4 * sizeof(int32_t), s);
     cudaMemsetAsync(m.status, 0, sizeof(int32_t) * N, s);
     k_mg_detect_w<D><<<(unsigned)((N + 7) / 8), 256, 0, s>>>(c->x, c->kind, N, c->g.nb_off, c->g.nb_idx, rm * rm,
-                                                             m_min, m.flag, m.counts);
+                                                             m_min, 1.0 / cf.h, cf.h2, cf.alpha_w, m.flag, m.counts);
     MgArgs A;
     A.x = c->x;
     A.kind = c->kind;

@@ -98,10 +98,9 @@ def test_cavity_rho1_steady_state_zero_wall_flux_every_step():
     mass flux through every wall particle zero to 1e-12 of the absolute flux after EVERY step
     (diffuse reflection), checked on the device from the internal f buffer.
     The cloud is the fixed one (grid velocity W = 0, the Eulerian case of the ALE scheme, Z21): on
-    the moving cloud the gas carries the particles out of the lid corner over the ~10^4 steps this
-    case needs, the corner's boundary-interpolation stencil becomes deficient (BGK_E_DEFICIENT_STENCIL
-    at the (0, L) corner, with and without particle management: the fill rule of Z28 reacts to
-    interior particles only) -- DESIGN.md NEXT(2)."""
+    the moving cloud the lid drives particles out of one lid corner and into the other over the
+    ~10^4 steps this case needs; the wall fills of Z30 repair the emptied corner, but the crowded one
+    eventually leaves its interpolation system deficient (tools/rho1_ale.py)."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")

@@ -135,3 +135,29 @@ def test_managed_column_sharded_steps(torch_cuda):
     for r, (c0, c1) in zip(ranks, shards):
         full[:, :, :, c0:c1] = r.get_f().reshape(N, -1, n1, c1 - c0)
     assert rel(full.reshape(N, -1), ref.f) <= TOL
+
+
+@pytest.mark.parametrize("dims,n", [(2, 15), (3, 9)])
+def test_wall_fill_matches_oracle(torch_cuda, dims, n):
+    """Z30 wall fills: a corner whose interpolation stencil lost its interior neighbours triggers an
+    insert inward of it -- one pass bit-exact against the oracle (report, positions, kinds; rows
+    1e-12), then three managed ALE steps at the step parity bar."""
+    from test_oracle_manage import _depleted_corner
+    cfg, cloud, corner = _depleted_corner(dims, n)
+    cfg = cfg.replace(init="stress", dt=5e-12)
+    cloud.update({k: v for k, v in zip(("rho", "U", "T"), bi.initial_fields(cfg, cloud["x"]))})
+    g = gpu(cfg, cloud)
+    rep = g.manage()
+    s = oracle.State(oracle.make_cfg(cfg), cloud)
+    ref = s.manage(*oracle.manage_params(cfg))
+    assert rep == ref and rep[2] >= 1
+    assert np.array_equal(g.positions(), s.x)
+    assert np.array_equal(g.kinds(), s.kind)
+    assert rel(g.get_f().reshape(g.N, -1), s.f) <= 1e-12
+    g2 = gpu(cfg, cloud)
+    g2.step(3)
+    g2.sync()
+    ref = oracle.run_steps(cfg, 3, cloud)
+    assert g2.N == ref.x.shape[0]
+    assert np.abs(g2.positions() - ref.x).max() <= 1e-12 * cfg.dx
+    assert rel(g2.get_f().reshape(g2.N, -1), ref.f) <= TOL

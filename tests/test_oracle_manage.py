@@ -203,3 +203,54 @@ def test_equilibrium_fixed_point_with_management(oracle_lib):
     assert np.abs(rho / r0[0] - 1).max() < 1e-12
     assert np.abs(U).max() / SIG < 1e-12
     assert np.abs(T / t0[0] - 1).max() < 1e-12
+
+
+# ------------------------------------------------------------ wall fills (Z30)
+def _depleted_corner(dims, n):
+    """A lattice whose corner x = 0, y = L (2D) / origin (3D) has lost interior neighbours: the
+    interior lattice points nearest to it are removed, leaving its interpolation stencil with
+    fewer than d + 2 members (the lattice corner has 4 in 2D and 7 in 3D)."""
+    cfg = bi.CavityConfig("wc", dims, n, 4, init="equilibrium", manage=1)
+    cloud = bi.make_cloud(cfg)
+    x, dx, L = cloud["x"], cfg.dx, cfg.L
+    corner = np.zeros(dims)
+    if dims == 2:
+        corner[1] = L
+    ii = np.rint(np.abs(x - corner) / dx).astype(int)            # lattice offsets from the corner
+    # 2D: the nearest interior point (4 -> 3 left); 3D: (1,1,1), (1,1,2), (1,2,1) (7 -> 4 left)
+    gone = [(1, 1)] if dims == 2 else [(1, 1, 1), (1, 1, 2), (1, 2, 1)]
+    drop = np.nonzero((cloud["kind"] == 0) & np.any(np.all(ii[:, None, :] == np.array(gone)[None], axis=2),
+                                                      axis=1))[0]
+    keep = np.setdiff1d(np.arange(len(x)), drop)
+    for k in ("x", "kind", "rho", "U", "T"):
+        cloud[k] = cloud[k][keep]
+    return cfg, cloud, corner
+
+
+@pytest.mark.parametrize("dims,n", [(2, 15), (3, 9)])
+def test_wall_fill_at_a_depleted_corner(oracle_lib, dims, n):
+    """Z30: a wall particle whose interpolation system is deficient (here: fewer than d + 2 interior
+    neighbours) proposes x_b + 0.5 h (sum of the inward normals); on the depleted corner that point is
+    inside the box and clear of every particle (> 0.45 dx), so it is inserted and the corner's
+    stencil has d + 2 members again."""
+    cfg, cloud, corner = _depleted_corner(dims, n)
+    s, _ = _state(cfg, cloud)
+    x0 = s.x.copy()
+    N = len(x0)
+    b = int(np.nonzero(np.all(x0 == corner, axis=1))[0][0])
+    off, idx = oracle.neighbors(x0, cfg.h2)
+    n_int = int((cloud["kind"][idx[off[b]:off[b + 1]]] == 0).sum())
+    assert n_int < dims + 2
+    rep = s.manage(cfg.merge_radius, cfg.min_neighbors, cfg.capacity)
+    assert rep[0] == 0 and rep[2] >= 1
+    inward = np.where(corner == 0.0, 1.0, -1.0)
+    want = corner + 0.5 * cfg.h * inward
+    new = s.x[N:]
+    assert np.any(np.all(new == want, axis=1)), (new, want)
+    assert np.all(s.kind[N:] == 0) and np.all((new > 0) & (new < cfg.L))
+    assert np.array_equal(s.x[:N], x0)
+    off2, idx2 = oracle.neighbors(s.x, cfg.h2)
+    n_int2 = int((s.kind[idx2[off2[b]:off2[b + 1]]] == 0).sum())
+    assert n_int2 == n_int + 1 == dims + 2
+    # the inserted rows are WLS interpolations: an equilibrium field stays the same Maxwellian row
+    assert np.abs(s.f[N:] - s.f[0]).max() <= 1e-10 * np.abs(s.f[0]).max()
