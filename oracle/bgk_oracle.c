@@ -846,7 +846,8 @@ static int interp_new(const or_cfg* c, int64_t N, const double* x, const double*
  *  2. fill: for i ascending, not processed in 1, either interior with |N(i)| < m_min -- the
  *     candidates p = x_i + s (0.5 h) e_a (a = 0..d-1; s = +1, then -1) -- or a boundary particle
  *     whose interpolation system (its interior neighbours, Z19) is deficient -- fewer than d + 2
- *     members or lambda_min < 1e-12 lambda_max, the test of or_boundary_weights_one -- the
+ *     members, or (for fewer than 3 (d + 1) members) lambda_min < 1e-12 lambda_max or a zero pivot,
+ *     the test of or_boundary_weights_one -- the
  *     candidates x_i + s h N, N = sum of the inward normals of the walls it lies on, s = 1/2, 1/4,
  *     3/4 in that order, of which it takes the first accepted one (Z30) --
  *     those strictly inside (0, L)^d and farther than 0.45 dx from every particle of the CURRENT
@@ -927,7 +928,9 @@ int or_manage(const or_cfg* c, int64_t N, const double* x, const int8_t* kind, c
         } else {
             /* a wall particle whose interpolation system (Z19: its interior neighbours) is
              * deficient -- fewer than d + 2 members or lambda_min < 1e-12 lambda_max (Z30) */
-            int mb = (int)(off[i + 1] - off[i]);
+            int mb = (int)(off[i + 1] - off[i]), n_int = 0;
+            for (int64_t e = off[i]; e < off[i + 1]; ++e) n_int += kind[idx[e]] == 0;
+            if (n_int >= 3 * (d + 1)) continue;   /* the conditioning test only on small stencils */
             double* cwt = (double*)malloc(sizeof(double) * (size_t)(mb > 0 ? mb : 1));
             int st_b = or_boundary_weights_one(d, x, kind, i, mb, idx + off[i], c->h2, c->alpha_w, cwt);
             free(cwt);

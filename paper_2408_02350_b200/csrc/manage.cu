@@ -66,40 +66,44 @@ __global__ void __launch_bounds__(256) k_mg_detect_w(const double* __restrict__ 
         if (__any_sync(0xffffffffu, close)) fl |= kMergeCand;
     } else {
         // a wall particle whose interpolation system (Z19: linear WLS with a constant term over its
-        // interior neighbours, offsets in units of h) is deficient -- fewer than d + 2 members or
-        // lambda_min < 1e-12 lambda_max, the test of k_wls_boundary: the fill pass proposes points
-        // inward of it (Z30)
+        // interior neighbours, offsets in units of h) is deficient -- fewer than d + 2 members, or,
+        // for fewer than 3 (d + 1) members, lambda_min < 1e-12 lambda_max or a zero pivot (the test of
+        // k_wls_boundary): the fill pass proposes points inward of it (Z30)
         constexpr int n = D + 1;
-        double xb[3];
-#pragma unroll
-        for (int a = 0; a < D; ++a) xb[a] = x[i * D + a];
-        double B[n][n];
-#pragma unroll
-        for (int r = 0; r < n; ++r)
-#pragma unroll
-            for (int q = 0; q < n; ++q) B[r][q] = 0.0;
         int n_int = 0;
-        for (int e = lane; e < m; e += 32) {
-            const int j = nb_idx[off + e];
-            if (kind[j] != 0) continue;
-            ++n_int;
-            double xj[3], Pv[n];
-            Pv[0] = 1.0;
+        for (int e = lane; e < m; e += 32) n_int += kind[nb_idx[off + e]] == 0;
+        n_int = warp_sum(n_int);
+        if (n_int < D + 2) {
+            fl |= kDeficient;
+        } else if (n_int < 3 * n) {               // small stencils: the full test of the boundary WLS
+            double xb[3];
 #pragma unroll
-            for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; Pv[1 + a] = (xj[a] - xb[a]) * inv_h; }
-            const double w = exp(-alpha * dist2_rn<D>(xb, xj) / h2);
+            for (int a = 0; a < D; ++a) xb[a] = x[i * D + a];
+            double B[n][n];
 #pragma unroll
             for (int r = 0; r < n; ++r)
 #pragma unroll
-                for (int q = 0; q < n; ++q) B[r][q] += w * Pv[r] * Pv[q];
+                for (int q = 0; q < n; ++q) B[r][q] = 0.0;
+            for (int e = lane; e < m; e += 32) {
+                const int j = nb_idx[off + e];
+                if (kind[j] != 0) continue;
+                double xj[3], Pv[n];
+                Pv[0] = 1.0;
+#pragma unroll
+                for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; Pv[1 + a] = (xj[a] - xb[a]) * inv_h; }
+                const double w = exp(-alpha * dist2_rn<D>(xb, xj) / h2);
+#pragma unroll
+                for (int r = 0; r < n; ++r)
+#pragma unroll
+                    for (int q = 0; q < n; ++q) B[r][q] += w * Pv[r] * Pv[q];
+            }
+#pragma unroll
+            for (int r = 0; r < n; ++r)
+#pragma unroll
+                for (int q = 0; q < n; ++q) B[r][q] = warp_sum(B[r][q]);
+            double Bi[n][n];
+            if (!(well_conditioned<n>(B) && small_inverse<n>(B, Bi))) fl |= kDeficient;
         }
-        n_int = warp_sum(n_int);
-#pragma unroll
-        for (int r = 0; r < n; ++r)
-#pragma unroll
-            for (int q = 0; q < n; ++q) B[r][q] = warp_sum(B[r][q]);
-        double Bi[n][n];
-        if (!(n_int >= D + 2 && well_conditioned<n>(B) && small_inverse<n>(B, Bi))) fl |= kDeficient;
     }
     if (lane == 0) {
         flag[i] = fl;
