@@ -692,8 +692,8 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
     int64_t k = 0;
     if (c->cfg.ale) k += launches_neighbors(c) + launches_wls() - (c->N_b ? 0 : 1) - (c->N_int ? 0 : 1);
     if (c->cfg.ale && c->N_b) k += 1;   // k_bnd_union
-    if (c->cfg.ale && c->cfg.manage) k += 2;   // k_mg_detect_w + k_mg_decide (plus 3 more and a neighbour
-                                               // rebuild in the rare steps where the cloud changes)
+    if (c->cfg.ale && c->cfg.manage)   // k_mg_detect_w (+ k_mg_detect_wall) + k_mg_decide (plus 3 more and a
+        k += 2 + (c->N_b ? 1 : 0);     // neighbour rebuild in the rare steps where the cloud changes)
     if (c->cfg.ale && c->cfg.manage && c->graph_ok && c->ncol == c->ncol_g)
         k += 3;                  // graph steps: the two conditional gates and the step counter (graph.cu)
     if (c->N_int) k += 3 + (c->fold ? 1 : 0);   // transport (+ the folded group), moment reduce, relax

@@ -41,7 +41,6 @@ template <int D>
 __global__ void __launch_bounds__(256) k_mg_detect_w(const double* __restrict__ x, const int8_t* __restrict__ kind,
                                                      int64_t N, const int64_t* __restrict__ nb_off,
                                                      const int32_t* __restrict__ nb_idx, double rm2, int m_min,
-                                                     double inv_h, double h2, double alpha,
                                                      uint8_t* __restrict__ flag, int32_t* __restrict__ counts) {
     const int lane = threadIdx.x & 31;
     const int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -64,50 +63,72 @@ __global__ void __launch_bounds__(256) k_mg_detect_w(const double* __restrict__ 
             close = close || dist2_rn<D>(xi, xj) < rm2;
         }
         if (__any_sync(0xffffffffu, close)) fl |= kMergeCand;
-    } else {
-        // a wall particle whose interpolation system (Z19: linear WLS with a constant term over its
-        // interior neighbours, offsets in units of h) is deficient -- fewer than d + 2 members, or,
-        // for fewer than 3 (d + 1) members, lambda_min < 1e-12 lambda_max or a zero pivot (the test of
-        // k_wls_boundary): the fill pass proposes points inward of it (Z30)
-        constexpr int n = D + 1;
-        int n_int = 0;
-        for (int e = lane; e < m; e += 32) n_int += kind[nb_idx[off + e]] == 0;
-        n_int = warp_sum(n_int);
-        if (n_int < D + 2) {
-            fl |= kDeficient;
-        } else if (n_int < 3 * n) {               // small stencils: the full test of the boundary WLS
-            double xb[3];
-#pragma unroll
-            for (int a = 0; a < D; ++a) xb[a] = x[i * D + a];
-            double B[n][n];
-#pragma unroll
-            for (int r = 0; r < n; ++r)
-#pragma unroll
-                for (int q = 0; q < n; ++q) B[r][q] = 0.0;
-            for (int e = lane; e < m; e += 32) {
-                const int j = nb_idx[off + e];
-                if (kind[j] != 0) continue;
-                double xj[3], Pv[n];
-                Pv[0] = 1.0;
-#pragma unroll
-                for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; Pv[1 + a] = (xj[a] - xb[a]) * inv_h; }
-                const double w = exp(-alpha * dist2_rn<D>(xb, xj) / h2);
-#pragma unroll
-                for (int r = 0; r < n; ++r)
-#pragma unroll
-                    for (int q = 0; q < n; ++q) B[r][q] += w * Pv[r] * Pv[q];
-            }
-#pragma unroll
-            for (int r = 0; r < n; ++r)
-#pragma unroll
-                for (int q = 0; q < n; ++q) B[r][q] = warp_sum(B[r][q]);
-            double Bi[n][n];
-            if (!(well_conditioned<n>(B) && small_inverse<n>(B, Bi))) fl |= kDeficient;
-        }
     }
     if (lane == 0) {
         flag[i] = fl;
         if (fl) atomicAdd(counts, 1);
+    }
+}
+
+
+// wall particles (the boundary list): Z30's deficiency of the interpolation system, in a kernel of
+// its own so that the interior flags keep their lean register budget
+template <int D>
+__global__ void __launch_bounds__(256) k_mg_detect_wall(const double* __restrict__ x, const int8_t* __restrict__ kind,
+                                                        const int32_t* __restrict__ bids, int64_t nb,
+                                                        const int64_t* __restrict__ nb_off,
+                                                        const int32_t* __restrict__ nb_idx, double inv_h, double h2,
+                                                        double alpha, uint8_t* __restrict__ flag,
+                                                        int32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= nb) return;
+    const int64_t i = bids[w];
+    const int64_t off = nb_off[i];
+    const int m = (int)(nb_off[i + 1] - off);
+    uint8_t fl = 0;
+    // a wall particle whose interpolation system (Z19: linear WLS with a constant term over its
+    // interior neighbours, offsets in units of h) is deficient -- fewer than d + 2 members, or,
+    // for fewer than 3 (d + 1) members, lambda_min < 1e-12 lambda_max or a zero pivot (the test of
+    // k_wls_boundary): the fill pass proposes points inward of it (Z30)
+    constexpr int n = D + 1;
+    int n_int = 0;
+    for (int e = lane; e < m; e += 32) n_int += kind[nb_idx[off + e]] == 0;
+    n_int = warp_sum(n_int);
+    if (n_int < D + 2) {
+        fl |= kDeficient;
+    } else if (n_int < 3 * n) {               // small stencils: the full test of the boundary WLS
+        double xb[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) xb[a] = x[i * D + a];
+        double B[n][n];
+#pragma unroll
+        for (int r = 0; r < n; ++r)
+#pragma unroll
+            for (int q = 0; q < n; ++q) B[r][q] = 0.0;
+        for (int e = lane; e < m; e += 32) {
+            const int j = nb_idx[off + e];
+            if (kind[j] != 0) continue;
+            double xj[3], Pv[n];
+            Pv[0] = 1.0;
+#pragma unroll
+            for (int a = 0; a < D; ++a) { xj[a] = x[(int64_t)j * D + a]; Pv[1 + a] = (xj[a] - xb[a]) * inv_h; }
+            const double w = exp(-alpha * dist2_rn<D>(xb, xj) / h2);
+#pragma unroll
+            for (int r = 0; r < n; ++r)
+#pragma unroll
+                for (int q = 0; q < n; ++q) B[r][q] += w * Pv[r] * Pv[q];
+        }
+#pragma unroll
+        for (int r = 0; r < n; ++r)
+#pragma unroll
+            for (int q = 0; q < n; ++q) B[r][q] = warp_sum(B[r][q]);
+        double Bi[n][n];
+        if (!(well_conditioned<n>(B) && small_inverse<n>(B, Bi))) fl |= kDeficient;
+    }
+    if (lane == 0 && fl) {
+        flag[i] = fl;
+        atomicAdd(counts, 1);
     }
 }
 
@@ -509,7 +530,11 @@ void decide_pass(bgk_ctx* c, cudaStream_t s) {
     cudaMemsetAsync(m.counts, 0, 4 * sizeof(int32_t), s);
     cudaMemsetAsync(m.status, 0, sizeof(int32_t) * N, s);
     k_mg_detect_w<D><<<(unsigned)((N + 7) / 8), 256, 0, s>>>(c->x, c->kind, N, c->g.nb_off, c->g.nb_idx, rm * rm,
-                                                             m_min, 1.0 / cf.h, cf.h2, cf.alpha_w, m.flag, m.counts);
+                                                             m_min, m.flag, m.counts);
+    if (c->N_b)
+        k_mg_detect_wall<D><<<(unsigned)((c->N_b + 7) / 8), 256, 0, s>>>(c->x, c->kind, c->boundary, c->N_b,
+                                                                          c->g.nb_off, c->g.nb_idx, 1.0 / cf.h, cf.h2,
+                                                                          cf.alpha_w, m.flag, m.counts);
     MgArgs A;
     A.x = c->x;
     A.kind = c->kind;
