@@ -2,6 +2,7 @@
 // sequence of one step (split into the three phases a velocity-sharded run
 // interleaves with its two all-reduces), copies and error reporting.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -154,8 +155,10 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
         if (c->rows_on) c->nwpp = std::max(c->nchunk, c->rows_nchunk) * c->ncg;
     }
     c->bnd_chunk = 256;
-    // k_bnd_interp_t chunks: 256 threads x NPT stored nodes (NPT = 4 in 3D, 2 in 2D)
-    c->bnd_nch = (int)((c->Ks + 256 * (c->d == 3 ? 4 : 2) - 1) / (256 * (c->d == 3 ? 4 : 2)));
+    // boundary interpolation chunks: 3D the tile kernel's per-wall plan of incoming nodes (bnd_plan),
+    // 2D k_bnd_interp_t's 256 threads x 2 stored nodes
+    if (c->d == 3) c->bnd_nch = std::max(1, bnd_plan(c, nullptr, nullptr, nullptr, c->bnd_nchw));
+    else c->bnd_nch = (int)((c->Ks + 511) / 512);
 }
 
 // particle-management scratch (only when cfg.manage): decision arrays over the capacity, the
@@ -226,16 +229,20 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     carve_manage(c, k);
     c->stage = k.take<double>(c->cfg.staging ? (size_t)N * c->nv * c->Kloc : 1);
     {
-        // boundary interpolation groups: 8 in 3D / 4 in 2D (ring kernel k_bnd_interp_t, C5 2.46 ms at 8
-        // against 2.91 at 4), or BGK_BND_G = 4 / 8
-        const char* e = getenv("BGK_BND_G");
-        c->bnd_g = e ? atoi(e) : (c->d == 3 ? 8 : 4);
-        if (c->bnd_g != 4 && c->bnd_g != 8) c->bnd_g = c->d == 3 ? 8 : 4;
+        // boundary interpolation groups: 3D face tiles of up to kBndTile members (install_lists; at most
+        // N / 8 + 64 groups, else runs of kBndTile), 2D 4 consecutive boundary particles
+        c->bnd_g = c->d == 3 ? kBndTile : 4;
         c->bu_cap = std::min(c->bnd_g * c->max_nb, 512);   // union rows per group (CAPACITY beyond)
-        const size_t ng = (size_t)N / c->bnd_g + 1;
+        c->bg_max = c->d == 3 ? N / 8 + 64 : N / c->bnd_g + 1;
+        const size_t ng = (size_t)c->bg_max;
+        c->bg_off = k.take<int32_t>(ng + 1);
         c->bu_j = k.take<int32_t>(ng * c->bu_cap);
         c->bu_w = k.take<double>(ng * c->bu_cap * c->bnd_g);
         c->bu_n = k.take<int32_t>(ng);
+        const size_t nt = c->d == 3 ? (size_t)2 * d * c->bnd_nch : 1;
+        c->bnd_chunks = k.take<BndChunk>(nt);
+        c->bnd_act_t = k.take<int32_t>(nt * (c->d == 3 ? kBndAct : 1));
+        c->bnd_act_s = k.take<int32_t>(nt * (c->d == 3 ? kBndAct : 1));
     }
     c->rows_p0 = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
     c->rows_stride = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
@@ -314,11 +321,63 @@ bgk_status bgk::install_lists(bgk_ctx* c, const int8_t* hk, const double* hx, cu
     });
     c->N_int = (int64_t)in.size();
     c->N_b = (int64_t)bd.size();
+    // 3D: face tiles for the boundary interpolation.  Within a wall the order above is (slow, fast)
+    // in-plane (x-walls (z, y), y-walls (z, x), z-walls (y, x)); rows are runs of one slow coordinate,
+    // a member's tile is (row / 4, position in its row / 4) -- 4 x 4 points on a lattice face -- and
+    // the wall's members are re-ordered tile by tile (stable).  A group is a tile's run, split into
+    // runs of kBndTile; if that gives more than bg_max groups, plain runs of kBndTile per wall.
+    std::vector<int32_t> goff{0};
+    if (d == 3) {
+        const double tol = 1e-9 * c->cfg.L;
+        std::vector<int32_t> tiled;
+        tiled.reserve(bd.size());
+        for (size_t i = 0; i < bd.size();) {
+            size_t j = i;
+            while (j < bd.size() && hk[bd[j]] == hk[bd[i]]) ++j;
+            const int ax = (hk[bd[i]] - 1) / 2, sa = ax == 2 ? 1 : 2;
+            std::vector<std::array<int64_t, 2>> key;
+            int64_t rs = 0, rf = 0;
+            for (size_t q = i; q < j; ++q) {
+                if (q > i) {
+                    if (std::fabs(hx[(int64_t)bd[q] * d + sa] - hx[(int64_t)bd[q - 1] * d + sa]) > tol) {
+                        ++rs;
+                        rf = 0;
+                    } else {
+                        ++rf;
+                    }
+                }
+                key.push_back({(rs / 4) * (int64_t)bd.size() + rf / 4, (int64_t)q});
+            }
+            std::stable_sort(key.begin(), key.end(),
+                             [](const std::array<int64_t, 2>& a, const std::array<int64_t, 2>& b) { return a[0] < b[0]; });
+            for (size_t q = 0; q < key.size(); ++q) {
+                tiled.push_back(bd[key[q][1]]);
+                const int run = (int)(tiled.size() - goff.back());
+                const bool last = q + 1 == key.size() || key[q + 1][0] != key[q][0];
+                if (last || run == kBndTile) goff.push_back((int32_t)tiled.size());
+            }
+            i = j;
+        }
+        if ((int64_t)goff.size() - 1 > c->bg_max) {          // fall back to runs of kBndTile per wall
+            goff.assign(1, 0);
+            for (size_t i = 0; i < bd.size();) {
+                size_t j = i;
+                while (j < bd.size() && hk[bd[j]] == hk[bd[i]]) ++j;
+                for (size_t q = i; q < j; q += kBndTile) goff.push_back((int32_t)std::min(j, q + kBndTile));
+                i = j;
+            }
+        } else {
+            bd.swap(tiled);
+        }
+        c->n_bg = (int64_t)goff.size() - 1;
+    }
     if (!make_tensor_maps(c)) return BGK_E_CUDA;
     cudaError_t e = cudaSuccess;
     if (!in.empty()) e = cudaMemcpyAsync(c->interior, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && !bd.empty())
         e = cudaMemcpyAsync(c->boundary, bd.data(), sizeof(int32_t) * bd.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && d == 3)
+        e = cudaMemcpyAsync(c->bg_off, goff.data(), sizeof(int32_t) * goff.size(), cudaMemcpyHostToDevice, s);
     // interior ids also serve as the initial processing order (the neighbour build re-sorts it)
     if (e == cudaSuccess && !in.empty())
         e = cudaMemcpyAsync(c->g.order, in.data(), sizeof(int32_t) * in.size(), cudaMemcpyHostToDevice, s);
@@ -401,6 +460,7 @@ bgk_status bgk_init_cloud(const bgk_config* cfg, const double* x, const int8_t* 
         if (hk[i] < 0 || hk[i] > 2 * c->d) { delete c; return BGK_E_INVALID_ARG; }
     {
         bgk_status st = install_lists(c, hk.data(), hx.data(), s);
+        if (st == BGK_OK) st = upload_bnd_plan(c, s);
         if (st != BGK_OK) { delete c; return st; }
     }
     const int64_t reset[4] = {0, 0, 0, 0};

@@ -31,6 +31,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes (or the
+// hint, in ns, expires) instead of re-issuing try_wait -- many warps spinning on their ring's barriers
+// saturated the pipe the barrier and TMA-completion updates go through (k_bnd_interp_s: XU pipe at
+// 100 %, 54 polls per k-step)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680)
+        : "memory");
+}
+
 // one elected lane of a fully active warp (elect.sync): the TMA operands it uses are warp-uniform,
 // so the compiler issues them from uniform registers without a per-lane serialisation loop
 __device__ __forceinline__ bool elect_one() {

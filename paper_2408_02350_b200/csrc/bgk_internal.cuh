@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/bgk.h"
 
 namespace bgk {
@@ -44,6 +46,20 @@ constexpr int kManageMaxNew = 4096;   // new particles (merges + inserts) per pa
 constexpr int kRowsG = 8;            // particles per lattice-row group (fixed-cloud transport)
 constexpr int kRowsR = BGK_ROWS_R;   // velocity nodes per lane along v_1 in the lattice-row kernel
 constexpr int kFoldR = 13;           // rows per lane of a folded column group (2 kFoldR >= n1)
+
+// 3D boundary interpolation over face tiles (relax.cu k_bnd_interp_s): a block stages one union row's
+// incoming nodes of a velocity chunk -- up to kBndSeg contiguous bulk-copy segments, at most
+// kBndStage stored nodes -- and applies it to up to kBndTile members; the chunk's incoming nodes
+// (at most kBndAct = 12 consumer warps x 64) are listed per wall by the host (bnd_plan)
+constexpr int kBndTile = 16;         // members per tile group (4 x 4 face-lattice points)
+constexpr int kBndSeg = 4;
+constexpr int kBndStage = 2048;
+constexpr int kBndAct = 768;
+constexpr int kBndGap = 64;          // an inactive run shorter than this stays inside a segment
+struct BndChunk {
+    int32_t nseg, slen, nact, pad;   // segments, staged nodes, listed nodes
+    int32_t src[kBndSeg], dst[kBndSeg], len[kBndSeg];   // stored node -> stage offset, node count (even)
+};
 struct Manage {
     uint8_t* flag;      // [Ncap] bit0: merge candidate (a j > i closer than r_merge), bit1: < m_min neighbours
     int32_t* status;    // [Ncap] 0 live, -1 removed (merged into its partner), q+1: slot holds merged particle q
@@ -86,7 +102,7 @@ struct bgk_ctx {
     int PD;                     // doubles of pair data per CSR entry
     int wls_order;              // 1 or 2 (second order adds the signed tail to the pair record)
     int R, nchunk, nslots, nwpp; // transport mapping
-    int bnd_chunk, bnd_nch;     // boundary node chunking
+    int bnd_chunk, bnd_nch;     // boundary node chunking (3D: chunks per wall of the tile kernel, max)
     bool geometry_valid;
     int fcur;
     // device buffers (carved from the caller's workspace)
@@ -108,13 +124,22 @@ struct bgk_ctx {
     unsigned long long* stab;  // [1] max_{i,k} sum_j |C_ijk| as ordered bits
     bgk::Manage mg;     // particle-management scratch (cfg.manage)
     double* stage;      // [Ncap][nv*Kloc] canonical input staging buffer (cfg.staging)
-    // grouped boundary interpolation (relax.cu, BGK_BND_G): union of bnd_g consecutive boundary
-    // particles' interior neighbours and the dense weight matrix, rebuilt with the geometry
-    int bnd_g;          // 0: per-particle kernel; 4 or 8
+    // grouped boundary interpolation (relax.cu): union of a group's interior neighbours and the dense
+    // weight matrix, rebuilt with the geometry.  2D: bnd_g = 4 consecutive boundary particles of the
+    // (wall, y, x) order.  3D: face tiles of up to kBndTile members of one wall (install_lists), member
+    // range bg_off[g] .. bg_off[g+1] of the boundary list
+    int bnd_g;          // members per group (2D 4; 3D kBndTile)
     int bu_cap;
+    int64_t bg_max;     // group capacity of the carved arrays
+    int64_t n_bg;       // groups (3D tiles)
+    int32_t* bg_off;    // [bg_max + 1] 3D: group g = boundary list positions bg_off[g] .. bg_off[g+1]-1
     int32_t* bu_j;      // [groups][bu_cap]
     double* bu_w;       // [groups][bu_cap][bnd_g]
     int32_t* bu_n;      // [groups]
+    int bnd_nchw[6];    // 3D: chunks of each wall (bnd_plan)
+    bgk::BndChunk* bnd_chunks;   // [2d][bnd_nch]
+    int32_t* bnd_act_t;          // [2d][bnd_nch][kBndAct] listed node: stored index
+    int32_t* bnd_act_s;          //                         and its stage offset
     cudaEvent_t ev_staged, ev_consumed;
     bool stage_pending;
     int64_t stage_N;        // N when the staged copy was enqueued
@@ -238,6 +263,11 @@ void launch_check_domain(bgk_ctx* c, cudaStream_t s);
 int transport_rows_per_thread(int d, int n1);
 
 bool make_tensor_maps(bgk_ctx* c);
+// 3D boundary tiles: the per-wall chunk plan of the incoming velocity nodes (host; returns the largest
+// chunk count, fills the tables when the vectors are given) and its upload
+int bnd_plan(const bgk_ctx* c, std::vector<BndChunk>* chunks, std::vector<int32_t>* act_t,
+             std::vector<int32_t>* act_s, int* nchw);
+bgk_status upload_bnd_plan(bgk_ctx* c, cudaStream_t s);
 // fixed-cloud lattice rows: host-side group detection on the cached geometry, and the kernel
 bgk_status build_rows(bgk_ctx* c, cudaStream_t s);
 void launch_transport_rows(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);

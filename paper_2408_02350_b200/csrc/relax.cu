@@ -395,23 +395,31 @@ constexpr int kBndChunk = 256;
 // (weight 0 if not its neighbour): fewer row loads for more FMAs.  Round 1 measured the per-particle
 // form at 3.20 ms on C5 and an __ldg union of 4 at 2.83-2.89 ms (both removed in round 2).
 // ---------------------------------------------------------------------------------------------
-template <int G>
+// TILE (3D): group g is the member range bg_off[g] .. bg_off[g+1] of the boundary list (face tiles,
+// install_lists).
+template <int G, bool TILE = false>
 __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ bids, int64_t nb,
+                                                   const int32_t* __restrict__ bg_off,
                                                    const int64_t* __restrict__ nb_off,
                                                    const int32_t* __restrict__ bidx, const double* __restrict__ bcw,
                                                    const int32_t* __restrict__ bcnt, int cap,
                                                    int32_t* __restrict__ bu_j, double* __restrict__ bu_w,
-                                                   int32_t* __restrict__ bu_n, int64_t* err) {
-    extern __shared__ int32_t keys[];                       // [2 n2]: sorted (j << 3 | q), then union slots
+                                                   int32_t* __restrict__ bu_n,
+                                                   int64_t* err) {
+    constexpr int QB = G > 8 ? 4 : 3;                       // member bits of a key
+    constexpr int QM = (1 << QB) - 1;
+    extern __shared__ int32_t keys[];                       // [2 n2]: sorted (j << QB | q), then union slots
     __shared__ int s_len[G + 1];
     __shared__ int s_n;
     const int64_t g = blockIdx.x;
+    const int64_t gb = TILE ? bg_off[g] : g * G;            // first member's position in the list
+    const int64_t ge = TILE ? bg_off[g + 1] : min(gb + G, nb);
     if (threadIdx.x == 0) {
         int tot = 0;
         for (int q = 0; q < G; ++q) {
             s_len[q] = tot;
-            const int64_t bi = g * G + q;
-            if (bi < nb) tot += bcnt[bids[bi]];
+            const int64_t bi = gb + q;
+            if (bi < ge) tot += bcnt[bids[bi]];
         }
         s_len[G] = tot;
     }
@@ -422,11 +430,11 @@ __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ b
     for (int i = threadIdx.x; i < n2; i += blockDim.x) keys[i] = INT_MAX;
     __syncthreads();
     for (int q = 0; q < G; ++q) {
-        const int64_t bi = g * G + q;
-        if (bi >= nb) break;
+        const int64_t bi = gb + q;
+        if (bi >= ge) break;
         const int b = bids[bi];
         const int64_t off = nb_off[b];
-        for (int i = threadIdx.x; i < bcnt[b]; i += blockDim.x) keys[s_len[q] + i] = (bidx[off + i] << 3) | q;
+        for (int i = threadIdx.x; i < bcnt[b]; i += blockDim.x) keys[s_len[q] + i] = (bidx[off + i] << QB) | q;
     }
     __syncthreads();
     for (int k = 2; k <= n2; k <<= 1)
@@ -450,8 +458,8 @@ __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ b
     int ubase = 0;
     for (int i0 = 0; i0 < tot; i0 += 256) {
         const int i = i0 + threadIdx.x;
-        const int j = i < tot ? keys[i] >> 3 : -1;
-        const bool first = i < tot && (i == 0 || (keys[i - 1] >> 3) != j);
+        const int j = i < tot ? keys[i] >> QB : -1;
+        const bool first = i < tot && (i == 0 || (keys[i - 1] >> QB) != j);
         const unsigned bal = __ballot_sync(0xffffffffu, first);
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         if (lane == 0) wcnt[wid] = __popc(bal);
@@ -471,7 +479,7 @@ __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ b
     }
     if (threadIdx.x == 0) {
         s_n = ubase;
-        if (ubase > cap) latch_error(err, BGK_E_CAPACITY, bids[g * G]);
+        if (ubase > cap) latch_error(err, BGK_E_CAPACITY, bids[gb]);
         bu_n[g] = ubase > cap ? 0 : ubase;
     }
     __syncthreads();
@@ -480,8 +488,8 @@ __global__ void __launch_bounds__(256) k_bnd_union(const int32_t* __restrict__ b
     for (int i = threadIdx.x; i < s_n * G; i += blockDim.x) W[i] = 0.0;
     __syncthreads();
     for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-        const int j = keys[i] >> 3, q = keys[i] & 7;
-        const int b = bids[g * G + q];
+        const int j = keys[i] >> QB, q = keys[i] & QM;
+        const int b = bids[gb + q];
         const int64_t off = nb_off[b];
         int lo = 0, hi = bcnt[b] - 1;                       // compacted lists are ascending in j
         while (lo < hi) {
@@ -628,6 +636,204 @@ __global__ void __launch_bounds__(256, MINB) k_bnd_interp_t(const int32_t* __res
         }
         const double tot = block_sum<256>(flux, sh);
         if (threadIdx.x == 0 && live[q]) wallpart[(g * G + q) * nch + blockIdx.y] = tot;
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// 3D boundary interpolation over face tiles (k_bnd_interp_s), on the FP64 tensor cores.  Block =
+// (tile group g of up to G = 16 members of ONE wall, chunk ch of that wall's plan).  The plan
+// (bnd_plan, host, once per context) lists for each wall the velocity nodes that can be incoming
+// (v.n <= 0) and cuts them into chunks of at most kBndAct nodes whose stored positions fit in
+// kBndSeg contiguous segments of at most kBndStage nodes -- only incoming nodes are computed and,
+// where they are contiguous runs (walls normal to v_1 or v_2), only their bytes are staged.
+// For the chunk the block computes the dense product
+//     F_b[member m][node n] = sum_u W[u][m] F[u][n]      (u = the group's union rows)
+// with mma.sync m16n8k4 f64: A = W^T (16 members x 4 union rows), B = 4 union rows x 8 listed nodes,
+// the 16 x 8 accumulator tile in registers; each of the 12 consumer warps owns 64 listed nodes
+// (8 tiles).  The ~70 % zero weights of a 4 x 4 tile's union cost tensor-pipe slots, not issue slots:
+// per 4 union rows a warp issues 8 MMAs against 4 x 64 predicated DFMAs + weight loads of the
+// DFMA form (2.1 ms on C5, latency-bound on the shared-memory loads feeding it).
+// The union rows (the chunk's segments + the row's 16 weights) stream through a ring of as many
+// stages as 192 KB holds (at most 32; the staged bytes per row differ 2x between walls): a producer
+// warp (warp 12) waits for a stage's "empty" mbarrier (one arrival per consumer warp) and its lanes
+// issue 6 rows' bulk copies at once on the stages' "full" mbarriers.  In a k-step lane l reads the
+// stage of union row u0 + (l & 3) only.  The flux partials reduce in a fixed order.
+// Measured on C5 (tools/phase_times.py; the line-group kernel k_bnd_interp_t took 2.44 ms): one lane
+// issuing the copies row after row ran ~800 cycles per row whatever the ring depth (2.1-2.5 ms; the
+// same per-thread issue limit shows in tools/probe/bulk_probe.cu), lanes issuing 6 rows at once
+// 1.61 ms with 32 stages -- copies alone 1.47 ms, the MMAs alone 1.27 ms.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mma_f64_16x8x4(double (&c)[4], double a0, double a1, double b) {
+    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0, %1, %2, %3}, {%4, %5}, {%6}, "
+                 "{%0, %1, %2, %3};"
+                 : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+                 : "d"(a0), "d"(a1), "d"(b));
+}
+
+constexpr int kBndWarps = 12;                                // consumer warps of k_bnd_interp_s
+static_assert(kBndWarps * 64 == kBndAct, "64 listed nodes per consumer warp");
+
+constexpr int kBndRing = 192 * 1024;                        // ring bytes of k_bnd_interp_s
+constexpr int kBndPR = 6;                                    // rows issued per producer iteration
+constexpr int kBndNSMax = 32;                                // ring stages at most
+
+__global__ void __launch_bounds__((kBndWarps + 1) * 32, 1) k_bnd_interp_s(const int32_t* __restrict__ bids,
+                                                         const int32_t* __restrict__ bg_off,
+                                                         const int8_t* __restrict__ kind,
+                                                         const int32_t* __restrict__ bu_j,
+                                                         const double* __restrict__ bu_w,
+                                                         const int32_t* __restrict__ bu_n, int cap,
+                                                         const BndChunk* __restrict__ chunks,
+                                                         const int32_t* __restrict__ act_t,
+                                                         const int32_t* __restrict__ act_s, double* __restrict__ f,
+                                                         double* __restrict__ wallpart, int nch, int n1, int ncol,
+                                                         int ncs, int c0, int64_t Ks, double vmax, double dv,
+                                                         int nsmax) {
+    constexpr int G = kBndTile;
+    static_assert(G == 16, "one m16 tile of members");
+    constexpr int NTILE = 8;                                  // 8-node MMA tiles per consumer warp
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + kBndRing);
+    uint64_t* empty = full + kBndNSMax;
+    int32_t* sJ = reinterpret_cast<int32_t*>(empty + kBndNSMax);   // [cap] union rows
+    __shared__ double red[kBndWarps][G];
+    const int64_t g = blockIdx.x;
+    const int ch = blockIdx.y, tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const int b0 = bg_off[g], nm = bg_off[g + 1] - b0;
+    const int w = kind[bids[b0]] - 1;                          // every member lies on this wall
+    const int axis = w / 2;
+    const double sgn = (w % 2 == 0) ? 1.0 : -1.0;
+    const int U = bu_n[g];
+    const int64_t cix = (int64_t)w * nch + ch;
+    const int nact = chunks[cix].nact;
+    // stage = the chunk's staged nodes + the row's weights; as many stages as the ring holds (the
+    // staged bytes per row differ 2x between walls: the ring keeps ~190 KB in flight for all)
+    const int FB = (chunks[cix].slen * (int)sizeof(double) + 127) / 128 * 128;
+    // stage stride = 64 (mod 128) bytes: the 4 stages a k-step reads (lanes with tig 0..3 at the same
+    // node offsets) fall on alternating bank halves -- 2 wavefronts per warp load instead of 4
+    const int SB = (FB + G * (int)sizeof(double) + 127) / 128 * 128 + 64;
+    const int NS = min(nsmax, kBndRing / SB);
+    if (U == 0 || nact == 0) {
+        if (tid < nm) wallpart[(int64_t)(b0 + tid) * nch + ch] = 0.0;
+        return;
+    }
+    for (int i = tid; i < U; i += blockDim.x) sJ[i] = bu_j[g * cap + i];
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            mbar_init(full + q, 1);
+            mbar_init(empty + q, kBndWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (wp == kBndWarps) {                                    // producer warp
+        // kBndPR rows per iteration, one lane per (row, piece): pieces 0 .. nseg-1 are the chunk's
+        // segments, piece kBndSeg the row's weights.  Issuing from many lanes at once matters: one
+        // lane issuing expect_tx + bulk copies row after row managed ~800 cycles per row whatever the
+        // size or ring depth (tools/probe/bulk_probe.cu: 3.0 TB/s at 8 KB per row), 4+ rows issued by
+        // parallel lanes stream at the DRAM rate (6.7-7.0 TB/s)
+        constexpr int PC = kBndSeg + 1;                       // pieces per row
+        const BndChunk* C = chunks + cix;
+        const int nseg = C->nseg;
+        const uint32_t txb = (uint32_t)C->slen * 8u + G * 8u;
+        const int pr = lane / PC, pc = lane - pr * PC;        // this lane's row in the batch, piece
+        const int sk = min(pc, kBndSeg - 1);
+        const int ssrc = C->src[sk], sdst = C->dst[sk];
+        const uint32_t slen = (uint32_t)C->len[sk] * 8u;
+        const bool active = pr < kBndPR && (pc < nseg || pc == kBndSeg);
+        for (int u0 = 0; u0 < U; u0 += kBndPR) {
+            const int u = u0 + pr;
+            const bool mine = active && u < U;
+            const int q = u % NS;
+            if (mine && u >= NS) mbar_wait_sleep(empty + q, (uint32_t)(u / NS - 1) & 1u);
+            if (mine && pc == 0) mbar_expect_tx(full + q, txb);
+            __syncwarp();
+            if (mine) {
+                unsigned char* st = sm + (size_t)q * SB;
+                if (pc < kBndSeg) bulk_load(st + (size_t)sdst * 8, f + (int64_t)sJ[u] * Ks + ssrc, slen, full + q);
+                else bulk_load(st + FB, bu_w + (g * cap + u) * G, G * 8u, full + q);
+            }
+            __syncwarp();
+        }
+    } else {
+        const int gq = lane >> 2, tig = lane & 3;
+        const int abase = wp * 64;                            // this warp's listed nodes
+        const int ntile = max(0, min(NTILE, (nact - abase + 7) / 8));   // tiles holding listed nodes
+        int so[NTILE];
+#pragma unroll
+        for (int j = 0; j < NTILE; ++j) {
+            const int a = abase + j * 8 + gq;
+            so[j] = a < nact ? act_s[cix * kBndAct + a] : 0;  // unlisted columns read a staged node
+        }
+        double acc[NTILE][4];
+#pragma unroll
+        for (int j = 0; j < NTILE; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+        for (int u0 = 0; u0 < U; u0 += 4) {
+            const int r = u0 + tig;                           // this lane's union row in the k-step
+            const bool live = r < U;
+            const double* st = reinterpret_cast<const double*>(sm + (size_t)(r % NS) * SB);
+            double a0 = 0.0, a1 = 0.0;
+            if (live) {
+                mbar_wait_sleep(full + r % NS, (uint32_t)(r / NS) & 1u);
+                a0 = st[FB / 8 + gq];
+                a1 = st[FB / 8 + gq + 8];
+            }
+            if (ntile == NTILE) {
+#pragma unroll
+                for (int j = 0; j < NTILE; ++j) mma_f64_16x8x4(acc[j], a0, a1, live ? st[so[j]] : 0.0);
+            } else {
+#pragma unroll
+                for (int j = 0; j < NTILE; ++j)
+                    if (j < ntile) mma_f64_16x8x4(acc[j], a0, a1, live ? st[so[j]] : 0.0);
+            }
+            __syncwarp();                                     // the warp is done with the 4 stages
+            if (lane < 4 && u0 + lane < U) mbar_arrive(empty + (u0 + lane) % NS);
+        }
+        // epilogue: acc[j] = members (gq, gq + 8) x listed nodes abase + 8 j + 2 tig + (0, 1)
+        double flux[2] = {0.0, 0.0};
+        const int64_t fm0 = gq < nm ? (int64_t)bids[b0 + gq] * Ks : -1;
+        const int64_t fm1 = gq + 8 < nm ? (int64_t)bids[b0 + gq + 8] * Ks : -1;
+#pragma unroll
+        for (int j = 0; j < NTILE; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int a = abase + j * 8 + 2 * tig + e;
+                if (a >= nact) continue;
+                const int64_t t = act_t[cix * kBndAct + a];
+                double v[3];
+                // the plan is a superset near v.n = 0; the device decides with the same expression as
+                // k_wall_M (incoming = not outgoing)
+                if (!node_vel_s<3>(t, ncs, ncol, c0, n1, vmax, dv, v) || !(sgn * v[axis] <= 0.0)) continue;
+                const double vn = sgn * v[axis];
+                if (fm0 >= 0) {
+                    f[fm0 + t] = acc[j][e];
+                    if (vn < 0.0) flux[0] += vn * acc[j][e];
+                }
+                if (fm1 >= 0) {
+                    f[fm1 + t] = acc[j][2 + e];
+                    if (vn < 0.0) flux[1] += vn * acc[j][2 + e];
+                }
+            }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            flux[h] += __shfl_xor_sync(0xffffffffu, flux[h], 1);
+            flux[h] += __shfl_xor_sync(0xffffffffu, flux[h], 2);
+        }
+        if (tig == 0) {
+            red[wp][gq] = flux[0];
+            red[wp][gq + 8] = flux[1];
+        }
+    }
+    __syncthreads();
+    if (tid < nm) {
+        double tot = 0.0;
+#pragma unroll
+        for (int k = 0; k < kBndWarps; ++k) tot += red[k][tid];
+        wallpart[(int64_t)(b0 + tid) * nch + ch] = tot;
     }
 }
 
@@ -787,19 +993,23 @@ void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s) {
     else k_relax<2><<<(unsigned)c->N_int, 256, smem, s>>>(a);
 }
 
-template <int G>
+template <int G, bool TILE>
 void bnd_union_g(bgk_ctx* c, cudaStream_t s) {
-    const unsigned ng = (unsigned)((c->N_b + G - 1) / G);
+    const unsigned ng = TILE ? (unsigned)c->n_bg : (unsigned)((c->N_b + G - 1) / G);
     int n2 = 1;
     while (n2 < G * c->max_nb) n2 <<= 1;
-    k_bnd_union<G><<<ng, 256, sizeof(int32_t) * 2 * n2, s>>>(c->boundary, c->N_b, c->g.nb_off, c->g.bidx, c->g.bcw,
-                                                           c->g.bcnt, c->bu_cap, c->bu_j, c->bu_w, c->bu_n, c->err);
+    const size_t smem = sizeof(int32_t) * 2 * n2;
+    static bool configured[kMaxDevices] = {};
+    if (smem > 48 * 1024 && first_use_on_device(configured))
+        cudaFuncSetAttribute(k_bnd_union<G, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_bnd_union<G, TILE><<<ng, 256, smem, s>>>(c->boundary, c->N_b, c->bg_off, c->g.nb_off, c->g.bidx, c->g.bcw,
+                                              c->g.bcnt, c->bu_cap, c->bu_j, c->bu_w, c->bu_n, c->err);
 }
 
 void launch_bnd_union(bgk_ctx* c, cudaStream_t s) {
     if (!c->N_b) return;
-    if (c->bnd_g == 4) bnd_union_g<4>(c, s);
-    else bnd_union_g<8>(c, s);
+    if (c->d == 3) bnd_union_g<kBndTile, true>(c, s);
+    else bnd_union_g<4, false>(c, s);
 }
 
 template <int D, int G, int NPT, int NS, int MINB = 2>
@@ -821,11 +1031,133 @@ void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
                                                                     c->wallnum);
 }
 
+// 3D: tiles of kBndTile members on the FP64 tensor cores, a 192 KB ring (one block of 12 consumer
+// warps + 1 producer warp per SM)
+void bnd_interp_s(bgk_ctx* c, double* fnew, cudaStream_t s) {
+    const size_t smem = kBndRing + 2 * kBndNSMax * sizeof(uint64_t) + (size_t)c->bu_cap * sizeof(int32_t);
+    static bool configured[kMaxDevices] = {};
+    if (first_use_on_device(configured))
+        cudaFuncSetAttribute(k_bnd_interp_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int nch = c->bnd_nch;
+    // ring stages at most (BGK_BND_NS, 8 .. 32; C5: 12 stages 2.12 ms, 32 stages 1.61 ms)
+    static const int nsmax = [] {
+        const char* e = getenv("BGK_BND_NS");
+        const int v = e ? atoi(e) : kBndNSMax;
+        return v >= 8 && v <= kBndNSMax ? v : kBndNSMax;
+    }();
+    dim3 gg((unsigned)c->n_bg, (unsigned)nch);
+    k_bnd_interp_s<<<gg, (kBndWarps + 1) * 32, smem, s>>>(c->boundary, c->bg_off, c->kind, c->bu_j, c->bu_w,
+                                                            c->bu_n, c->bu_cap, c->bnd_chunks, c->bnd_act_t,
+                                                            c->bnd_act_s, fnew, c->wallpart, nch, c->n1, c->ncol,
+                                                            c->ncs, c->c0, c->Ks, c->cfg.vmax, c->dv, nsmax);
+    k_wall_reduce<<<(unsigned)((c->N_b + 255) / 256), 256, 0, s>>>(c->boundary, c->N_b, c->wallpart, nch,
+                                                                    c->wallnum);
+}
+
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s) {
     if (!c->N_b) return;
-    // ring depth 6 (C5: 2.48 ms; 8 stages the same, 10 stages 3.82 ms -- one block per SM)
-    if (c->d == 3) (c->bnd_g == 4 ? bnd_interp_t<3, 4, 4, 6>(c, fnew, s) : bnd_interp_t<3, 8, 4, 6>(c, fnew, s));
+    if (c->d == 3) bnd_interp_s(c, fnew, s);
     else (c->bnd_g == 4 ? bnd_interp_t<2, 4, 2, 6>(c, fnew, s) : bnd_interp_t<2, 8, 2, 6>(c, fnew, s));
+}
+
+// The per-wall plan of the tile kernel's velocity chunks.  A node is listed for wall w if it is a
+// valid local node whose v.n is <= 0 up to 1e-9 dv (a superset of the device's incoming test, which
+// the kernel re-applies).  Listed nodes are taken in stored order; a listed node within kBndGap of
+// the current segment's end extends it (the gap is staged, not computed), otherwise it opens a new
+// segment; a chunk closes when it holds kBndAct nodes, kBndSeg segments or kBndStage staged nodes.
+// Segment starts and lengths are even (16-B bulk copies of fp64 rows whose stride Ks is even).
+int bnd_plan(const bgk_ctx* c, std::vector<BndChunk>* chunks, std::vector<int32_t>* act_t,
+             std::vector<int32_t>* act_s, int* nchw) {
+    const int nw = 2 * c->d;
+    const int64_t kA = 16;                      // segment alignment in nodes (128 B: whole L2 lines)
+    std::vector<std::vector<BndChunk>> per(nw);
+    std::vector<std::vector<int32_t>> pt(nw), ps(nw);
+    int mx = 0;
+    for (int w = 0; w < nw; ++w) {
+        const int axis = w / 2;
+        const double sgn = (w % 2 == 0) ? 1.0 : -1.0;
+        BndChunk cur{};
+        int64_t seg_end = -1;                   // stored end (exclusive, unrounded) of the open segment
+        auto close = [&]() {
+            if (cur.nact == 0) return;
+            const int k = cur.nseg - 1;
+            cur.len[k] = (int32_t)std::min<int64_t>(((seg_end - cur.src[k]) + kA - 1) / kA * kA, c->Ks - cur.src[k]);
+            cur.slen = cur.dst[k] + cur.len[k];
+            per[w].push_back(cur);
+            while ((int)pt[w].size() < (int)per[w].size() * kBndAct) {
+                pt[w].push_back(0);
+                ps[w].push_back(0);
+            }
+            cur = BndChunk{};
+            seg_end = -1;
+        };
+        for (int64_t t = 0; t < c->Ks; ++t) {
+            const int k1 = (int)(t / c->ncs), col = (int)(t - (int64_t)k1 * c->ncs);
+            if (col >= c->ncol) continue;
+            const int gc = c->c0 + col;
+            const int kk[3] = {k1, gc / c->n1, gc - (gc / c->n1) * c->n1};
+            const double va = -c->cfg.vmax + (double)kk[axis] * c->dv;
+            if (!(sgn * va <= 1e-9 * c->dv)) continue;
+            for (int pass = 0; pass < 2; ++pass) {
+                const bool extend = cur.nseg > 0 && t - seg_end < kBndGap;
+                const int64_t src = extend ? cur.src[cur.nseg - 1] : (t / kA * kA);
+                const int64_t dst = extend ? cur.dst[cur.nseg - 1]
+                                           : (cur.nseg > 0 ? cur.dst[cur.nseg - 1] +
+                                                                 ((seg_end - cur.src[cur.nseg - 1]) + kA - 1) / kA * kA
+                                                           : 0);
+                const int64_t stage_end = dst + (t + 1 - src) + kA - 1;   // + kA - 1: the round-up
+                const bool fits = cur.nact < kBndAct && stage_end <= kBndStage && (extend || cur.nseg < kBndSeg);
+                if (!fits) {
+                    close();
+                    continue;                       // second pass: a fresh chunk always fits
+                }
+                if (!extend) {
+                    if (cur.nseg > 0) cur.len[cur.nseg - 1] = (int32_t)(dst - cur.dst[cur.nseg - 1]);
+                    cur.src[cur.nseg] = (int32_t)src;
+                    cur.dst[cur.nseg] = (int32_t)dst;
+                    ++cur.nseg;
+                }
+                seg_end = t + 1;
+                pt[w].push_back((int32_t)t);
+                ps[w].push_back((int32_t)(dst + (t - src)));
+                ++cur.nact;
+                break;
+            }
+        }
+        close();
+        if (nchw) nchw[w] = (int)per[w].size();
+        mx = std::max(mx, (int)per[w].size());
+    }
+    if (chunks) {
+        const int nch = std::max(1, mx);
+        chunks->assign((size_t)nw * nch, BndChunk{});
+        act_t->assign((size_t)nw * nch * kBndAct, 0);
+        act_s->assign((size_t)nw * nch * kBndAct, 0);
+        for (int w = 0; w < nw; ++w)
+            for (size_t k = 0; k < per[w].size(); ++k) {
+                (*chunks)[(size_t)w * nch + k] = per[w][k];
+                for (int a = 0; a < per[w][k].nact; ++a) {
+                    (*act_t)[((size_t)w * nch + k) * kBndAct + a] = pt[w][k * kBndAct + a];
+                    (*act_s)[((size_t)w * nch + k) * kBndAct + a] = ps[w][k * kBndAct + a];
+                }
+            }
+    }
+    return mx;
+}
+
+bgk_status upload_bnd_plan(bgk_ctx* c, cudaStream_t s) {
+    if (c->d != 3) return BGK_OK;
+    std::vector<BndChunk> ch;
+    std::vector<int32_t> at, as;
+    bnd_plan(c, &ch, &at, &as, c->bnd_nchw);
+    if ((int64_t)ch.size() != (int64_t)2 * c->d * c->bnd_nch) return BGK_E_INVALID_ARG;
+    cudaError_t e = cudaMemcpyAsync(c->bnd_chunks, ch.data(), sizeof(BndChunk) * ch.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->bnd_act_t, at.data(), sizeof(int32_t) * at.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->bnd_act_s, as.data(), sizeof(int32_t) * as.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return e == cudaSuccess ? BGK_OK : BGK_E_CUDA;
 }
 
 void launch_boundary_fill(bgk_ctx* c, double* fnew, cudaStream_t s) {
