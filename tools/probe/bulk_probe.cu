@@ -42,6 +42,73 @@ __global__ void __launch_bounds__(416, 1) k_probe(const char* __restrict__ src, 
             }
             __syncwarp();
         }
+    } else if (wp == nconsumer && mode == 3) {      // row u issued by lane u % 32, one row at a time
+        for (int u = 0; u < nrow; ++u) {
+            const int q = u % NS;
+            if (lane == (u & 31)) {
+                if (u >= NS) mbar_wait(empty + q, (uint32_t)(u / NS - 1) & 1u);
+                mbar_expect_tx(full + q, (uint32_t)S);
+                const size_t off = ((size_t)(blockIdx.x * (size_t)nrow + u) * stride) % (nbytes - S - 4096);
+                bulk_load(sm + (size_t)q * SB, src + off / 128 * 128, S, full + q);
+            }
+            __syncwarp();
+        }
+    } else if (wp == nconsumer && mode == 8) {      // lanes 0,1 issue rows u, u+1 in one instruction, then 2x25x4 DFMA
+        double x0 = lane, x1 = lane + 1, x2 = lane + 2, x3 = lane + 3;
+        for (int u0 = 0; u0 < nrow; u0 += 2) {
+            const int u = u0 + lane;
+            const int q = u % NS;
+            if (lane < 2 && u < nrow) {
+                if (u >= NS) mbar_wait(empty + q, (uint32_t)(u / NS - 1) & 1u);
+                mbar_expect_tx(full + q, (uint32_t)S);
+                const size_t off = ((size_t)(blockIdx.x * (size_t)nrow + u) * stride) % (nbytes - S - 4096);
+                bulk_load(sm + (size_t)q * SB, src + off / 128 * 128, S, full + q);
+            }
+            __syncwarp();
+            for (int k = 0; k < 2 * P; ++k) {
+                x0 = fma(x0, 1.0000001, 0.5); x1 = fma(x1, 1.0000001, 0.5);
+                x2 = fma(x2, 1.0000001, 0.5); x3 = fma(x3, 1.0000001, 0.5);
+            }
+        }
+        if (x0 + x1 + x2 + x3 == 12345.0) full[0] = 1;
+    } else if (wp == nconsumer && mode == 9) {      // expect_tx for row u issued one row EARLY (separate), copy now
+        double x0 = lane, x1 = lane + 1, x2 = lane + 2, x3 = lane + 3;
+        if (lane == 0) mbar_expect_tx(full + 0, (uint32_t)S);
+        for (int u = 0; u < nrow; ++u) {
+            const int q = u % NS;
+            if (u >= NS) mbar_wait(empty + q, (uint32_t)(u / NS - 1) & 1u);
+            if (lane == 0) {
+                const size_t off = ((size_t)(blockIdx.x * (size_t)nrow + u) * stride) % (nbytes - S - 4096);
+                bulk_load(sm + (size_t)q * SB, src + off / 128 * 128, S, full + q);
+                const int q1 = (u + 1) % NS;
+                if (u + 1 < nrow) {
+                    if (u + 1 >= NS) mbar_wait(empty + q1, (uint32_t)((u + 1) / NS - 1) & 1u);
+                    mbar_expect_tx(full + q1, (uint32_t)S);
+                }
+            }
+            for (int k = 0; k < P; ++k) {
+                x0 = fma(x0, 1.0000001, 0.5); x1 = fma(x1, 1.0000001, 0.5);
+                x2 = fma(x2, 1.0000001, 0.5); x3 = fma(x3, 1.0000001, 0.5);
+            }
+        }
+        if (x0 + x1 + x2 + x3 == 12345.0) full[0] = 1;
+    } else if (wp == nconsumer && mode >= 5) {      // lane 0 issues a row, then ~P*4 dependent-free DFMAs per lane
+        double x0 = lane, x1 = lane + 1, x2 = lane + 2, x3 = lane + 3;
+        for (int u = 0; u < nrow; ++u) {
+            const int q = u % NS;
+            if (u >= NS) mbar_wait(empty + q, (uint32_t)(u / NS - 1) & 1u);
+            if (lane == 0 && mode != 6) {
+                mbar_expect_tx(full + q, (uint32_t)S);
+                const size_t off = ((size_t)(blockIdx.x * (size_t)nrow + u) * stride) % (nbytes - S - 4096);
+                bulk_load(sm + (size_t)q * SB, src + off / 128 * 128, S, full + q);
+            }
+            if (mode == 6 && lane == 0) mbar_arrive(full + q);
+            for (int k = 0; k < P; ++k) {
+                x0 = fma(x0, 1.0000001, 0.5); x1 = fma(x1, 1.0000001, 0.5);
+                x2 = fma(x2, 1.0000001, 0.5); x3 = fma(x3, 1.0000001, 0.5);
+            }
+        }
+        if (x0 + x1 + x2 + x3 == 12345.0) full[0] = 1;
     } else if (wp == nconsumer && mode == 2) {      // no wait on empty at all (NS >= nrow impossible) -> issue only
         for (int u = 0; u < nrow; ++u) {
             const int q = u % NS;
@@ -73,7 +140,9 @@ int main() {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     struct Cfg { int S, ncopy, NS; long stride; int mode, P; };
-    Cfg cfgs[] = {{8192, 1, 12, 128000, 0, 1}, {8192, 1, 12, 128000, 2, 1},
+    Cfg cfgs[] = {{8192, 1, 12, 128000, 5, 25}, {8192, 1, 12, 128000, 6, 25}, {8192, 1, 12, 128000, 8, 25},
+                  {8192, 1, 12, 128000, 9, 25}, {8192, 1, 12, 128000, 5, 100}, {8192, 1, 12, 128000, 8, 100},
+                  {8192, 1, 12, 128000, 9, 100},
                   {8192, 1, 20, 128000, 1, 4}, {8192, 1, 20, 128000, 1, 8}, {8192, 1, 24, 128000, 1, 12},
                   {4096, 1, 40, 128000, 1, 8}, {4096, 1, 40, 128000, 1, 16},
                   {16384, 1, 12, 128000, 1, 4}};
