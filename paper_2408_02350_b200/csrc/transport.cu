@@ -209,10 +209,11 @@ struct Stage {
     static constexpr uint32_t BYTES = (F_BYTES + P_BYTES + 127) / 128 * 128;
 };
 
-template <int D, int R, int NST, int WPB, bool SG, int XC = 0, int FD = 0>
+template <int D, int R, int NST, int WPB, bool SG, int XC = 0, int FD = 0, int MINB = 1>
 // minBlocks = 1 is explicit on purpose: with __launch_bounds__(64) alone ptxas capped the R = 25
-// instantiation at 164 registers (229 with it) and C5 transport went from 69 to 93 ms.
-__global__ void __launch_bounds__(WPB * 32, 1) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
+// instantiation at 164 registers (229 with it) and C5 transport went from 69 to 93 ms.  2D may ask
+// for more resident blocks (MINB: fewer registers, more warps per SM sub-partition).
+__global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
     static_assert(XC == 0 || (D == 2 && !SG && R <= 32), "extra column: 2D first order, one row per lane");
     static_assert(FD == 0 || (D == 3 && !SG && XC == 0), "folded group: 3D first order");
     using St = Stage<D, R, SG, XC, FD>;
@@ -544,27 +545,27 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
         transport_epilogue<3, R, false>(A, p0 + k * S, w, k1s, colc, gc, valid, Qf[k], Sc, Sa, Qt);
 }
 
-template <int D, int R, int WPB, bool SG, int XC = 0, int FD = 0>
+template <int D, int R, int WPB, bool SG, int XC = 0, int FD = 0, int MINB = 1>
 constexpr int stages_for() {
     // ring depth: keep NST-1 neighbour boxes in flight; bounded by 227 KB of shared memory
-    // (sized for 8 resident warps per SM: blocks of WPB warps)
-    constexpr int blocks = WPB >= 8 ? 1 : 8 / WPB;
-    constexpr int n = (220 * 1024) / (blocks * WPB * Stage<D, R, SG, XC, FD>::BYTES);
+    // (sized for max(8, MINB x WPB) resident warps per SM: blocks of WPB warps)
+    constexpr int warps = MINB * WPB > 8 ? MINB * WPB : 8;
+    constexpr int n = (220 * 1024) / (warps * Stage<D, R, SG, XC, FD>::BYTES);
     return n > 8 ? 8 : (n < 2 ? 2 : n);
 }
 
-template <int D, int R, int WPB, bool SG = false, int XC = 0, int FD = 0>
+template <int D, int R, int WPB, bool SG = false, int XC = 0, int FD = 0, int MINB = 1>
 void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
-    constexpr int NST = stages_for<D, R, WPB, SG, XC, FD>();
+    constexpr int NST = stages_for<D, R, WPB, SG, XC, FD, MINB>();
     constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG, XC, FD>::BYTES + WPB * NST * 8;
     static bool configured[kMaxDevices] = {};
     if (first_use_on_device(configured)) {
-        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, XC, FD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, XC, FD, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     }
     const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
     const unsigned gy = FD ? 1u : (unsigned)a.nw_grid;
-    k_transport<D, R, NST, WPB, SG, XC, FD><<<dim3(gx, gy), WPB * 32, smem, s>>>(tm, a);
+    k_transport<D, R, NST, WPB, SG, XC, FD, MINB><<<dim3(gx, gy), WPB * 32, smem, s>>>(tm, a);
 }
 
 template <int D, int R>
@@ -574,7 +575,18 @@ void launch_wpb(int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_t s) 
         if (wpb == 2) return launch_one<D, R, 2>(tm, a, s);
     }
     if constexpr (D == 2 && (R == 17 || R == 13 || R == 11 || R == 9)) {
-        if (a.xc) return launch_one<D, R, kDefaultWarps, false, 1>(tm, a, s);   // 33 columns
+        // resident 4-warp blocks per SM (BGK_TRANSPORT_MINB): 3 = 12 warps at <= 168 registers, 3 ring
+        // stages -- C2 transport at R = 11: 0.395 ms with 8 warps, 0.328 with 12 (R = 17, 8 warps: 0.349)
+        static const int minb = [] {
+            const char* e = getenv("BGK_TRANSPORT_MINB");
+            return e ? atoi(e) : 3;
+        }();
+        if (a.xc) {                                                              // 33 columns
+            if (minb == 2) return launch_one<D, R, kDefaultWarps, false, 1, 0, 2>(tm, a, s);
+            if (minb == 3) return launch_one<D, R, kDefaultWarps, false, 1, 0, 3>(tm, a, s);
+            if (minb == 4) return launch_one<D, R, kDefaultWarps, false, 1, 0, 4>(tm, a, s);
+            return launch_one<D, R, kDefaultWarps, false, 1>(tm, a, s);
+        }
     }
     launch_one<D, R, kDefaultWarps>(tm, a, s);
 }
@@ -633,6 +645,9 @@ int transport_rows_per_thread(int d, int n1) {
     const char* e = getenv("BGK_TRANSPORT_R");
     const int want = e ? atoi(e) : 0;
     if (d == 3) return listed(kRChoices3, want) ? want : fewest_padded(kRChoices3, n1);
+    // 2D, N_v = 32 (33 rows and columns: the XC mapping): three chunks of 11 rows with 12 warps per
+    // SM beat two of 17 with 8 (C2 transport 0.328 against 0.349 ms; R x warps sweep in DESIGN.md)
+    if (n1 == 33 && !listed(kRChoices2, want)) return 11;
     return listed(kRChoices2, want) ? want : fewest_padded(kRChoices2, n1);
 }
 
