@@ -106,3 +106,36 @@ def test_coarse_grid_degenerate_state_matches_oracle(torch_cuda):
         g.step(1)
         g.sync()
     assert ei.value.status == 4 and ei.value.particle == ref_bad
+
+
+@pytest.mark.parametrize("n, nv", [(10, 8), (9, 24)])
+def test_offlattice_wall_points_and_ragged_tiles(torch_cuda, n, nv):
+    """3D boundary interpolation on face tiles (k_bnd_interp_s): wall points moved along their face
+    (seeded, up to 0.3 dx; edges and corners stay) so no face row holds more than one point and every
+    tile is a ragged column of rows; n = 9 gives 7-wide faces (tiles of 4 and 3).  N_v = 24 is C5's
+    velocity grid (per-wall chunk plans of 11 chunks).  Five ALE steps against the oracle."""
+    cfg = bi.CavityConfig(f"offlat{n}_{nv}", 3, n, nv, dt=5e-12)
+    cloud = bi.make_cloud(cfg)
+    x, kind = cloud["x"].copy(), cloud["kind"]
+    rng = np.random.Generator(np.random.PCG64(2408023511))
+    dx = cfg.dx
+    on = np.stack([(np.abs(x[:, a]) < 1e-12 * cfg.L) | (np.abs(x[:, a] - cfg.L) < 1e-12 * cfg.L)
+                   for a in range(3)], axis=1)
+    face = (kind > 0) & (on.sum(axis=1) == 1)
+    for a in range(3):
+        sel = face & ~on[:, a]
+        x[sel, a] += rng.uniform(-0.3, 0.3, size=int(sel.sum())) * dx
+    cloud = dict(cloud, x=x)
+    cloud.update(zip(("rho", "U", "T"), bi.initial_fields(cfg, x)))
+    g = gpu(cfg, cloud)
+    g.step(5)
+    g.sync()
+    ref = oracle.run_steps(cfg, 5, cloud)
+    f = g.get_f().reshape(g.N, -1)
+    assert rel(f, ref.f) <= TOL, rel(f, ref.f)
+    rho, U, T = g.moments()
+    r0, u0, t0 = ref.moments()
+    assert np.abs(rho / r0 - 1).max() <= TOL
+    assert np.abs(U - u0).max() / SIG <= TOL
+    assert np.abs(T / t0 - 1).max() <= TOL
+    g.close()
