@@ -479,21 +479,23 @@ __global__ void __launch_bounds__(WPB * 32) k_transport_rows(const __grid_consta
         while (e1 < m && (snb[e1] >> 8) == (snb[e1 - 1] >> 8) + S && e1 - e0 + G <= kRowsMaxWin) ++e1;
         return e1;
     };
+    // The window's boxes and records are issued by parallel lanes (lane q: box q; lanes 16 + e: the
+    // run's records) after lane 0's expect_tx: one lane issuing ~12 copies in sequence held the warp
+    // for each (tools/probe/bulk_probe.cu: sequential issue ~500-800 cycles per copy)
     auto issue = [&](int e0, int e1, int b) {          // window + pair records of run [e0, e1) into buffer b
         const int nbox = e1 - e0 - 1 + G;
-        if (elect_one()) {
-            const uint32_t prec = (uint32_t)(e1 - e0) * PD * sizeof(double);
-            mbar_expect_tx(bars + b, (uint32_t)nbox * BOX + prec);
-            for (int q = 0; q < nbox; ++q)
-                tma_load_3d(win + b * BUF + q * BOX, &tmap, cg * ROW, k1s, (snb[e0] >> 8) + q * S, bars + b);
-            const int pe0 = snb[e0] & 255, pe1 = snb[e1 - 1] & 255;
-            if (pe1 - pe0 == e1 - 1 - e0) {                  // records contiguous in the CSR (x lines)
-                bulk_load(win + b * BUF + PREC, Pp + (int64_t)pe0 * PD, prec, bars + b);
-            } else {
-                for (int e = e0; e < e1; ++e)
-                    bulk_load(win + b * BUF + PREC + (e - e0) * PD * sizeof(double), Pp + (int64_t)(snb[e] & 255) * PD,
-                              PD * sizeof(double), bars + b);
-            }
+        const uint32_t prec = (uint32_t)(e1 - e0) * PD * sizeof(double);
+        if (lane == 0) mbar_expect_tx(bars + b, (uint32_t)nbox * BOX + prec);
+        __syncwarp();
+        if (lane < nbox)
+            tma_load_3d(win + b * BUF + lane * BOX, &tmap, cg * ROW, k1s, (snb[e0] >> 8) + lane * S, bars + b);
+        const int pe0 = snb[e0] & 255, pe1 = snb[e1 - 1] & 255;
+        if (pe1 - pe0 == e1 - 1 - e0) {                    // records contiguous in the CSR (x lines)
+            if (lane == 16) bulk_load(win + b * BUF + PREC, Pp + (int64_t)pe0 * PD, prec, bars + b);
+        } else if (lane >= 16 && lane - 16 < e1 - e0) {
+            const int e = e0 + lane - 16;
+            bulk_load(win + b * BUF + PREC + (e - e0) * PD * sizeof(double), Pp + (int64_t)(snb[e] & 255) * PD,
+                      PD * sizeof(double), bars + b);
         }
     };
     const double c1dv = axis_node(A.vmax, A.dv, k1s) / A.dv;   // W = 0 on a fixed cloud

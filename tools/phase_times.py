@@ -14,8 +14,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5_3d_40cube_Nv24")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--warmup", type=int, default=2)
+ap.add_argument("--fixed", action="store_true", help="fixed cloud (W = 0, geometry cached), no management")
 a = ap.parse_args()
 cfg = bi.CONFIGS[a.config]
+if a.fixed:
+    cfg = cfg.replace(ale=0, manage=0)
 g = Bgk(cfg, bi.make_cloud(cfg), device="cuda:0")
 g.step(a.warmup)
 try:
