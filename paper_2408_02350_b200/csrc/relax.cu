@@ -864,11 +864,34 @@ __global__ void __launch_bounds__(kBndChunk) k_bnd_fill(const int32_t* __restric
     // the wall table holds M(1, U_w, T_w) on the wall's outgoing nodes and -1 elsewhere (k_wall_M)
     (void)axis;
     (void)sgn;
-    for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
-        const double m0 = Mrow[t * NV];
-        if (m0 < 0.0) continue;
+    if constexpr (NV == 1) {
+        // 16-B pairs of stored nodes (Ks is even in 3D), four in flight per thread; a pair with one
+        // outgoing node writes that node alone
+        const double2* M2 = reinterpret_cast<const double2*>(Mrow);
+        double2* f2 = reinterpret_cast<double2*>(frow);
+        const int64_t np = Kloc / 2;
+        for (int64_t t0 = threadIdx.x; t0 < np; t0 += 4 * (int64_t)blockDim.x) {
+            double2 m[4];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) frow[t * NV + q] = rho_w * Mrow[t * NV + q];
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + u * (int64_t)blockDim.x;
+                m[u] = t < np ? __ldg(M2 + t) : make_double2(-1.0, -1.0);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t t = t0 + u * (int64_t)blockDim.x;
+                if (m[u].x >= 0.0 && m[u].y >= 0.0) f2[t] = make_double2(rho_w * m[u].x, rho_w * m[u].y);
+                else if (m[u].x >= 0.0) frow[2 * t] = rho_w * m[u].x;
+                else if (m[u].y >= 0.0) frow[2 * t + 1] = rho_w * m[u].y;
+            }
+        }
+    } else {
+        for (int64_t t = threadIdx.x; t < Kloc; t += blockDim.x) {
+            const double m0 = Mrow[t * NV];
+            if (m0 < 0.0) continue;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) frow[t * NV + q] = rho_w * Mrow[t * NV + q];
+        }
     }
 }
 
