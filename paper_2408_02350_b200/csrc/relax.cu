@@ -1059,8 +1059,9 @@ void bnd_interp_t(bgk_ctx* c, double* fnew, cudaStream_t s) {
 void bnd_interp_s(bgk_ctx* c, double* fnew, cudaStream_t s) {
     const size_t smem = kBndRing + 2 * kBndNSMax * sizeof(uint64_t) + (size_t)c->bu_cap * sizeof(int32_t);
     static bool configured[kMaxDevices] = {};
-    if (first_use_on_device(configured))
-        cudaFuncSetAttribute(k_bnd_interp_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (first_use_on_device(configured))      // opt in once for the largest union capacity (512 rows)
+        cudaFuncSetAttribute(k_bnd_interp_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kBndRing + 2 * kBndNSMax * sizeof(uint64_t) + 512 * sizeof(int32_t)));
     const int nch = c->bnd_nch;
     // ring stages at most (BGK_BND_NS, 8 .. 32; C5: 12 stages 2.12 ms, 32 stages 1.61 ms)
     static const int nsmax = [] {
