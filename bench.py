@@ -505,7 +505,10 @@ def run_ours(args):
         info = g2.transport_info()
         out["secondary"] = {"workload": cfg2.name + " fixed cloud (W = 0, geometry cached)", "ms_per_step": ms2,
                             "value": N * K / (ms2 / 1e3), "unit": UNIT, "steps": n2,
-                            "lattice_row_groups": info[2], "general_kernel_particles": info[3]}
+                            "lattice_row_groups": info[2], "general_kernel_particles": info[3],
+                            "deep_tiles": info[4], "deep_tile_particles": info[4] * 512,
+                            "hbm_gbs": 32.0 * N * K / (ms2 / 1e3) / 1e9,
+                            "hbm_frac": 32.0 * N * K / (ms2 / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0))}
         g2.close()
     if world == 1 and cfg.dims == 3 and not args.no_secondary:
         out["secondary_2d"] = [measure_2d(c2, dev, 50, 5, peaks) for c2 in (bi.C2, bi.C3)]

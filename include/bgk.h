@@ -292,9 +292,10 @@ bgk_status bgk_manage(bgk_ctx* ctx, int64_t* report, bgk_stream stream);
  * boundary (host pointers, each may be NULL), and the capacity. */
 bgk_status bgk_count(bgk_ctx* ctx, int64_t* N, int64_t* n_interior, int64_t* n_boundary, int64_t* capacity);
 
-/* Transport mapping in use (diagnostics): info[0] particles per warp (1 or 2), info[1] rows per
- * lane R of the general kernel, info[2] fixed-cloud lattice-row groups (8 particles each, 0 if
- * the lattice-row kernel is not used), info[3] interior particles left to the general kernel. */
+/* Transport mapping in use (diagnostics; info holds 5 values): info[0] particles per warp, info[1]
+ * rows per lane R of the general kernel, info[2] fixed-cloud lattice-row groups (8 particles each,
+ * 0 if the lattice-row kernel is not used), info[3] interior particles left to the general kernel,
+ * info[4] fixed-cloud deep-interior tiles (8 x 8 x 8 particles each, tiles.cu). */
 bgk_status bgk_transport_info(bgk_ctx* ctx, int64_t* info);
 
 /* Whole-step graph use (diagnostics, host int64[4]): info[0] 1 if graphs are enabled and usable,

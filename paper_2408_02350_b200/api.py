@@ -124,8 +124,9 @@ class Bgk:
         self._check(self.L.bgk_use_staged_f(self.ctx, self.stream))
 
     def transport_info(self):
-        """(particles per warp, rows per lane, lattice-row groups, particles left to the general kernel)."""
-        v = np.zeros(4, dtype=np.int64)
+        """(particles per warp, rows per lane, lattice-row groups, particles left to the general kernel,
+        deep-interior tiles of 512 particles)."""
+        v = np.zeros(5, dtype=np.int64)
         self._check(self.L.bgk_transport_info(self.ctx, _ptr(v)))
         return tuple(int(q) for q in v)
 

@@ -248,6 +248,8 @@ size_t carve(bgk_ctx* c, char* base, bool dry) {
     c->rows_stride = k.take<int32_t>(c->rows_on ? (size_t)N / kRowsG + 1 : 1);
     c->rows_perm = k.take<int16_t>(c->rows_on ? ((size_t)N / kRowsG + 1) * 256 : 1);
     c->order_rest = k.take<int32_t>(c->rows_on ? (size_t)N : 1);
+    c->tile_org = k.take<int32_t>(c->rows_on ? ((size_t)N / 512 + 1) * 3 : 1);
+    c->ctab = k.take<double>(c->rows_on ? (size_t)123 * c->Ks : 1);
     return k.off + 256;
 }
 
@@ -757,6 +759,7 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
     if (c->cfg.ale && c->cfg.manage && c->graph_ok && c->ncol == c->ncol_g)
         k += 3;                  // graph steps: the two conditional gates and the step counter (graph.cu)
     if (c->N_int) k += 3 + (c->fold ? 1 : 0);   // transport (+ the folded group), moment reduce, relax
+    if (c->rows_built) k += (c->n_tiles > 0) + (c->n_rows > 0) - (c->n_rest == 0);   // fixed cloud
     if (c->N_b) k += 3;          // boundary interp, wall reduce, fill
     *n = k;
     return BGK_OK;
@@ -851,6 +854,7 @@ bgk_status bgk_transport_info(bgk_ctx* c, int64_t* info) {
     info[1] = c->R;
     info[2] = c->rows_built ? c->n_rows : 0;
     info[3] = c->rows_built ? c->n_rest : c->N_int;
+    info[4] = c->rows_built ? c->n_tiles : 0;
     return BGK_OK;
 }
 

@@ -156,6 +156,14 @@ struct bgk_ctx {
     int32_t* rows_stride;   // [Ncap / kRowsG] index step between the group's particles (x, y or z line)
     int16_t* rows_perm;     // [Ncap / kRowsG][256] p0's neighbour entries in run order
     int32_t* order_rest;// [Ncap] the rest, in cell order
+    // fixed cloud, deep lattice interior as a 3D stencil (tiles.cu): 8 x 8 x 8 tiles of particles whose
+    // stencil is the 122-offset ball; C'_delta(k) tabulated once per cached geometry
+    int n_tiles;        // tiles in use (0: none)
+    int tile_nlat;      // lattice points per axis (particle = ix + n iy + n^2 iz)
+    int32_t* tile_org;  // [Ncap / 512 + 1][3] lattice index of each tile's first particle
+    double* ctab;       // [123][Ks] C'_delta(k) of the 122 offsets, then S(k)
+    CUtensorMap tmap_halo[2];   // f[b] as {Ks, n, n, n}, box {4, 15, 14, 14}
+    CUtensorMap tmap_ctab;      // ctab as {Ks, 123}, box {4, 123}
     int rows_nchunk;    // velocity chunks of kRowsR nodes along v_1
     // whole-step CUDA graphs (graph.cu): one executable per buffer parity, rebuilt when the key changes
     bool graph_ok;                 // graphs usable (BGK_GRAPH != 0, conditional nodes available)
@@ -271,6 +279,13 @@ bgk_status upload_bnd_plan(bgk_ctx* c, cudaStream_t s);
 // fixed-cloud lattice rows: host-side group detection on the cached geometry, and the kernel
 bgk_status build_rows(bgk_ctx* c, cudaStream_t s);
 void launch_transport_rows(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
+// tiles.cu: the deep-interior stencil of a fixed lattice cloud
+bool tile_ball_order(const int64_t* offsets_dxdydz, int m);
+bool make_tile_maps(bgk_ctx* c);
+void launch_tile_ctab(bgk_ctx* c, int64_t off_ref, cudaStream_t s);
+void launch_transport_tile(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
+int tile_particles();
+int tile_ranges(const bgk_ctx* c);
 // storage index of local node t = k1*ncol + col  ->  k1*ncs + col
 __host__ __device__ __forceinline__ int64_t stored_node(int64_t t, int ncol, int ncs) {
     const int64_t k1 = t / ncol;

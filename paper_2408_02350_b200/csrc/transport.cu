@@ -727,8 +727,9 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.ncg_l = c->ncg;
     a.cg_fold = 0;
     const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
-    if (c->rows_built && c->n_rows > 0) {          // fixed-cloud lattice rows + the general kernel on the rest
-        launch_transport_rows(c, fin, fout, s);
+    if (c->rows_built && (c->n_rows > 0 || c->n_tiles > 0)) {   // fixed cloud: deep tiles, lattice rows,
+        launch_transport_tile(c, fin, fout, s);                   // the general kernel on the rest
+        if (c->n_rows > 0) launch_transport_rows(c, fin, fout, s);
         if (c->n_rest == 0) return;
         a.order = c->order_rest;
         a.n_int = c->n_rest;
@@ -796,6 +797,57 @@ bgk_status build_rows(bgk_ctx* c, cudaStream_t s) {
     // lines along x, then y, then z (index steps 1, n, n^2 on the lattice: n points per axis)
     const int64_t n_axis = (int64_t)std::llround(c->cfg.L / dx) + 1;
     std::vector<char> grouped(N, 0);
+    // the deep lattice interior first: 8 x 8 x 8 tiles whose particles all carry the 122-offset ball
+    // (tiles.cu); needs the whole cloud to be the lattice with particle = ix + n iy + n^2 iz
+    c->n_tiles = 0;
+    {
+        static const bool tiles_env = [] {
+            const char* ev = getenv("BGK_TILES");
+            return !(ev && atoi(ev) == 0);
+        }();
+        const int64_t nl = n_axis;
+        bool lattice = tiles_env && d == 3 && N == nl * nl * nl && nl >= 14 && c->ncol == c->ncol_g;
+        for (int64_t p = 0; lattice && p < N; ++p) {
+            const int64_t id[3] = {p % nl, (p / nl) % nl, p / (nl * nl)};
+            for (int a = 0; a < 3; ++a)
+                if (std::fabs(x[p * 3 + a] - (double)id[a] * dx) > 1e-9 * dx) lattice = false;
+        }
+        const int64_t pref = 3 + 3 * nl + 3 * nl * nl;
+        if (lattice) {
+            const int64_t m = off[pref + 1] - off[pref];
+            std::vector<int64_t> o(3 * std::max<int64_t>(m, 1));
+            for (int64_t e2 = 0; e2 < m; ++e2)
+                for (int a = 0; a < 3; ++a)
+                    o[3 * e2 + a] = std::llround((x[nb[off[pref] + e2] * 3 + a] - x[pref * 3 + a]) / dx);
+            lattice = tile_ball_order(o.data(), (int)m);
+        }
+        std::vector<int32_t> org;
+        const int64_t nt = lattice ? (nl - 6) / 8 : 0;
+        for (int64_t tz = 0; tz < nt; ++tz)
+            for (int64_t ty = 0; ty < nt; ++ty)
+                for (int64_t tx = 0; tx < nt; ++tx) {
+                    const int64_t x0 = 3 + 8 * tx, y0 = 3 + 8 * ty, z0 = 3 + 8 * tz;
+                    bool ok = true;
+                    for (int64_t k = 0; ok && k < 512; ++k) {
+                        const int64_t q = (x0 + (k & 7)) + nl * (y0 + ((k >> 3) & 7)) + nl * nl * (z0 + (k >> 6));
+                        ok = kind[q] == 0 && same_stencil(pref, q, q - pref);
+                    }
+                    if (!ok) continue;
+                    org.push_back((int32_t)x0);
+                    org.push_back((int32_t)y0);
+                    org.push_back((int32_t)z0);
+                    for (int64_t k = 0; k < 512; ++k)
+                        grouped[(x0 + (k & 7)) + nl * (y0 + ((k >> 3) & 7)) + nl * nl * (z0 + (k >> 6))] = 1;
+                }
+        if (!org.empty()) {
+            c->tile_nlat = (int)nl;
+            if (cudaMemcpy(c->tile_org, org.data(), sizeof(int32_t) * org.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+                !make_tile_maps(c))
+                return BGK_E_CUDA;
+            launch_tile_ctab(c, off[pref], s);
+            c->n_tiles = (int)(org.size() / 3);
+        }
+    }
     std::vector<int32_t> p0s, strides;
     std::vector<int16_t> perms;
     static const int axes = [] {

@@ -388,14 +388,16 @@ def test_staged_input_matches_set_f(torch_cuda):
 # ------------------------------------ fixed-cloud lattice rows (SURVEY §8(d) lever)
 @pytest.mark.parametrize("cfg", [bi.C4.replace(ale=0), bi.CavityConfig("C4r", 3, 24, 8, ale=0)])
 def test_lattice_rows_fixed_cloud(torch_cuda, cfg, monkeypatch):
-    """Fixed cloud on the lattice: groups of 8 x-consecutive particles with identical stencils
-    share coefficients and boxes (k_transport_rows); the rest runs the general kernel.  Same
-    oracle bar, and the same state as the general kernel alone (BGK_TRANSPORT_ROWS=0) to 1e-13."""
+    """Fixed cloud on the lattice: 8 x 8 x 8 tiles of the deep interior run the tabulated 122-point
+    stencil (k_transport_tile), groups of 8 line-consecutive particles with identical stencils share
+    coefficients and boxes (k_transport_rows), the rest runs the general kernel.  Same oracle bar,
+    and the same state as the general kernel alone (BGK_TRANSPORT_ROWS=0) to 1e-13."""
     g, cloud = gpu(cfg)
     g.step(10)
     g.sync()
     info = g.transport_info()
-    assert info[2] > 0 and info[2] * 8 + info[3] == int((cloud["kind"] == 0).sum()), info
+    assert info[2] > 0 and info[4] > 0, info
+    assert info[2] * 8 + info[3] + info[4] * 512 == int((cloud["kind"] == 0).sum()), info
     check_state(g, oracle_run(cfg, 10), cfg)
     monkeypatch.setenv("BGK_TRANSPORT_ROWS", "0")
     h, _ = gpu(cfg, cloud)
