@@ -132,6 +132,10 @@ void derive(bgk_ctx* c, const bgk_config* cfg, int64_t N) {
                 ? 1
                 : 0;
     if (c->xc) c->ncg = 1;
+    {
+        const char* e = getenv("BGK_FUSE");
+        c->fuse2 = (c->xc && c->R == 11 && c->n1 == 33 && c->ncol == c->ncol_g && !(e && atoi(e) == 0)) ? 1 : 0;
+    }
     c->nwpp = c->nchunk * c->ncg;
     // 3D: a last column group of at most 16 columns (e.g. 78-79 columns per rank at P = 8 on C5) runs
     // folded -- 16 columns x two halves of v_1 in one warp -- instead of a full-width pass with half
@@ -618,8 +622,15 @@ bgk_status bgk_step(bgk_ctx* c, int n_steps, bgk_stream stream) {
     for (int n = 0; n < n_steps; ++n) {
         if (graph_step(c, S(stream))) continue;         // the whole step as one graph launch (graph.cu)
         bgk_status st;
-        if ((st = bgk_step_transport(c, stream)) != BGK_OK) return st;
-        if ((st = bgk_step_relax(c, stream)) != BGK_OK) return st;
+        if (c->fuse2) {                                  // 2D XC: transport + relaxation in one kernel
+            if ((st = bgk_run_phase(c, BGK_PHASE_GEOMETRY, stream)) != BGK_OK) return st;
+            launch_transport_fused(c, c->f[c->fcur], c->f[1 - c->fcur], S(stream));
+            if ((st = check_launch(c)) != BGK_OK) return st;
+            if ((st = bgk_run_phase(c, BGK_PHASE_BOUNDARY_INTERP, stream)) != BGK_OK) return st;
+        } else {
+            if ((st = bgk_step_transport(c, stream)) != BGK_OK) return st;
+            if ((st = bgk_step_relax(c, stream)) != BGK_OK) return st;
+        }
         if ((st = bgk_step_boundary(c, stream)) != BGK_OK) return st;
     }
     return BGK_OK;
@@ -758,7 +769,8 @@ bgk_status bgk_launches_per_step(bgk_ctx* c, int64_t* n) {
         k += 2 + (c->N_b ? 1 : 0);     // neighbour rebuild in the rare steps where the cloud changes)
     if (c->cfg.ale && c->cfg.manage && c->graph_ok && c->ncol == c->ncol_g)
         k += 3;                  // graph steps: the two conditional gates and the step counter (graph.cu)
-    if (c->N_int) k += 3 + (c->fold ? 1 : 0);   // transport (+ the folded group), moment reduce, relax
+    if (c->N_int) k += c->fuse2 ? 1 : 3 + (c->fold ? 1 : 0);   // transport (+ the folded group), moment
+                                                                 // reduce, relax -- or the fused kernel
     if (c->rows_built) k += (c->n_tiles > 0) + (c->n_rows > 0) - (c->n_rest == 0);   // fixed cloud
     if (c->N_b) k += 3;          // boundary interp, wall reduce, fill
     *n = k;

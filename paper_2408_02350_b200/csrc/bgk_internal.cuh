@@ -89,6 +89,7 @@ struct bgk_ctx {
     int64_t Ncap;                      // particle capacity of the workspace (>= N; management inserts)
     int ncg;                           // 32-column groups per chunk (transport)
     int xc;                            // 2D, 33 columns: column 32 rides in the group's box (k_transport XC)
+    int fuse2;                         // 2D XC, single rank: bgk_step runs transport + relaxation fused
     CUtensorMap tmap[2];               // TMA descriptors of f[0], f[1] viewed as [N][n1][ncs*nv] fp64
     CUtensorMap tmap_rows[2];          //   the same with the lattice-row kernel's box {32, kRowsR, 1}
     CUtensorMap tmap_fold[2];          //   the folded last group's box {16, 2 kFoldR, 1} (fold)
@@ -256,6 +257,8 @@ void launch_wls_export(bgk_ctx* c, double* rot, double* frames, cudaStream_t s);
 void launch_wls_interior(bgk_ctx* c, cudaStream_t s);
 void launch_wls_boundary(bgk_ctx* c, cudaStream_t s);
 void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
+// 2D, 33 columns, single rank (c->fuse2): transport + moments + relaxation in one kernel
+void launch_transport_fused(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s);
 void launch_moment_reduce(bgk_ctx* c, cudaStream_t s);
 void launch_relax(bgk_ctx* c, double* fnew, cudaStream_t s);
 void launch_boundary_interp(bgk_ctx* c, double* fnew, cudaStream_t s);

@@ -90,9 +90,13 @@ void geometry_tail(bgk_ctx* c, cudaStream_t s) {
 // transport .. boundary fill with the current parity (fcur is flipped by the caller)
 void phases(bgk_ctx* c, cudaStream_t s) {
     double* fn = c->f[1 - c->fcur];
-    launch_transport(c, c->f[c->fcur], fn, s);
-    launch_moment_reduce(c, s);
-    launch_relax(c, fn, s);
+    if (c->fuse2) {
+        launch_transport_fused(c, c->f[c->fcur], fn, s);
+    } else {
+        launch_transport(c, c->f[c->fcur], fn, s);
+        launch_moment_reduce(c, s);
+        launch_relax(c, fn, s);
+    }
     launch_boundary_interp(c, fn, s);
     launch_boundary_fill(c, fn, s);
 }

@@ -37,6 +37,7 @@
 
 #include "async.cuh"
 #include "bgk_internal.cuh"
+#include "relax_params.cuh"
 
 namespace bgk {
 
@@ -188,6 +189,106 @@ __device__ __forceinline__ void transport_epilogue(const TArgs& A, int p, int w,
     }
 }
 
+// 2D, 33 columns (XC = 1), single rank: transport and relaxation fused (the north star's "fused
+// transport+relaxation kernel").  A block of nchunk warps owns one particle
+// (warp w: rows w R .. w R + R of all 33 columns), so after the rows every node of the particle is in
+// the block's registers: the warps' moment partials meet in shared memory in chunk order (the same
+// fixed-order sums k_moment_reduce forms), one thread turns them into rho, U, T, tau and the relaxation
+// weights (relax_params, the unfused kernels' code), the block tabulates the separable Maxwellian's
+// 2 x 33 exponentials, and each lane writes f^{n+1} = (tau ftilde + dt M) / (tau + dt) straight from
+// its registers -- ftilde never goes to memory and the moment-sum and relaxation launches disappear.
+template <int R, int NCH>
+__device__ __forceinline__ void fused_epilogue2(const TArgs& A, const RelaxArgs& RA, int p, int wib, int k1s,
+                                                const double (&Qf)[R][2], const double (&Sc)[R],
+                                                const double (&Qt)[3]) {
+    __shared__ double part[NCH][kPM];
+    __shared__ double par[8];
+    __shared__ double ex[2][64];
+    const int lane = threadIdx.x & 31;
+    const int64_t rowstride = (int64_t)A.ncs * 2;
+    const double* fi = A.f + (int64_t)p * A.n1 * rowstride + (int64_t)k1s * rowstride + lane * 2;
+    double* fo = A.ft + (int64_t)p * A.n1 * rowstride + (int64_t)k1s * rowstride + lane * 2;
+    const double v2v = axis_node(A.vmax, A.dv, A.c0 + lane);
+    const double dtq = 2.0 * A.dt;
+    double out[R][2];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, sE = 0.0, amax = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        out[r][0] = out[r][1] = 0.0;
+        if (k1s + r >= A.n1) break;
+        const double v1 = axis_node(A.vmax, A.dv, k1s + r);
+        const double2 fv = __ldg(reinterpret_cast<const double2*>(fi + r * rowstride));
+        out[r][0] = fv.x - dtq * (Qf[r][0] - fv.x * Sc[r]);
+        out[r][1] = fv.y - dtq * (Qf[r][1] - fv.y * Sc[r]);
+        s0 += out[r][0];
+        s1 += v1 * out[r][0];
+        s2 += v2v * out[r][0];
+        sE += (v1 * v1 + v2v * v2v) * out[r][0];
+        sE += out[r][1];
+        amax = fmax(amax, -2.0 * Sc[r]);
+    }
+    const int kr = k1s + lane;                                 // the extra column's node of this lane
+    double ot[2] = {0.0, 0.0};
+    const bool xl = lane < R && kr < A.n1;
+    const int64_t ot_off = ((int64_t)p * A.n1 + kr) * rowstride + 64;
+    if (xl) {
+        const double2 fv = __ldg(reinterpret_cast<const double2*>(A.f + ot_off));
+        ot[0] = fv.x - dtq * (Qt[0] - fv.x * Qt[2]);
+        ot[1] = fv.y - dtq * (Qt[1] - fv.y * Qt[2]);
+        const double v1 = axis_node(A.vmax, A.dv, kr), v2 = axis_node(A.vmax, A.dv, A.c0 + 32);
+        s0 += ot[0];
+        s1 += v1 * ot[0];
+        s2 += v2 * ot[0];
+        sE += (v1 * v1 + v2 * v2) * ot[0] + ot[1];
+        amax = fmax(amax, -2.0 * Qt[2]);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    sE = warp_sum(sE);
+    amax = warp_max(amax);
+    if (lane == 0) {
+        part[wib][0] = s0;
+        part[wib][1] = s1;
+        part[wib][2] = s2;
+        part[wib][3] = sE;
+        part[wib][4] = 0.0;
+        atomicMax(A.stab, (unsigned long long)__double_as_longlong(amax));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum[kPM];
+#pragma unroll
+        for (int k = 0; k < kPM; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int w = 0; w < NCH; ++w) acc += part[w][k];   // chunk order, as k_moment_reduce
+            sum[k] = acc;
+        }
+        relax_params<2>(RA, sum, p, par);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 2 * A.n1; t += blockDim.x) {   // separable Maxwellian (k_relax_w2)
+        const int a = t / A.n1, j = t - a * A.n1;
+        const double dvel = axis_node(A.vmax, A.dv, j) - par[5 + a];
+        ex[a][j] = exp(-dvel * dvel * par[4]);
+    }
+    __syncthreads();
+    const double a1 = par[0], a2 = par[1], pref = par[2], RT = par[3];
+    const double e1 = ex[1][A.c0 + lane];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (k1s + r >= A.n1) break;
+        const double M = pref * ex[0][k1s + r] * e1;
+        *reinterpret_cast<double2*>(fo + r * rowstride) =
+            make_double2(a1 * out[r][0] + a2 * M, a1 * out[r][1] + a2 * (RT * M));
+    }
+    if (xl) {
+        const double M = pref * ex[0][kr] * ex[1][A.c0 + 32];
+        *reinterpret_cast<double2*>(A.ft + ot_off) = make_double2(a1 * ot[0] + a2 * M, a1 * ot[1] + a2 * (RT * M));
+    }
+}
+
 // One ring stage: the neighbour's box of f (R rows x 32 columns x nv) and its pair data P_e.
 // SG (second-order WLS): the pair record carries s_n = -sign(abar) after the first-order fields,
 // and C's n-term is y_n + s_n |y_n| (abar may be negative; P:408-410 applied literally).
@@ -209,11 +310,12 @@ struct Stage {
     static constexpr uint32_t BYTES = (F_BYTES + P_BYTES + 127) / 128 * 128;
 };
 
-template <int D, int R, int NST, int WPB, bool SG, int XC = 0, int FD = 0, int MINB = 1>
+template <int D, int R, int NST, int WPB, bool SG, int XC = 0, int FD = 0, int MINB = 1, bool FUSE = false>
 // minBlocks = 1 is explicit on purpose: with __launch_bounds__(64) alone ptxas capped the R = 25
 // instantiation at 164 registers (229 with it) and C5 transport went from 69 to 93 ms.  2D may ask
 // for more resident blocks (MINB: fewer registers, more warps per SM sub-partition).
-__global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A) {
+__global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_constant__ CUtensorMap tmap, const TArgs A,
+                                                             const RelaxArgs RA) {
     static_assert(XC == 0 || (D == 2 && !SG && R <= 32), "extra column: 2D first order, one row per lane");
     static_assert(FD == 0 || (D == 3 && !SG && XC == 0), "folded group: 3D first order");
     using St = Stage<D, R, SG, XC, FD>;
@@ -238,10 +340,11 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
     // indexing below keeps the running stage offset g0 so items could be chained.)
     const uint32_t g0 = 0;
     {
-    const int64_t pos = (int64_t)blockIdx.x * WPB + wib;
+    // FUSE: the block's warps are the chunks of ONE particle (block-uniform exit)
+    const int64_t pos = FUSE ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * WPB + wib;
     if (pos >= A.n_int) return;                           // warp-uniform
-    const int chunk = FD ? 0 : (int)blockIdx.y / A.ncg_l;
-    const int cg = FD ? A.cg_fold : (int)blockIdx.y - chunk * A.ncg_l;
+    const int chunk = FUSE ? wib : (FD ? 0 : (int)blockIdx.y / A.ncg_l);
+    const int cg = FUSE ? 0 : (FD ? A.cg_fold : (int)blockIdx.y - chunk * A.ncg_l);
     const int w = chunk * A.ncg + cg;                     // partial slot of (chunk, group)
     const int p = A.order[pos];
     const int cl = FD ? (lane & 15) : lane;               // column within the group
@@ -397,7 +500,12 @@ __global__ void __launch_bounds__(WPB * 32, MINB) k_transport(const __grid_const
             coeffs(e + 1, y, dy, Lc, dL, sn);
         }
     }
-    transport_epilogue<D, R, SG, XC>(A, p, w, k1s, colc, gc, valid, Qf, Sc, Sa, Qt);
+    if constexpr (FUSE) {
+        static_assert(D == 2 && XC == 1 && !SG && FD == 0, "fused relaxation: 2D, 33 columns, first order");
+        fused_epilogue2<R, WPB>(A, RA, p, wib, k1s, Qf, Sc, Qt);
+    } else {
+        transport_epilogue<D, R, SG, XC>(A, p, w, k1s, colc, gc, valid, Qf, Sc, Sa, Qt);
+    }
     }
 }
 
@@ -556,18 +664,19 @@ constexpr int stages_for() {
     return n > 8 ? 8 : (n < 2 ? 2 : n);
 }
 
-template <int D, int R, int WPB, bool SG = false, int XC = 0, int FD = 0, int MINB = 1>
-void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s) {
+template <int D, int R, int WPB, bool SG = false, int XC = 0, int FD = 0, int MINB = 1, bool FUSE = false>
+void launch_one(const CUtensorMap& tm, const TArgs& a, cudaStream_t s, const RelaxArgs* ra = nullptr) {
     constexpr int NST = stages_for<D, R, WPB, SG, XC, FD, MINB>();
     constexpr size_t smem = (size_t)WPB * NST * Stage<D, R, SG, XC, FD>::BYTES + WPB * NST * 8;
     static bool configured[kMaxDevices] = {};
     if (first_use_on_device(configured)) {
-        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, XC, FD, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(k_transport<D, R, NST, WPB, SG, XC, FD, MINB, FUSE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
-    const unsigned gx = (unsigned)((a.n_int + WPB - 1) / WPB);
-    const unsigned gy = FD ? 1u : (unsigned)a.nw_grid;
-    k_transport<D, R, NST, WPB, SG, XC, FD, MINB><<<dim3(gx, gy), WPB * 32, smem, s>>>(tm, a);
+    const unsigned gx = FUSE ? (unsigned)a.n_int : (unsigned)((a.n_int + WPB - 1) / WPB);
+    const unsigned gy = (FD || FUSE) ? 1u : (unsigned)a.nw_grid;
+    const RelaxArgs none{};
+    k_transport<D, R, NST, WPB, SG, XC, FD, MINB, FUSE><<<dim3(gx, gy), WPB * 32, smem, s>>>(tm, a, ra ? *ra : none);
 }
 
 template <int D, int R>
@@ -614,6 +723,8 @@ void dispatch(int R, int wpb, const CUtensorMap& tm, const TArgs& a, cudaStream_
         default: launch_wpb<D, 1>(wpb, tm, a, s); break;
     }
 }
+
+constexpr int kFuse2R = 11;                // fused 2D: 3 chunks of 11 rows (n1 = 33)
 
 constexpr int kRChoices3[] = {25, 21, 17, 15, 13, 11, 9, 7, 5, 3, 1};
 constexpr int kRChoices2[] = {17, 13, 11, 9, 7, 5, 3, 1};
@@ -699,8 +810,40 @@ bool make_tensor_maps(bgk_ctx* c) {
     return true;
 }
 
-void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
+static TArgs transport_args(bgk_ctx* c, const double* fin, double* fout);
+
+// 2D, 33 columns, single rank: transport + moments + relaxation in one launch (block = the three
+// 11-row chunks of one particle; 4 blocks = 12 warps per SM)
+void launch_transport_fused(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
     if (c->N_int == 0) return;
+    const TArgs a = transport_args(c, fin, fout);
+    RelaxArgs r{};
+    r.ids = c->interior;
+    r.sums = c->sums;
+    r.f = fout;
+    r.macro = c->macro;
+    r.W = c->W;
+    r.x = c->x;
+    r.err = c->err;
+    r.n = c->N_int;
+    r.n1 = c->n1;
+    r.ncol = c->ncol;
+    r.ncs = c->ncs;
+    r.c0 = c->c0;
+    r.Ks = (int)c->Ks;
+    r.ale = c->cfg.ale;
+    r.vmax = c->cfg.vmax;
+    r.dv = c->dv;
+    r.dt = c->cfg.dt;
+    r.R = c->cfg.R;
+    r.kb = c->cfg.kb;
+    r.dmol = c->cfg.dmol;
+    r.L = c->cfg.L;
+    r.clamp_eps = 1e-3 * c->cfg.dx;
+    launch_one<2, kFuse2R, 3, false, 1, 0, 4, true>(c->tmap[fin == c->f[0] ? 0 : 1], a, s, &r);
+}
+
+static TArgs transport_args(bgk_ctx* c, const double* fin, double* fout) {
     TArgs a;
     a.f = fin;
     a.ft = fout;
@@ -726,6 +869,12 @@ void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t 
     a.xc = c->xc;
     a.ncg_l = c->ncg;
     a.cg_fold = 0;
+    return a;
+}
+
+void launch_transport(bgk_ctx* c, const double* fin, double* fout, cudaStream_t s) {
+    if (c->N_int == 0) return;
+    TArgs a = transport_args(c, fin, fout);
     const CUtensorMap& tm = c->tmap[fin == c->f[0] ? 0 : 1];
     if (c->rows_built && (c->n_rows > 0 || c->n_tiles > 0)) {   // fixed cloud: deep tiles, lattice rows,
         launch_transport_tile(c, fin, fout, s);                   // the general kernel on the rest
