@@ -88,4 +88,22 @@ __device__ inline bool well_conditioned(const double (&A)[n][n]) {
     return hi > 0.0 && lo >= 1e-12 * hi;
 }
 
+// The rank test without the sweeps where it cannot fail: lambda_max <= ||A||_F and 1 / lambda_min =
+// ||A^-1||_2 <= ||A^-1||_F, so ||A||_F ||A^-1||_F <= 1e10 proves lambda_min >= 1e-10 lambda_max -- a
+// factor 100 above the 1e-12 threshold, far beyond the sweeps' rounding, so the decision is the one
+// well_conditioned takes.  Only stencils the bound cannot clear pay for the Jacobi sweeps.
+template <int n>
+__device__ inline bool rank_test(const double (&A)[n][n], const double (&Ai)[n][n]) {
+    double fa = 0.0, fi = 0.0;
+#pragma unroll
+    for (int r = 0; r < n; ++r)
+#pragma unroll
+        for (int q = 0; q < n; ++q) {
+            fa += A[r][q] * A[r][q];
+            fi += Ai[r][q] * Ai[r][q];
+        }
+    if (fa * fi <= 1e20) return true;
+    return well_conditioned<n>(A);
+}
+
 }  // namespace bgk

@@ -117,7 +117,7 @@ __global__ void k_wls_interior(const double* __restrict__ x, const int32_t* __re
     }
     double Si[NU][NU];
     const int m_min = ORDER == 1 ? D + 2 : NU + 1;
-    bool ok = (m >= m_min) && well_conditioned<NU>(A) && small_inverse<NU>(A, Si);
+    bool ok = (m >= m_min) && small_inverse<NU>(A, Si) && rank_test<NU>(A, Si);
     if (!ok) {
         if (lane == 0) latch_error(err, BGK_E_DEFICIENT_STENCIL, p);
         return;
@@ -228,7 +228,7 @@ __global__ void k_wls_boundary(const double* __restrict__ x, const int8_t* __res
 #pragma unroll
         for (int q = 0; q < n; ++q) B[r][q] = warp_sum(B[r][q]);
     double Bi[n][n];
-    const bool ok = (mi >= D + 2) && well_conditioned<n>(B) && small_inverse<n>(B, Bi);
+    const bool ok = (mi >= D + 2) && small_inverse<n>(B, Bi) && rank_test<n>(B, Bi);
     if (!ok) {
         if (lane == 0) {
             latch_error(err, BGK_E_DEFICIENT_STENCIL, b);
