@@ -368,6 +368,18 @@ def test_fixed_cloud_3d_ten_steps(torch_cuda):
     check_state(g, oracle_run(cfg, 10), cfg)
 
 
+def test_fixed_cloud_jittered_no_tiles(torch_cuda):
+    """Tiles and lattice rows need the regular lattice: a jittered fixed cloud runs the general
+    kernel only (transport_info reports neither) and still meets the oracle bar."""
+    cfg = bi.CavityConfig("fixjit", 3, 16, 8, ale=0, jitter=0.2, dt=5e-12)
+    g, _ = gpu(cfg)
+    g.step(5)
+    g.sync()
+    info = g.transport_info()
+    assert info[2] == 0 and info[4] == 0, info
+    check_state(g, oracle_run(cfg, 5), cfg)
+
+
 def test_staged_input_matches_set_f(torch_cuda):
     """bgk_stage_f on a copy stream + bgk_use_staged_f is the same state as bgk_set_f: a
     fixed-cloud run restarted from a staged f^0 reproduces the fresh run bitwise."""
