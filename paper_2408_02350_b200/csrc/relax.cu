@@ -524,8 +524,9 @@ __global__ void __launch_bounds__(256, MINB) k_bnd_interp_t(const int32_t* __res
         mbar_expect_tx(full + s, bytes);
         bulk_load(ring + (size_t)s * CH * NV, f + ((int64_t)sJ[u] * Kloc + c0n) * NV, bytes, full + s);
     };
-    if (tid == 0)
-        for (int u = 0; u < NS && u < U; ++u) issue(u);
+    // rows are issued by parallel threads (one row each): one thread issuing a ring's rows in sequence
+    // holds ~800 cycles per row (tools/probe/bulk_probe.cu)
+    if (tid < NS && tid < U) issue(tid);
     double acc[G][NPT][NV];
 #pragma unroll
     for (int q = 0; q < G; ++q)
@@ -560,8 +561,8 @@ __global__ void __launch_bounds__(256, MINB) k_bnd_interp_t(const int32_t* __res
         }
         if (u % NH == NH - 1 && u + 1 < U) {                  // a half consumed by every warp:
             __syncthreads();                                  // refill it NS rows ahead
-            if (tid == 0)
-                for (int q = u + 1 - NH + NS; q <= u + NS && q < U; ++q) issue(q);
+            const int q = u + 1 - NH + NS + tid;
+            if (tid < NH && q < U) issue(q);
         }
     }
 #pragma unroll
