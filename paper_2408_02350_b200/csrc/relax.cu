@@ -2,13 +2,16 @@
 // motion, diffuse-reflection walls, initial state and diagnostics moments.
 //
 //  k_moment_reduce : per-particle sum of the transport warps' partials (fixed order)
-//  k_relax         : rho, U, T from the (all-reduced) sums,
+//  k_relax(_w2)    : rho, U, T from the (all-reduced) sums,
 //                    tau, M^{n+1} inline as a product of three 1D Gaussian
 //                    factors (P:46-49 / P:98-105 with Z1, Z2),
 //                    f^{n+1} = (tau ftilde + dt M)/(tau + dt),
 //                    W <- U^{n+1}, x += dt U^{n+1} clamped
-//  k_bnd_interp    : incoming half of each boundary row by WLS interpolation of the
-//                    interior f^{n+1} (Z17, Z19) + rank-local incoming wall flux partials
+//  k_bnd_union     : per geometry build, the union of a boundary group's interior neighbours
+//                    and its dense weight matrix (3D: face tiles of <= 16 members; 2D: 4)
+//  k_bnd_interp_s  : 3D incoming half of each boundary row by WLS interpolation of the
+//                    interior f^{n+1} (Z17, Z19) on the FP64 tensor cores + flux partials
+//  k_bnd_interp_t  : the same in 2D (ring-staged union rows, FMA)
 //  k_wall_reduce   : per boundary particle, fixed-order sum of the flux partials
 //  k_bnd_fill      : rho_w = -flux_in / sum_{v.n>0}(v.n) M_w ; outgoing half = rho_w M_w
 #include "async.cuh"
